@@ -1,0 +1,327 @@
+#!/usr/bin/env python
+"""bench.py — throughput of the B200-native CRM SPH particle update (one JSON line on rank 0).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config bed32M] [--impl ours|reference]
+
+A "step" is one full pass of the hot path (SURVEY.md §8(a) A1–A8: bin, sort, reorder, neighbour
+lists, BCE extrapolation x2, fused rates + RK2 epilogues + return map) over the whole workload.
+Default workload: BASELINE.json configs[4], the synthetic 32M-particle granular bed (1024 x 512 x 64
+fluid at d0 = 5 mm, h = 1.3 d0 = 6.5 mm, 2.22M wall markers), the largest configuration that fits one
+GPU.  The state (~2 GB) is larger than L2, so no L2 flush is needed between timed steps.
+
+Timing: W untimed warm-up steps, then K steps bracketed by barrier + cudaStreamSynchronize, timed with
+CUDA events on the library's stream; max over ranks.  Per-kernel device times come from the library's
+own event pairs (crm_profile_*) over the same timed region.  `e2e` re-measures the metric through the
+public C-ABI with pinned host buffers: every step uploads the fluid state (crm_set_state), steps, and
+reads it back (crm_get_state).  `cpu_baseline` times the fp64 oracle (oracle/) on a bounded sample of
+the same workload on the host cores (rank 0, N = 1 only).  `--impl reference` times that oracle as the
+reference arm.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads  # noqa: E402
+
+METRIC = "SPH particle-updates/sec and ms/step at 1/2/4/8 B200; % of HBM roofline"
+UNIT = "particle-updates/s"
+
+# algorithmic work: FP32 flops per directed pair of the rates loop, per
+# neighbour-search candidate, per marker-fluid pair; epilogue flops per fluid particle
+FLOPS_PER_PAIR = 84
+FLOPS_PER_CANDIDATE = 8
+FLOPS_PER_BCE_PAIR = 30
+FLOPS_EPILOGUE = {"k_rates_A": 110, "k_rates_B": 170}
+# algorithmic HBM bytes per fluid particle-update and per BCE marker
+BYTES_PER_FLUID_UPDATE = 404
+BYTES_PER_BCE_UPDATE = 72
+# per-kernel algorithmic bytes per particle (for HBM-bound kernels)
+KERNEL_BYTES = {"k_bin": 16 + 4 + 8 + 4, "k_scatter": 12 + 8, "k_reorder": 56 + 56 + 24 + 8}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return dict(hbm_gbs=d["hbm_gbs"], sm_max_mhz=d.get("sm_max_mhz", 1965.0), source="measured")
+    return dict(hbm_gbs=6650.0, sm_max_mhz=1965.0, source="fallback")
+
+
+def fp32_peak_tflops(mhz):
+    # 148 SMs x 128 FP32 lanes x 2 flops (FFMA) per clock (B200_PROFILING.md unit counts)
+    return 148 * 128 * 2 * mhz * 1e6 / 1e12
+
+
+def scenario(name: str):
+    if name == "bed32M":
+        return workloads.bed()
+    if name.startswith("bed"):
+        nx, ny, nz = (int(t) for t in name[3:].split("x"))
+        return workloads.bed(n=(nx, ny, nz))
+    if name == "block8k":
+        return workloads.block_settle()
+    if name == "cone1M":
+        return workloads.cone_bed()
+    if name == "mgru3":
+        return workloads.mgru3_bin()
+    if name == "crater":
+        return workloads.cratering()
+    raise SystemExit(f"unknown config {name}")
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        rows = []
+        for line in open(self.path):
+            parts = [t.strip() for t in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                rows.append((float(parts[0]), float(parts[1]), parts[3:7]))
+            except ValueError:
+                continue
+        os.unlink(self.path)
+        if not rows:
+            return None
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for _, _, r in rows for k in range(4) if r[k].lower() == "active"})
+        return {"sm_mhz": float(np.median([r[0] for r in rows])), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------------ oracle timing
+def oracle_rate(name: str, steps: int):
+    """Time the fp64 oracle (as it stands) on a bounded sample of the workload."""
+    import oracle
+    oracle.build()
+    if name.startswith("bed"):
+        sample = workloads.bed(n=(64, 64, 64))
+        desc = "64x64x64-fluid sub-bed (262,144 fluid + walls) of the bed recipe (same d0, h, material, dt)"
+    else:
+        sample = scenario(name)
+        desc = f"full {name} workload"
+    s = oracle.load_scenario(sample)
+    t0 = time.perf_counter()
+    s.step(sample.dt, steps)
+    t = time.perf_counter() - t0
+    return dict(value=sample.n_fluid * steps / t, unit=UNIT, cores=oracle.num_threads(), kind="oracle",
+                sample=f"{desc}; {steps} step(s) in {t:.2f} s; {sample.n_fluid + sample.n_bce} particles")
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cb = oracle_rate(args.config, max(1, args.steps + args.warmup) if args.config == "block8k" else 1)
+    # warm-up + timed steps of the oracle itself on the sample (bounded: one sample step per bench step)
+    import oracle
+    sample = workloads.bed(n=(64, 64, 64)) if args.config.startswith("bed") else scenario(args.config)
+    s = oracle.load_scenario(sample)
+    s.step(sample.dt, args.warmup)
+    t0 = time.perf_counter()
+    s.step(sample.dt, args.steps)
+    t = time.perf_counter() - t0
+    val = sample.n_fluid * args.steps / t
+    cb = dict(cb, value=val, sample=cb["sample"].split(";")[0] + f"; {args.steps} timed steps in {t:.2f} s")
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": args.config, "sample_fluid": sample.n_fluid},
+            "cpu_baseline": cb,
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="bed32M")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    assert args.warmup >= 3, "timing rules: at least 3 warm-up steps"
+
+    import torch
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    else:
+        dist = None
+    torch.cuda.set_device(local)
+
+    from paper_2507_05643_b200 import build as _b
+    _b.build_library()
+    from paper_2507_05643_b200 import crm
+
+    sc = scenario(args.config)
+    n_fluid, n_bce = sc.n_fluid, sc.n_bce
+    # replicas: each rank advances its own copy of the workload (slab decomposition: DESIGN.md §Multi-GPU)
+    g = crm.load_scenario(sc, device=local)
+    stream = torch.cuda.ExternalStream(g.stream(), device=local)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    # warm-up
+    g.step(sc.dt, args.warmup)
+    # pair / candidate counts of the current state (algorithmic work of the rates kernels)
+    st = g.structure()
+    counts = st["counts"].astype(np.int64)
+    tags_fluid = np.zeros(n_fluid + n_bce, bool); tags_fluid[:n_fluid] = True
+    pairs_fluid = int(counts[:n_fluid].sum())
+    cs = st["cell_start"].astype(np.int64)
+
+    g.profile(True)
+    g.profile_reset()
+    clk = ClockSampler(local)
+    barrier()
+    torch.cuda.synchronize()
+    clk.start()
+    n0 = g.launch_count()
+    ev0 = torch.cuda.Event(enable_timing=True); ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    g.step(sc.dt, args.steps)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = clk.stop()
+    launches = g.launch_count() - n0
+    ms = ev0.elapsed_time(ev1)
+    prof = g.profile_read()
+    g.profile(False)
+    if dist is not None:
+        t = torch.tensor([ms], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = world * n_fluid / (ms_step * 1e-3)
+
+    pk = peaks()
+    # dominant kernel and its roofline
+    dom = max(prof.items(), key=lambda kv: kv[1][0])
+    dname, (dms, dl) = dom
+    per_launch_s = dms / dl * 1e-3
+    if dname in ("k_rates_A", "k_rates_B"):
+        flops = pairs_fluid * FLOPS_PER_PAIR + n_fluid * FLOPS_EPILOGUE[dname]
+        achieved = flops / per_launch_s / 1e12
+        peak = fp32_peak_tflops(pk["sm_max_mhz"])
+        roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "kernel": dname, "algorithmic_flops_per_launch": flops, "flops_per_pair": FLOPS_PER_PAIR,
+                "peak_note": "148 SM x 128 FP32 lanes x 2 x sm_max_mhz (DESIGN.md §Roofline)"}
+    else:
+        nbytes = (n_fluid + n_bce) * KERNEL_BYTES.get(dname, 56)
+        achieved = nbytes / per_launch_s / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / pk["hbm_gbs"], "kernel": dname}
+    roof["traffic"] = None
+    prof_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof_path):
+        tr = json.load(open(prof_path)).get(args.config, {}).get(dname)
+        if tr is not None:
+            roof["traffic"] = tr
+    roof["peak_source"] = pk["source"]
+    alg_bytes = n_fluid * BYTES_PER_FLUID_UPDATE + n_bce * BYTES_PER_BCE_UPDATE
+    hbm = {"bytes_per_step": alg_bytes, "achieved_gbs": alg_bytes / (ms_step * 1e-3) / 1e9,
+           "peak_gbs": pk["hbm_gbs"], "frac": alg_bytes / (ms_step * 1e-3) / 1e9 / pk["hbm_gbs"]}
+    kernels = {k: {"ms_per_step": v[0] / args.steps, "launches": v[1]} for k, v in sorted(prof.items())}
+
+    # e2e through the public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        n = n_fluid
+        pin = lambda *shape: torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy()  # noqa: E731
+        pos, vel, rho, sig = pin(n, 3), pin(n, 3), pin(n), pin(n, 6)
+        g.get_state(0, n, out=(pos, vel, rho, sig))
+        ke = max(1, args.e2e_steps)
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(ke):
+            g.set_state(0, pos, vel, rho, sig)
+            g.step(sc.dt, 1)
+            g.get_state(0, n, out=(pos, vel, rho, sig))
+        torch.cuda.synchronize()
+        te = time.perf_counter() - t0
+        if dist is not None:
+            t = torch.tensor([te], device=f"cuda:{local}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            te = float(t.item())
+        nbytes = n * 13 * 8
+        e2e = {"value": world * n / (te / ke), "unit": UNIT, "h2d_bytes_per_step": nbytes,
+               "d2h_bytes_per_step": nbytes, "steps": ke,
+               "note": "per step: crm_set_state(all fluid, fp64 pinned) + crm_step(dt,1) + crm_get_state; host wall clock"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = oracle_rate(args.config, 1)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": args.config, "n_fluid": n_fluid, "n_bce": n_bce, "d0": sc.params["d0"],
+                           "h": sc.params["h"], "dt": sc.dt, "pairs_fluid": pairs_fluid,
+                           "particle_updates_incl_bce_per_s": world * (n_fluid + n_bce) / (ms_step * 1e-3),
+                           "l2": "inputs larger than L2 (56 B x N state >> 126 MB), no flush",
+                           "parallelism": f"replica x{world}" if world > 1 else "single GPU"},
+                "roofline": roof, "hbm_roofline": hbm, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": launches, "clocks": clocks}
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,95 @@
+// common.cuh — device-side types shared by the libcrm kernels (sm_100a).
+//
+// Device state layout (HBM, structure of arrays, (cell, id) sorted order):
+//   P  float4 (x, y, z, rho)          positions + density          16 B
+//   U  float4 (u, v, w, tag)          velocity + kind/body tag      16 B
+//   S1 float4 (sxx, syy, szz, sxy)    stress part 1                 16 B
+//   S2 float2 (sxz, syz)              stress part 2                  8 B
+// i.e. 56 B per particle; fluid and BCE markers share the arrays (A8: markers are
+// ordinary neighbours carrying extrapolated u, sigma and rho0).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace crmk {
+
+// tag word stored in U.w (bit pattern, not a float value)
+//   bit 0      : 1 = BCE marker, 0 = fluid
+//   bits 1..15 : body index (0 = static walls)
+//   bit 16     : 1 = the body moves (FREE or PRESCRIBED)
+__host__ __device__ __forceinline__ uint32_t make_tag(uint32_t kind, uint32_t body, uint32_t moving) {
+  return (kind & 1u) | ((body & 0x7fffu) << 1) | ((moving & 1u) << 16);
+}
+__device__ __forceinline__ uint32_t tag_of(float w) { return __float_as_uint(w); }
+__device__ __forceinline__ bool tag_is_bce(uint32_t t) { return t & 1u; }
+__device__ __forceinline__ uint32_t tag_body(uint32_t t) { return (t >> 1) & 0x7fffu; }
+__device__ __forceinline__ bool tag_moving(uint32_t t) { return (t >> 16) & 1u; }
+
+// fixed grid (reading A19); cells of size s = support*h
+struct Grid {
+  float lo[3];
+  float s;                 // (float)(support*h), B1
+  int dims[3];             // Nx, Ny, Nz
+  uint32_t M;              // Nx*Ny*Nz
+  float R2;                // (float)((support*h)^2), B2
+};
+
+// physical constants of one context, fp32
+struct Phys {
+  float h, hinv;
+  float wnorm;             // 1/(pi h^3)  (cubic spline sigma3, A1)
+  float fnorm;             // 1/(pi h^5)  (W'(r)/r prefactor)
+  float R2;                // support radius squared (W = 0 beyond, A17)
+  float m;                 // particle mass rho0 d0^3
+  float rho0;
+  float avc;               // gamma_a h c_s (Eq. 13)
+  float xi2;               // xi^2 (A10)
+  float g[3];              // gravity
+  float K, G;              // elastic moduli (Eq. 3)
+  float mu_s, mu_2, I0, coh, grain_d;   // mu(I) (Eq. muI)
+  int unilateral;          // Eq. 14 switch
+};
+
+// rigid-body kinematics at one instant, used to place markers and extrapolate BCE values
+struct Pose {
+  float pos[3];
+  float R[9];
+  float vel[3], omega[3], acc[3], alpha[3];
+};
+
+// rigid-body state (fp64, device-resident; updated once per step by k_body_update)
+struct BodyState {
+  double mass, inertia[3], pos[3], quat[4], vel[3], omega[3];
+  double acc[3], alpha[3], force[3], torque[3];
+  int motion, dof_mask, pad0, pad1;
+};
+
+// first-error latch (written with atomicCAS on `code`)
+struct ErrLatch {
+  int code;
+  int pad;
+  long long step;
+  long long id;
+  long long aux;
+};
+
+__device__ __forceinline__ void latch_error(ErrLatch* e, int code, long long id, long long step, long long aux) {
+  if (atomicCAS(&e->code, 0, code) == 0) {
+    e->id = id;
+    e->step = step;
+    e->aux = aux;
+  }
+}
+
+// Debug capture buffers (sorted order), written only when armed.
+struct Debug {
+  float* drho[2];
+  float4* acc[2];
+  float4* ds1[2];
+  float2* ds2[2];
+  float4* bu[2];
+  float4* bs1[2];
+  float2* bs2[2];
+};
+
+}  // namespace crmk

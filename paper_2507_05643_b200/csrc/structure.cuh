@@ -1,0 +1,210 @@
+// structure.cuh — cell binning, deterministic counting sort by (cell, id), reorder and
+// neighbour lists (§4.1; rules B1–B5 of DESIGN.md).
+//
+// Per step (ps_freq = 1):
+//   k_bin        hash every particle, count per cell (atomics), remember arrival rank
+//   scan         exclusive scan of the counts -> cellStart (CSR, M+1)
+//   k_scatter    slot = cellStart[c] + arrival  (arrival order is not deterministic)
+//   k_reorder    rank inside the cell by id -> final (cell, id) position; moves the
+//                56-B state with float4/float2 vector loads/stores
+//   k_neighbors  Alg. 1 over the 9 contiguous index runs of the 27-cell stencil, strict
+//                r^2 < (2h)^2 evaluated in fp32 exactly as B2; ELL list k-major
+#pragma once
+#include "common.cuh"
+
+namespace crmk {
+
+// ---------------------------------------------------------------------------------------
+// B1: cell coordinate = floor((x - lo) / s), IEEE fp32 sub + div (no reciprocal multiply)
+__device__ __forceinline__ float b1_floor(float x, float lo, float s) {
+  return floorf(__fdiv_rn(__fsub_rn(x, lo), s));
+}
+
+// B2: dx = xj - xi; r2 = fma(dz,dz, fma(dy,dy, dx*dx)); neighbour iff r2 < R2
+__device__ __forceinline__ bool b2_pred(float xi, float yi, float zi, float xj, float yj, float zj, float R2) {
+  const float dx = __fsub_rn(xj, xi);
+  const float dy = __fsub_rn(yj, yi);
+  const float dz = __fsub_rn(zj, zi);
+  const float r2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
+  return r2 < R2;
+}
+
+// ---------------------------------------------------------------------------------------
+// moving markers: x = p + R x_local at the pose of the step start (body 0 never moves)
+__global__ void k_markers_place(int nm, const uint32_t* __restrict__ moving_ids,
+                                const float4* __restrict__ xlocal, const uint32_t* __restrict__ slot_of_id,
+                                const Pose* __restrict__ pose, float4* __restrict__ P,
+                                const float4* __restrict__ U) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nm) return;
+  const uint32_t id = moving_ids[k];
+  const uint32_t s = slot_of_id[id];
+  const uint32_t b = tag_body(tag_of(U[s].w));
+  const float4 xl = xlocal[k];
+  const Pose& q = pose[b];
+  float4 p = P[s];
+  p.x = q.pos[0] + q.R[0] * xl.x + q.R[1] * xl.y + q.R[2] * xl.z;
+  p.y = q.pos[1] + q.R[3] * xl.x + q.R[4] * xl.y + q.R[5] * xl.z;
+  p.z = q.pos[2] + q.R[6] * xl.x + q.R[7] * xl.y + q.R[8] * xl.z;
+  P[s] = p;
+}
+
+// hash + per-cell count; the error latch reports particles outside the grid
+__global__ void k_bin(int n, const float4* __restrict__ P, const uint32_t* __restrict__ ids, Grid g,
+                      uint32_t* __restrict__ key, uint32_t* __restrict__ arrival,
+                      uint32_t* __restrict__ cell_count, ErrLatch* err, long long step) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float4 p = P[i];
+  float f[3] = {b1_floor(p.x, g.lo[0], g.s), b1_floor(p.y, g.lo[1], g.s), b1_floor(p.z, g.lo[2], g.s)};
+  int c3[3];
+  bool ok = true;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const bool in = (f[a] >= 0.0f) && (f[a] < (float)g.dims[a]);   // false for NaN too
+    ok = ok && in;
+    c3[a] = in ? (int)f[a] : 0;
+  }
+  if (!ok) latch_error(err, -2 /*CRM_E_DOMAIN*/, (long long)ids[i], step, 0);
+  const uint32_t c = (uint32_t)c3[0] * (uint32_t)(g.dims[1] * g.dims[2]) + (uint32_t)c3[1] * (uint32_t)g.dims[2] + (uint32_t)c3[2];
+  key[i] = c;
+  arrival[i] = atomicAdd(&cell_count[c], 1u);
+}
+
+// ---------------------------------------------------------------------------------------
+// exclusive scan of uint32 (tiles of SCAN_BS * SCAN_IPT), recursive over tile sums
+constexpr int SCAN_BS = 512;
+constexpr int SCAN_IPT = 8;
+constexpr int SCAN_TILE = SCAN_BS * SCAN_IPT;
+
+__global__ void __launch_bounds__(SCAN_BS) k_scan_tiles(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+                                                        uint32_t* __restrict__ tile_sums, long long n) {
+  __shared__ uint32_t warp_sums[SCAN_BS / 32];
+  const long long base = (long long)blockIdx.x * SCAN_TILE + (long long)threadIdx.x * SCAN_IPT;
+  uint32_t v[SCAN_IPT];
+  uint32_t sum = 0;
+#pragma unroll
+  for (int k = 0; k < SCAN_IPT; ++k) {
+    v[k] = (base + k < n) ? in[base + k] : 0u;
+    sum += v[k];
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t incl = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) warp_sums[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t w = (lane < SCAN_BS / 32) ? warp_sums[lane] : 0u;
+    uint32_t wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += t;
+    }
+    if (lane < SCAN_BS / 32) warp_sums[lane] = wi - w;   // exclusive warp offsets
+    if (lane == SCAN_BS / 32 - 1) tile_sums[blockIdx.x] = wi;
+  }
+  __syncthreads();
+  uint32_t run = warp_sums[warp] + incl - sum;
+#pragma unroll
+  for (int k = 0; k < SCAN_IPT; ++k) {
+    if (base + k < n) out[base + k] = run;
+    run += v[k];
+  }
+}
+
+__global__ void k_scan_add(uint32_t* __restrict__ out, const uint32_t* __restrict__ tile_off, long long n) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] += tile_off[i / SCAN_TILE];
+}
+
+__global__ void k_copy_u32(uint32_t* dst, const uint32_t* src) { *dst = *src; }
+
+// ---------------------------------------------------------------------------------------
+__global__ void k_scatter(int n, const uint32_t* __restrict__ key, const uint32_t* __restrict__ arrival,
+                          const uint32_t* __restrict__ cell_start, const uint32_t* __restrict__ ids,
+                          uint32_t* __restrict__ tmp_src, uint32_t* __restrict__ tmp_id) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t slot = cell_start[key[i]] + arrival[i];
+  tmp_src[slot] = (uint32_t)i;
+  tmp_id[slot] = ids[i];
+}
+
+// final position = cellStart[c] + #(ids in the cell smaller than mine)  (B4, history-free)
+__global__ void k_reorder(int n, const uint32_t* __restrict__ tmp_src, const uint32_t* __restrict__ tmp_id,
+                          const uint32_t* __restrict__ key, const uint32_t* __restrict__ cell_start,
+                          const float4* __restrict__ P, const float4* __restrict__ U,
+                          const float4* __restrict__ S1, const float2* __restrict__ S2,
+                          float4* __restrict__ Pn, float4* __restrict__ Un, float4* __restrict__ S1n,
+                          float2* __restrict__ S2n, uint32_t* __restrict__ ids_n, uint32_t* __restrict__ cell_of,
+                          uint32_t* __restrict__ slot_of_id) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const uint32_t i = tmp_src[s];
+  const uint32_t myid = tmp_id[s];
+  const uint32_t c = key[i];
+  const uint32_t b = cell_start[c], e = cell_start[c + 1];
+  uint32_t rank = 0;
+  for (uint32_t t = b; t < e; ++t) rank += (tmp_id[t] < myid) ? 1u : 0u;
+  const uint32_t d = b + rank;
+  Pn[d] = P[i];
+  Un[d] = U[i];
+  S1n[d] = S1[i];
+  S2n[d] = S2[i];
+  ids_n[d] = myid;
+  cell_of[d] = c;
+  slot_of_id[myid] = d;
+}
+
+// ---------------------------------------------------------------------------------------
+// Alg. 1 on the sorted state.  With c = cx*(Ny*Nz) + cy*Nz + cz the 27-cell
+// stencil is 9 runs of 3 consecutive cells, i.e. 9 contiguous particle index ranges.
+// Fluid i stores every neighbour; a marker stores only its fluid neighbours (the only ones
+// it uses) unless store_all.  count_all = |P(i)| (fluid + BCE) for the parity check.
+__global__ void __launch_bounds__(256) k_neighbors(int n, Grid g, const float4* __restrict__ P,
+                            const float4* __restrict__ U, const uint32_t* __restrict__ cell_of,
+                            const uint32_t* __restrict__ cell_start, uint32_t* __restrict__ list,
+                            uint32_t* __restrict__ nlist, uint32_t* __restrict__ count_all, int cap,
+                            int store_all, ErrLatch* err, const uint32_t* __restrict__ ids, long long step) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float4 pi = P[i];
+  const bool i_bce = tag_is_bce(tag_of(U[i].w));
+  const uint32_t c = cell_of[i];
+  const int Nz = g.dims[2], Ny = g.dims[1], Nx = g.dims[0];
+  const int cz = (int)(c % (uint32_t)Nz);
+  const int cy = (int)((c / (uint32_t)Nz) % (uint32_t)Ny);
+  const int cx = (int)(c / (uint32_t)(Ny * Nz));
+  const int zlo = max(cz - 1, 0), zhi = min(cz + 1, Nz - 1);
+  uint32_t cnt = 0, k = 0;
+  const size_t stride = (size_t)n;
+  for (int a = -1; a <= 1; ++a) {
+    const int x = cx + a;
+    if (x < 0 || x >= Nx) continue;
+    for (int b = -1; b <= 1; ++b) {
+      const int y = cy + b;
+      if (y < 0 || y >= Ny) continue;
+      const uint32_t base = (uint32_t)x * (uint32_t)(Ny * Nz) + (uint32_t)y * (uint32_t)Nz;
+      const uint32_t jb = cell_start[base + zlo], je = cell_start[base + zhi + 1];
+      for (uint32_t j = jb; j < je; ++j) {
+        if (j == (uint32_t)i) continue;
+        const float4 pj = P[j];
+        if (!b2_pred(pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, g.R2)) continue;
+        ++cnt;
+        if (i_bce && !store_all && tag_is_bce(tag_of(U[j].w))) continue;
+        if (k < (uint32_t)cap) list[(size_t)k * stride + i] = j;
+        ++k;
+      }
+    }
+  }
+  count_all[i] = cnt;
+  nlist[i] = min(k, (uint32_t)cap);
+  if (k > (uint32_t)cap) latch_error(err, -9 /*CRM_E_CAPACITY*/, (long long)ids[i], step, (long long)k);
+}
+
+}  // namespace crmk

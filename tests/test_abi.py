@@ -1,0 +1,86 @@
+"""CPU checks of the boundary: libcrm.so builds for sm_100a, loads, exports every symbol that
+include/crm.h declares, and refuses to run without an sm_100 device (no CPU fallback)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2507_05643_b200 import build
+    build.build_library()
+    from paper_2507_05643_b200 import crm
+    return crm.load_library()
+
+
+def declared_functions():
+    src = open(os.path.join(ROOT, "include", "crm.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(crm_[a-z_]+)\s*\(", src)))
+
+
+def test_header_declares_the_north_star_calls():
+    names = declared_functions()
+    for required in ["crm_create", "crm_add_fluid", "crm_add_bce", "crm_step", "crm_get_state"]:
+        assert required in names
+
+
+def test_library_exports_every_declared_symbol(lib):
+    from paper_2507_05643_b200 import crm
+    names = declared_functions()
+    for nm in names:
+        assert hasattr(lib, nm), nm
+    assert sorted(crm.EXPORTS) == names
+    out = subprocess.run(["nm", "-D", "--defined-only", crm.LIB_PATH], capture_output=True, text=True).stdout
+    for nm in names:
+        assert re.search(rf"\bT {nm}\b", out), nm
+
+
+def test_library_is_sm100a_cubin(lib):
+    from paper_2507_05643_b200 import crm
+    out = subprocess.run(["cuobjdump", "--list-elf", crm.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_strerror_and_kernel_names(lib):
+    from paper_2507_05643_b200 import crm
+    assert lib.crm_strerror(0) == b"ok"
+    assert lib.crm_strerror(-2) == b"particle outside the grid box"
+    names = crm.kernel_names()
+    assert "k_rates_B" in names and "k_neighbors" in names
+
+
+def test_invalid_parameters_rejected_before_device(lib):
+    import workloads
+    from paper_2507_05643_b200 import crm
+    sc = workloads.block_settle(n=(4, 4, 4))
+    p = dict(sc.params, h=sc.params["d0"] * 0.5)      # h < d0
+    with pytest.raises(crm.CrmError) as e:
+        crm.Crm(p)
+    assert e.value.code == crm.CRM_E_INVALID
+    p = dict(sc.params, mu_s=0.9, mu_2=0.5)           # mu_s > mu_2
+    with pytest.raises(crm.CrmError) as e:
+        crm.Crm(p)
+    assert e.value.code == crm.CRM_E_INVALID
+    p = dict(sc.params, ps_freq=10)                   # Alg. 2 persistence: not in this build
+    with pytest.raises(crm.CrmError) as e:
+        crm.Crm(p)
+    assert e.value.code == crm.CRM_E_UNSUPPORTED
+
+
+def test_no_cpu_fallback_without_gpu(lib):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is visible")
+    import workloads
+    from paper_2507_05643_b200 import crm
+    sc = workloads.block_settle(n=(4, 4, 4))
+    with pytest.raises(crm.CrmError) as e:
+        crm.Crm(sc.params)
+    assert e.value.code == crm.CRM_E_CUDA

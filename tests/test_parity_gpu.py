@@ -1,0 +1,235 @@
+"""GPU parity: the CUDA path (libcrm.so, through the C-ABI) against the fp64 oracle on the same
+seeded inputs.  Bars (BASELINE.json north_star):
+  * cell hashes, sorted order, cellStart and neighbour counts/sets: bit-exact;
+  * per-step fp32 rates: relative L-inf <= 1e-4 per field (drho, acc, dsigma);
+  * 100-step macroscopic outputs: within 2 %.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import workloads
+
+pytestmark = pytest.mark.gpu
+
+RATE_TOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def crm():
+    from paper_2507_05643_b200 import build
+    build.build_library()
+    from paper_2507_05643_b200 import crm as m
+    m.load_library()
+    return m
+
+
+def rel_linf(a, b):
+    den = np.abs(b).max()
+    return np.abs(a - b).max() / (den if den > 0 else 1.0)
+
+
+def both(crm, sc, **kw):
+    g = crm.load_scenario(sc, **kw)
+    o = oracle.load_scenario(sc)
+    return g, o
+
+
+def assert_structure_equal(g, o):
+    sg, so = g.structure(), o.structure()
+    assert np.array_equal(sg["cell"], so["cell"])
+    assert np.array_equal(sg["sorted_ids"], so["sorted_ids"])
+    assert np.array_equal(sg["cell_start"], so["cell_start"])
+    assert np.array_equal(sg["counts"], so["counts"])
+    og, lg = g.neighbors()
+    oo, lo = o.neighbors()
+    assert np.array_equal(og, oo) and np.array_equal(lg, lo)
+
+
+# ---------------------------------------------------------------- structure (bit-exact)
+@pytest.mark.parametrize("jitter", [0.0, 0.05])
+def test_structure_block8k(crm, jitter):
+    sc = workloads.block_settle(jitter=jitter, seed=0)
+    g, o = both(crm, sc)
+    assert_structure_equal(g, o)
+    fluid_counts = g.structure()["counts"][: sc.n_fluid]
+    if jitter == 0.0:
+        assert fluid_counts.max() == 80          # interior lattice count at h = 1.3 d0
+
+
+def test_structure_rate_state_S0(crm):
+    sc = workloads.rate_state_S0(workloads.block_settle())
+    g, o = both(crm, sc)
+    assert_structure_equal(g, o)
+
+
+def test_structure_random_clouds(crm):
+    rng = np.random.default_rng(77)
+    for k in range(12):
+        n = int(rng.integers(1, 5000))
+        h = float(rng.uniform(0.01, 0.08))
+        x = workloads.random_cloud(n, seed=500 + k)
+        p = workloads.base_params(rho0=1000.0, mu_s=0.5, mu_2=0.5, I0=0.08, cohesion=0.0, grain_d=1e-3,
+                                  d0=h / 1.3, h=h, visc_mode=0, gamma_a=0.0, lo=(-0.05,) * 3, hi=(1.05,) * 3)
+        sc = workloads.Scenario("cloud", p, x, None, None, np.zeros((0, 3)), [], 1e-5, 1)
+        g, o = both(crm, sc, max_neighbors=1024)
+        assert_structure_equal(g, o)
+
+
+def test_structure_h12_tie_margin(crm):
+    # h = 1.2 d0: the first outside shell is only 2 % beyond 2h; jitter flips pairs
+    sc = workloads.block_settle(jitter=0.02, seed=3)
+    p = dict(sc.params, h=1.2 * sc.params["d0"])
+    sc = workloads.Scenario("b12", p, sc.fluid_pos, None, None, sc.wall_pos, [], sc.dt, 1)
+    g, o = both(crm, sc)
+    assert_structure_equal(g, o)
+
+
+# ---------------------------------------------------------------- rates (1e-4)
+def run_one_armed(crm, sc, dt):
+    g, o = both(crm, sc)
+    g.debug_arm(True)
+    g.step(dt, 1)
+    o.step(dt, 1)
+    return g, o
+
+
+@pytest.mark.parametrize("visc", [workloads.VISC_BILATERAL, workloads.VISC_UNILATERAL])
+def test_rates_stage_A_and_B_S0(crm, visc):
+    sc = workloads.rate_state_S0(workloads.block_settle())
+    sc.params["visc_mode"] = visc
+    sc.params["gamma_a"] = 0.2
+    g, o = run_one_armed(crm, sc, sc.dt)
+    nf = sc.n_fluid
+    for stage in (0, 1):
+        dg, ag, sg = g.last_rates(stage)
+        do, ao, so = o.last_rates(stage)
+        assert rel_linf(dg[:nf], do[:nf]) <= RATE_TOL, ("drho", stage)
+        assert rel_linf(ag[:nf], ao[:nf]) <= RATE_TOL, ("acc", stage)
+        assert rel_linf(sg[:nf], so[:nf]) <= RATE_TOL, ("dsig", stage)
+        ug, tg = g.last_bce(stage)
+        uo, to = o.last_bce(stage)
+        assert rel_linf(ug[nf:], uo[nf:]) <= RATE_TOL, ("bce u", stage)
+        assert rel_linf(tg[nf:], to[nf:]) <= RATE_TOL, ("bce sigma", stage)
+
+
+def test_one_step_state_S0_confined(crm):
+    sc = workloads.rate_state_S0(workloads.block_settle())
+    sc.fluid_sig = workloads.f32(sc.fluid_sig + np.array([-2000.0, -2000.0, -2000.0, 0, 0, 0]))
+    g, o = run_one_armed(crm, sc, sc.dt)
+    nf = sc.n_fluid
+    x0, u0, r0, s0 = sc.fluid_pos, sc.fluid_vel, np.full(nf, sc.params["rho0"]), sc.fluid_sig
+    xg, ug, rg, sg = [a[:nf] for a in g.get_state()]
+    xo, uo, ro, so = [a[:nf] for a in o.get_state()]
+    assert np.abs(xg - xo).max() <= 1e-6 * sc.params["d0"] + 2e-9
+    assert rel_linf(ug - u0, uo - u0) <= 1e-3
+    assert rel_linf(rg - r0, ro - r0) <= 1e-3
+    assert rel_linf(sg - s0, so - s0) <= 1e-3
+
+
+def test_rates_settling_block_bilateral(crm):
+    sc = workloads.block_settle(jitter=0.05)
+    g, o = both(crm, sc)
+    g.step(sc.dt, 3)
+    o.step(sc.dt, 3)
+    # continue from each side's own state; compare the 4th step's rates
+    g.debug_arm(True)
+    g.step(sc.dt, 1)
+    o.step(sc.dt, 1)
+    nf = sc.n_fluid
+    da, aa, sa = g.last_rates(0)
+    db, ab, sb = o.last_rates(0)
+    assert rel_linf(aa[:nf], ab[:nf]) <= 1e-3
+    assert rel_linf(da[:nf], db[:nf]) <= 1e-3
+
+
+# ---------------------------------------------------------------- macroscopic (2 %)
+def settled_height(pos, ids_top, d0):
+    return pos[ids_top, 2].mean() + 0.5 * d0
+
+
+def test_block_100_steps_macroscopic(crm):
+    sc = workloads.block_settle()
+    g, o = both(crm, sc)
+    g.step(sc.dt, 100)
+    o.step(sc.dt, 100)
+    nf = sc.n_fluid
+    top = np.argsort(sc.fluid_pos[:, 2])[-400:]
+    xg = g.get_state()[0][:nf]
+    xo = o.get_state()[0][:nf]
+    hg, ho = settled_height(xg, top, sc.params["d0"]), settled_height(xo, top, sc.params["d0"])
+    assert abs(hg - ho) <= 0.02 * ho
+    # the two trajectories stay close particle by particle too
+    assert np.abs(xg - xo).max() < 0.02 * sc.params["d0"]
+
+
+def test_determinism_bit_identical(crm):
+    sc = workloads.block_settle(jitter=0.05)
+    a = crm.load_scenario(sc)
+    b = crm.load_scenario(sc)
+    a.step(sc.dt, 20)
+    b.step(sc.dt, 20)
+    for x, y in zip(a.get_state(), b.get_state()):
+        assert np.array_equal(x, y)
+
+
+# ---------------------------------------------------------------- edge cases
+def test_single_particle_ballistic(crm):
+    p = workloads.base_params(rho0=1500.0, mu_s=0.5, mu_2=0.5, I0=0.08, cohesion=0.0, grain_d=1e-3, d0=0.01,
+                              h=0.013, visc_mode=0, gamma_a=0.1, lo=(-1, -1, -1), hi=(1, 1, 1),
+                              gravity=(0.1, -0.2, -9.81))
+    g = crm.Crm(p)
+    g.add_fluid(np.array([[0.1, 0.2, 0.3]]), np.array([[0.5, -0.3, 1.0]]))
+    dt = 1e-3
+    g.step(dt, 1)
+    x, u, rho, s = g.get_state()
+    gg = np.array(p["gravity"])
+    assert np.allclose(x[0], [0.1, 0.2, 0.3] + dt * np.array([0.5, -0.3, 1.0]) + 0.5 * dt * dt * gg, atol=1e-6)
+    assert np.allclose(u[0], [0.5, -0.3, 1.0] + dt * gg, atol=1e-6)
+
+
+def test_domain_error_names_particle(crm):
+    sc = workloads.block_settle(n=(6, 6, 6))
+    sc.fluid_pos[7] = [10.0, 0.0, 0.0]
+    g = crm.load_scenario(sc)
+    with pytest.raises(crm.CrmError) as e:
+        g.step(sc.dt, 1)
+    assert e.value.code == crm.CRM_E_DOMAIN and "id 7" in str(e.value)
+
+
+def test_capacity_error(crm):
+    sc = workloads.block_settle(n=(6, 6, 6))
+    g = crm.load_scenario(sc, max_neighbors=16)
+    with pytest.raises(crm.CrmError) as e:
+        g.step(sc.dt, 1)
+    assert e.value.code == crm.CRM_E_CAPACITY
+
+
+def test_nonfinite_error(crm):
+    sc = workloads.block_settle(n=(6, 6, 6))
+    sc.fluid_vel = np.zeros_like(sc.fluid_pos)
+    sc.fluid_vel[11] = [np.inf, 0, 0]
+    g = crm.load_scenario(sc)
+    with pytest.raises(crm.CrmError) as e:
+        g.step(sc.dt, 1)
+    assert e.value.code in (crm.CRM_E_NONFINITE, crm.CRM_E_DOMAIN)
+
+
+def test_add_after_step_rejected(crm):
+    sc = workloads.block_settle(n=(4, 4, 4))
+    g = crm.load_scenario(sc)
+    g.step(sc.dt, 1)
+    with pytest.raises(crm.CrmError) as e:
+        g.add_fluid(np.zeros((1, 3)))
+    assert e.value.code == crm.CRM_E_STATE
+
+
+def test_get_set_state_roundtrip(crm):
+    sc = workloads.rate_state_S0(workloads.block_settle(n=(8, 8, 8)))
+    g = crm.load_scenario(sc)
+    g.step(sc.dt, 2)
+    st = g.get_state()
+    g2 = crm.load_scenario(sc)
+    g2.set_state(0, *st)
+    for x, y in zip(g2.get_state(), st):
+        assert np.array_equal(x, y)
