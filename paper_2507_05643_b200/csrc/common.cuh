@@ -48,7 +48,24 @@ struct Phys {
   float K, G;              // elastic moduli (Eq. 3)
   float mu_s, mu_2, I0, coh, grain_d;   // mu(I) (Eq. muI)
   int unilateral;          // Eq. 14 switch
+  // folded constants of the pair loop
+  float kin_a;             // 2.25 fnorm / h      : W'/r = kin_a r + kin_b          (q < 1)
+  float kin_b;             // -3 fnorm
+  float kout;              // -0.75 h fnorm       : W'/r = kout (2 - q)^2 / r       (1 <= q < 2)
+  float c_av;              // 2 m gamma_a h c_s   : AV coefficient numerator (Eq. 13)
 };
+
+// MUFU approximations (no IEEE/denormal wrappers): max rel. error ~2^-22 (rsqrt, rcp)
+__device__ __forceinline__ float rsqrt_approx(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 
 // rigid-body kinematics at one instant, used to place markers and extrapolate BCE values
 struct Pose {

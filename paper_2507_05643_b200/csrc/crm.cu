@@ -2,7 +2,8 @@
 //
 // One crm_step(dt, n) issues, per step, on the context's stream:
 //   memset counts | k_bin | scan (k_scan_tiles, k_scan_add) | k_scatter | k_reorder |
-//   k_neighbors | k_bce(A) | k_rates<0> | [k_markers_place(mid)] | k_bce(B) | k_rates<1> |
+//   k_bce_t<0> (marker filter + extrapolation) | k_rates_t<0> (fluid filter + rates + half step) |
+//   [k_markers_place(mid)] | k_bce_t<1> | k_rates_t<1> (rates + full step + return map) |
 //   [k_body_update | k_body_poses | k_markers_place]
 // and synchronises once at the end to read the device error latch.  The step sequence can
 // be captured once in a CUDA graph per (dt, buffer parity) and replayed.
@@ -19,18 +20,21 @@
 #include "common.cuh"
 #include "physics.cuh"
 #include "structure.cuh"
+#include "tiled.cuh"
 
 using namespace crmk;
 
 namespace {
 
 enum KernelId {
-  KID_MARKERS = 0, KID_BIN, KID_SCAN, KID_SCAN_ADD, KID_SCATTER, KID_REORDER, KID_NEIGHBORS,
-  KID_BCE, KID_RATES_A, KID_RATES_B, KID_BODY, KID_POSES, KID_STATE, KID_COPY, KID_COUNT
+  KID_MARKERS = 0, KID_BIN, KID_SCAN, KID_SCAN_ADD, KID_SCATTER, KID_REORDER,
+  KID_BCE_A, KID_RATES_A, KID_BCE_B, KID_RATES_B, KID_BODY, KID_POSES, KID_STATE, KID_COPY, KID_DECODE,
+  KID_COUNT
 };
 const char* kKernelNames[KID_COUNT] = {"k_markers_place", "k_bin", "k_scan_tiles", "k_scan_add", "k_scatter",
-                                       "k_reorder", "k_neighbors", "k_bce", "k_rates_A", "k_rates_B",
-                                       "k_body_update", "k_body_poses", "k_get_set_state", "k_copy_u32"};
+                                       "k_reorder", "k_bce_A", "k_rates_A", "k_bce_B", "k_rates_B",
+                                       "k_body_update", "k_body_poses", "k_get_set_state", "k_copy_u32",
+                                       "k_decode_lists"};
 
 struct ProfRec {
   int kid;
@@ -69,7 +73,11 @@ struct crm {
   float2* S2m = nullptr;
   uint32_t *key = nullptr, *arrival = nullptr, *cell_count = nullptr, *cell_start = nullptr;
   uint32_t *tmp_src = nullptr, *tmp_id = nullptr, *cell_of = nullptr, *slot_of_id = nullptr;
-  uint32_t *list = nullptr, *nlist = nullptr, *count_all = nullptr;
+  uint16_t* list = nullptr;             // hot-path lists: window offsets, cap per particle
+  uint32_t *nlist = nullptr, *count_all = nullptr;
+  uint32_t* list32 = nullptr;           // debug only: global indices, ELL k-major
+  long long ntiles = 0;
+  bool attrs_set = false;
   std::vector<uint32_t*> scan_sums, scan_sums_x;
   std::vector<long long> scan_len;
   BodyState* d_bodies = nullptr;
@@ -167,6 +175,24 @@ void launch(crm_t* c, int kid, Kern kern, dim3 grid, dim3 block, Args... args) {
   }
 }
 
+template <typename Kern, typename... Args>
+void launch_smem(crm_t* c, int kid, Kern kern, dim3 grid, dim3 block, size_t smem, Args... args) {
+  if (grid.x == 0) return;
+  cudaEvent_t a = nullptr, b = nullptr;
+  if (c->prof) {
+    a = get_event(c);
+    cudaEventRecord(a, c->stream);
+  }
+  kern<<<grid, block, smem, c->stream>>>(args...);
+  c->launches++;
+  if (c->prof) {
+    b = get_event(c);
+    cudaEventRecord(b, c->stream);
+    c->recs.push_back({kid, a, b});
+    if (c->recs.size() > 4096) prof_flush(c);
+  }
+}
+
 inline float u2f(uint32_t u) {
   float f;
   std::memcpy(&f, &u, 4);
@@ -216,6 +242,8 @@ int alloc_debug(crm_t* c) {
   return r ? CRM_E_OOM : CRM_OK;
 }
 
+void set_attrs(crm_t* c);
+
 int commit(crm_t* c) {
   if (c->committed) return CRM_OK;
   if (c->n <= 0) return fail(c, CRM_E_STATE, "no particles added");
@@ -232,6 +260,7 @@ int commit(crm_t* c) {
   r |= dalloc(c, &c->tmp_src, n); r |= dalloc(c, &c->tmp_id, n); r |= dalloc(c, &c->cell_of, n);
   r |= dalloc(c, &c->slot_of_id, n);
   r |= dalloc(c, &c->list, n * (size_t)c->cap); r |= dalloc(c, &c->nlist, n); r |= dalloc(c, &c->count_all, n);
+  c->ntiles = num_tiles(c->grid);
   r |= dalloc(c, &c->d_err, 1);
   r |= dalloc(c, &c->d_step, 1);
   if (r) return CRM_E_OOM;
@@ -299,13 +328,14 @@ int commit(crm_t* c) {
   CK(cudaStreamSynchronize(c->stream));
   c->cur = 0;
   c->committed = true;
+  set_attrs(c);
   c->hP.clear(); c->hP.shrink_to_fit(); c->hU.clear(); c->hU.shrink_to_fit();
   c->hS1.clear(); c->hS1.shrink_to_fit(); c->hS2.clear(); c->hS2.shrink_to_fit();
   return CRM_OK;
 }
 
-// structural phase of a step on the current state: bin, sort, reorder, neighbour lists
-void issue_structure(crm_t* c, int store_all, long long step) {
+// sort phase of a step on the current state: bin, scan, scatter, reorder
+void issue_sort(crm_t* c, long long step) {
   const int n = (int)c->n;
   const int a = c->cur, b = 1 - c->cur;
   cudaMemsetAsync(c->cell_count, 0, (size_t)c->grid.M * 4, c->stream);
@@ -319,37 +349,57 @@ void issue_structure(crm_t* c, int store_all, long long step) {
          (const float4*)c->P[a], (const float4*)c->U[a], (const float4*)c->S1[a], (const float2*)c->S2[a],
          c->P[b], c->U[b], c->S1[b], c->S2[b], c->ids[b], c->cell_of, c->slot_of_id);
   c->cur = b;
-  launch(c, KID_NEIGHBORS, k_neighbors, dim3(blocks(n, 256)), dim3(256), n, c->grid, (const float4*)c->P[b],
-         (const float4*)c->U[b], (const uint32_t*)c->cell_of, (const uint32_t*)c->cell_start, c->list, c->nlist,
-         c->count_all, c->cap, store_all, c->d_err, (const uint32_t*)c->ids[b], step);
+}
+
+void set_attrs(crm_t* c) {
+  if (c->attrs_set) return;
+  const int sm = (int)sizeof(TileSmem);
+  cudaFuncSetAttribute(k_bce_t<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  cudaFuncSetAttribute(k_bce_t<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  cudaFuncSetAttribute(k_rates_t<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  cudaFuncSetAttribute(k_rates_t<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  c->attrs_set = true;
+}
+
+// stage A (filter + BCE + rates at y_n -> y_mid); store_all keeps marker-marker pairs (debug)
+void issue_stage_a(crm_t* c, float dt, long long step, int store_all) {
+  const int y = c->cur;
+  const int dbg = c->dbg_on ? 1 : 0;
+  const dim3 tg((unsigned)c->ntiles), tb(TILE_THREADS);
+  const size_t sm = sizeof(TileSmem);
+  if (c->n_bce)
+    launch_smem(c, KID_BCE_A, k_bce_t<0>, tg, tb, sm, c->grid, c->ph, (const uint32_t*)c->cell_start,
+                (const float4*)c->P[y], c->U[y], c->S1[y], c->S2[y], c->list, c->nlist, c->count_all,
+                (const uint32_t*)c->cell_of, (const Pose*)c->d_pose0, c->cap, store_all, c->dbg, dbg, c->d_err,
+                (const uint32_t*)c->ids[y], step);
+  launch_smem(c, KID_RATES_A, k_rates_t<0>, tg, tb, sm, c->grid, c->ph, dt, (const uint32_t*)c->cell_start,
+              (const float4*)c->P[y], (const float4*)c->U[y], (const float4*)c->S1[y], (const float2*)c->S2[y], c->Pm,
+              c->Um, c->S1m, c->S2m, c->list, c->nlist, c->count_all, (const uint32_t*)c->cell_of, c->cap, c->macc,
+              c->dbg, dbg, c->d_err, (const uint32_t*)c->ids[y], step);
 }
 
 // one RK2 step (everything on the stream, no host sync)
 void issue_step(crm_t* c, float dt, long long step) {
-  const int n = (int)c->n;
-  issue_structure(c, 0, step);
+  issue_sort(c, step);
+  issue_stage_a(c, dt, step, 0);
   const int y = c->cur;
   const int dbg = c->dbg_on ? 1 : 0;
-  // ---- stage A at y_n
-  if (c->n_bce)
-    launch(c, KID_BCE, k_bce, dim3(blocks(n, 256)), dim3(256), n, c->ph, (const float4*)c->P[y], c->U[y], c->S1[y],
-           c->S2[y], (const uint32_t*)c->list, (const uint32_t*)c->nlist, (const Pose*)c->d_pose0, c->dbg, 0, dbg);
-  launch(c, KID_RATES_A, k_rates<0>, dim3(blocks(n, 256)), dim3(256), n, c->ph, dt, (const float4*)c->P[y],
-         (const float4*)c->U[y], (const float4*)c->S1[y], (const float2*)c->S2[y], c->Pm, c->Um, c->S1m, c->S2m,
-         (const uint32_t*)c->list, (const uint32_t*)c->nlist, c->macc, c->dbg, dbg, c->d_err,
-         (const uint32_t*)c->ids[y], step);
+  const dim3 tg((unsigned)c->ntiles), tb(TILE_THREADS);
+  const size_t sm = sizeof(TileSmem);
   if (c->n_moving_markers)
     launch(c, KID_MARKERS, k_markers_place, dim3(blocks(c->n_moving_markers, 128)), dim3(128), c->n_moving_markers,
            (const uint32_t*)c->d_moving_ids, (const float4*)c->d_xlocal, (const uint32_t*)c->slot_of_id,
            (const Pose*)c->d_posem, c->Pm, (const float4*)c->Um);
   // ---- stage B at y_mid, same lists
   if (c->n_bce)
-    launch(c, KID_BCE, k_bce, dim3(blocks(n, 256)), dim3(256), n, c->ph, (const float4*)c->Pm, c->Um, c->S1m, c->S2m,
-           (const uint32_t*)c->list, (const uint32_t*)c->nlist, (const Pose*)c->d_posem, c->dbg, 1, dbg);
-  launch(c, KID_RATES_B, k_rates<1>, dim3(blocks(n, 256)), dim3(256), n, c->ph, dt, (const float4*)c->Pm,
-         (const float4*)c->Um, (const float4*)c->S1m, (const float2*)c->S2m, c->P[y], c->U[y], c->S1[y], c->S2[y],
-         (const uint32_t*)c->list, (const uint32_t*)c->nlist, c->macc, c->dbg, dbg, c->d_err,
-         (const uint32_t*)c->ids[y], step);
+    launch_smem(c, KID_BCE_B, k_bce_t<1>, tg, tb, sm, c->grid, c->ph, (const uint32_t*)c->cell_start,
+                (const float4*)c->Pm, c->Um, c->S1m, c->S2m, c->list, c->nlist, c->count_all,
+                (const uint32_t*)c->cell_of, (const Pose*)c->d_posem, c->cap, 0, c->dbg, dbg, c->d_err,
+                (const uint32_t*)c->ids[y], step);
+  launch_smem(c, KID_RATES_B, k_rates_t<1>, tg, tb, sm, c->grid, c->ph, dt, (const uint32_t*)c->cell_start,
+              (const float4*)c->Pm, (const float4*)c->Um, (const float4*)c->S1m, (const float2*)c->S2m, c->P[y],
+              c->U[y], c->S1[y], c->S2[y], c->list, c->nlist, c->count_all, (const uint32_t*)c->cell_of, c->cap,
+              c->macc, c->dbg, dbg, c->d_err, (const uint32_t*)c->ids[y], step);
   // ---- bodies
   if (c->n_moving_bodies) {
     launch(c, KID_BODY, k_body_update, dim3(c->n_moving_bodies), dim3(BODY_BS), (const int*)c->d_moving_bodies,
@@ -361,7 +411,7 @@ void issue_step(crm_t* c, float dt, long long step) {
            (const uint32_t*)c->d_moving_ids, (const float4*)c->d_xlocal, (const uint32_t*)c->slot_of_id,
            (const Pose*)c->d_pose0, c->P[y], (const float4*)c->U[y]);
   }
-  if (dbg) cudaMemcpyAsync(c->dbg_ids, c->ids[y], (size_t)n * 4, cudaMemcpyDeviceToDevice, c->stream);
+  if (dbg) cudaMemcpyAsync(c->dbg_ids, c->ids[y], (size_t)c->n * 4, cudaMemcpyDeviceToDevice, c->stream);
 }
 
 int read_latch(crm_t* c) {
@@ -479,6 +529,13 @@ int crm_create(const crm_material_t* mat, const crm_kernel_t* ker, const crm_bou
   c->ph.coh = (float)m.cohesion;
   c->ph.grain_d = (float)m.grain_d;
   c->ph.unilateral = k.visc_mode == CRM_VISC_UNILATERAL;
+  {
+    const double fnorm = 1.0 / (M_PI * h * h * h * h * h);
+    c->ph.kin_a = (float)(2.25 * fnorm / h);
+    c->ph.kin_b = (float)(-3.0 * fnorm);
+    c->ph.kout = (float)(-0.75 * h * fnorm);
+    c->ph.c_av = (float)(2.0 * m.rho0 * k.d0 * k.d0 * k.d0 * k.gamma_a * h * cs);
+  }
   // neighbour capacity: twice the lattice count of the 2h ball, rounded up to 32
   if (k.max_neighbors > 0) {
     c->cap = k.max_neighbors;
@@ -532,7 +589,7 @@ void crm_destroy(crm_t* c) {
   cudaFree(c->Pm); cudaFree(c->Um); cudaFree(c->S1m); cudaFree(c->S2m);
   cudaFree(c->key); cudaFree(c->arrival); cudaFree(c->cell_count); cudaFree(c->cell_start);
   cudaFree(c->tmp_src); cudaFree(c->tmp_id); cudaFree(c->cell_of); cudaFree(c->slot_of_id);
-  cudaFree(c->list); cudaFree(c->nlist); cudaFree(c->count_all);
+  cudaFree(c->list); cudaFree(c->nlist); cudaFree(c->count_all); cudaFree(c->list32);
   for (auto p : c->scan_sums) cudaFree(p);
   for (auto p : c->scan_sums_x) cudaFree(p);
   cudaFree(c->d_bodies); cudaFree(c->d_pose0); cudaFree(c->d_posem);
@@ -778,7 +835,8 @@ int crm_debug_structure(crm_t* c, uint32_t* cell_by_id, int64_t* sorted_ids, uin
   if (r) return r;
   if (n_cells) *n_cells = c->grid.M;
   if (!cell_by_id && !sorted_ids && !nbr_count_by_id && !cell_start) return CRM_OK;
-  issue_structure(c, 0, c->steps_done);
+  issue_sort(c, c->steps_done);
+  issue_stage_a(c, 0.0f, c->steps_done, 0);
   r = read_latch(c);
   if (r) return r;
   const size_t n = (size_t)c->n;
@@ -800,10 +858,15 @@ int crm_debug_neighbors(crm_t* c, int64_t* offsets, int64_t* list) {
   cudaSetDevice(c->device);
   int r = commit(c);
   if (r) return r;
-  issue_structure(c, 1, c->steps_done);
+  issue_sort(c, c->steps_done);
+  issue_stage_a(c, 0.0f, c->steps_done, 1);
+  const size_t n = (size_t)c->n;
+  if (!c->list32 && dalloc(c, &c->list32, n * (size_t)c->cap)) return CRM_E_OOM;
+  launch(c, KID_DECODE, k_decode_lists, dim3(blocks((long long)n, 256)), dim3(256), (int)n, c->grid,
+         (const uint32_t*)c->cell_start, (const uint32_t*)c->cell_of, (const uint16_t*)c->list,
+         (const uint32_t*)c->nlist, c->cap, c->list32);
   r = read_latch(c);
   if (r) return r;
-  const size_t n = (size_t)c->n;
   std::vector<uint32_t> ids(n), nl(n);
   CK(cudaMemcpy(ids.data(), c->ids[c->cur], n * 4, cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(nl.data(), c->nlist, n * 4, cudaMemcpyDeviceToHost));
@@ -813,7 +876,7 @@ int crm_debug_neighbors(crm_t* c, int64_t* offsets, int64_t* list) {
   for (size_t i = 0; i < n; ++i) offsets[i + 1] = offsets[i] + cnt_by_id[i];
   if (!list) return CRM_OK;
   std::vector<uint32_t> L(n * (size_t)c->cap);
-  CK(cudaMemcpy(L.data(), c->list, L.size() * 4, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(L.data(), c->list32, L.size() * 4, cudaMemcpyDeviceToHost));
   for (size_t s = 0; s < n; ++s) {
     const uint32_t id = ids[s];
     int64_t* row = list + offsets[id];

@@ -83,62 +83,6 @@ __device__ __forceinline__ float kernel_F(float r2, const Phys& ph) {
 }
 
 // ------------------------------------------------------------------------------------
-// Adami extrapolation for every marker of the stage state (in place on the marker slots)
-__global__ void __launch_bounds__(256) k_bce(int n, Phys ph, const float4* __restrict__ P, float4* __restrict__ U,
-                                             float4* __restrict__ S1, float2* __restrict__ S2,
-                                             const uint32_t* __restrict__ list, const uint32_t* __restrict__ nlist,
-                                             const Pose* __restrict__ pose, Debug dbg, int stage, int dbg_on) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const float4 ui = U[i];
-  const uint32_t tag = tag_of(ui.w);
-  if (!tag_is_bce(tag)) return;
-  const float4 pa = P[i];
-  float ub[3] = {0.f, 0.f, 0.f}, ab[3] = {0.f, 0.f, 0.f};
-  if (tag_moving(tag)) body_kinematics(pose[tag_body(tag)], pa.x, pa.y, pa.z, ub, ab);
-  const float ga[3] = {ph.g[0] - ab[0], ph.g[1] - ab[1], ph.g[2] - ab[2]};
-  float SW = 0.f, su[3] = {0.f, 0.f, 0.f}, ss[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, sh = 0.f;
-  const int nl = (int)nlist[i];
-  for (int k = 0; k < nl; ++k) {
-    const uint32_t j = list[(size_t)k * n + i];
-    const float4 pf = P[j];
-    const float dx = pa.x - pf.x, dy = pa.y - pf.y, dz = pa.z - pf.z;
-    const float r2 = dx * dx + dy * dy + dz * dz;
-    if (r2 >= ph.R2) continue;
-    const float W = kernel_W(r2, ph);
-    const float4 uf = U[j];
-    const float4 s1 = S1[j];
-    const float2 s2 = S2[j];
-    SW += W;
-    su[0] += uf.x * W; su[1] += uf.y * W; su[2] += uf.z * W;
-    ss[0] += s1.x * W; ss[1] += s1.y * W; ss[2] += s1.z * W;
-    ss[3] += s1.w * W; ss[4] += s2.x * W; ss[5] += s2.y * W;
-    sh += pf.w * (ga[0] * dx + ga[1] * dy + ga[2] * dz) * W;
-  }
-  float4 uo, s1o;
-  float2 s2o;
-  if (SW > 0.f) {
-    const float inv = 1.0f / SW;
-    uo = make_float4(2.f * ub[0] - su[0] * inv, 2.f * ub[1] - su[1] * inv, 2.f * ub[2] - su[2] * inv, ui.w);
-    const float hyd = sh * inv;
-    s1o = make_float4(ss[0] * inv - hyd, ss[1] * inv - hyd, ss[2] * inv - hyd, ss[3] * inv);
-    s2o = make_float2(ss[4] * inv, ss[5] * inv);
-  } else {   // A11
-    uo = make_float4(ub[0], ub[1], ub[2], ui.w);
-    s1o = make_float4(0.f, 0.f, 0.f, 0.f);
-    s2o = make_float2(0.f, 0.f);
-  }
-  U[i] = uo;
-  S1[i] = s1o;
-  S2[i] = s2o;
-  if (dbg_on) {
-    dbg.bu[stage][i] = uo;
-    dbg.bs1[stage][i] = s1o;
-    dbg.bs2[stage][i] = s2o;
-  }
-}
-
-// ------------------------------------------------------------------------------------
 // mu(I) return map in fp32; readings A16 (gamma_dot >= 0, p floor 1 Pa for I
 // only, I = 0 -> mu_s), A27 (tau_max >= 0).  s, sn = (xx,yy,zz,xy,xz,yz)
 __device__ __forceinline__ void return_map(float s[6], const float sn[6], const Phys& ph, float dt) {
@@ -162,140 +106,6 @@ __device__ __forceinline__ void return_map(float s[6], const float sn[6], const 
   const float sc = tmax / tb;                                             // Step 4
   s[0] = sc * t0 - p; s[1] = sc * t1 - p; s[2] = sc * t2 - p;
   s[3] *= sc; s[4] *= sc; s[5] *= sc;
-}
-
-// Fused pair loop + epilogue.  STAGE 0: (P,U,S) = y_n, writes y_mid into (YP,YU,YS).
-// STAGE 1: (P,U,S) = y_mid, (YP,YU,YS) = y_n in, y_{n+1} out (own slot only; neighbours are
-// read from y_mid, so the in-place update is race-free).
-template <int STAGE>
-__global__ void __launch_bounds__(256) k_rates(int n, Phys ph, float dt,
-                                               const float4* __restrict__ P, const float4* __restrict__ U,
-                                               const float4* __restrict__ S1, const float2* __restrict__ S2,
-                                               float4* __restrict__ YP, float4* __restrict__ YU,
-                                               float4* __restrict__ YS1, float2* __restrict__ YS2,
-                                               const uint32_t* __restrict__ list, const uint32_t* __restrict__ nlist,
-                                               float4* __restrict__ macc, Debug dbg, int dbg_on,
-                                               ErrLatch* err, const uint32_t* __restrict__ ids, long long step) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const float4 pi = P[i];
-  const float4 ui = U[i];
-  const uint32_t tag = tag_of(ui.w);
-  const bool bce = tag_is_bce(tag);
-  if (bce) {
-    if (STAGE == 0) {
-      YP[i] = pi;
-      YU[i] = ui;   // carries the tag; u, sigma are replaced by the stage-B extrapolation
-    } else {
-      YU[i] = ui;   // y_{n+1} of a marker: its last (stage-B) extrapolated u and sigma
-      YS1[i] = S1[i];
-      YS2[i] = S2[i];
-      if (!tag_moving(tag)) return;
-    }
-    if (STAGE == 0) return;
-  }
-  const float4 si1 = S1[i];
-  const float2 si2 = S2[i];
-  float L[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  float Gs[3] = {0.f, 0.f, 0.f}, Ms[3] = {0.f, 0.f, 0.f}, Pi[3] = {0.f, 0.f, 0.f};
-  const float two_m = 2.0f * ph.m;
-  const int nl = (int)nlist[i];
-  for (int k = 0; k < nl; ++k) {
-    const uint32_t j = list[(size_t)k * n + i];
-    const float4 pj = P[j];
-    const float dx = pi.x - pj.x, dy = pi.y - pj.y, dz = pi.z - pj.z;   // x_ij = x_i - x_j
-    const float r2 = dx * dx + dy * dy + dz * dz;
-    if (r2 >= ph.R2 || r2 == 0.f) continue;                              // A17, A18
-    const float F = kernel_F(r2, ph);                                     // W'(r)/r
-    const float4 uj = U[j];
-    const float4 sj1 = S1[j];
-    const float2 sj2 = S2[j];
-    const float w = __fdividef(ph.m, pj.w) * F;                           // V_j W'/r (A7)
-    const float gx = w * dx, gy = w * dy, gz = w * dz;                   // V_j grad_i W_ij
-    const float dux = uj.x - ui.x, duy = uj.y - ui.y, duz = uj.z - ui.z; // u_ji
-    // velocity gradient L_ab += V_j u_ji,a gradW_b (F2, A4)
-    L[0] += dux * gx; L[1] += dux * gy; L[2] += dux * gz;
-    L[3] += duy * gx; L[4] += duy * gy; L[5] += duy * gz;
-    L[6] += duz * gx; L[7] += duz * gy; L[8] += duz * gz;
-    // F3 momentum: sum V_j (sigma_i + sigma_j) grad W = sigma_i sum V_j gradW + sum V_j sigma_j gradW
-    Gs[0] += gx; Gs[1] += gy; Gs[2] += gz;
-    Ms[0] += sj1.x * gx + sj1.w * gy + sj2.x * gz;
-    Ms[1] += sj1.w * gx + sj1.y * gy + sj2.y * gz;
-    Ms[2] += sj2.x * gx + sj2.y * gy + sj1.z * gz;
-    // artificial viscosity (Eq. 13/14, sign of reading A9): v_ij . r_ij with v_ij = u_i - u_j
-    const float vr = -(dux * dx + duy * dy + duz * dz);
-    if (!ph.unilateral || vr < 0.f) {
-      // gamma_a h c_s (m_j / rho_bar_ij) (v_ij . r_ij) / (r^2 + xi^2) W'/r, rho_bar = (rho_i + rho_j)/2
-      const float coef = ph.avc * __fdividef(two_m, pi.w + pj.w) * __fdividef(vr, r2 + ph.xi2) * F;
-      Pi[0] += coef * dx; Pi[1] += coef * dy; Pi[2] += coef * dz;
-    }
-  }
-  const float rinv_i = 1.0f / pi.w;
-  float a[3];
-  a[0] = (si1.x * Gs[0] + si1.w * Gs[1] + si2.x * Gs[2] + Ms[0]) * rinv_i + Pi[0];
-  a[1] = (si1.w * Gs[0] + si1.y * Gs[1] + si2.y * Gs[2] + Ms[1]) * rinv_i + Pi[1];
-  a[2] = (si2.x * Gs[0] + si2.y * Gs[1] + si1.z * Gs[2] + Ms[2]) * rinv_i + Pi[2];
-  if (bce) {   // STAGE 1, moving-body marker: m a_s for the body loads (no gravity, A13)
-    macc[i] = make_float4(ph.m * a[0], ph.m * a[1], ph.m * a[2], 0.f);
-    if (dbg_on) dbg.acc[1][i] = make_float4(a[0], a[1], a[2], 0.f);
-    return;
-  }
-  a[0] += ph.g[0]; a[1] += ph.g[1]; a[2] += ph.g[2];
-  // continuity (Eq. continuity_dis): drho = -rho_i sum (u_j - u_i) . gradW V_j = -rho_i tr L
-  const float drho = -pi.w * (L[0] + L[4] + L[8]);
-  // Jaumann stress rate (Eq. stress_rate, Eq. 3; A4–A6)
-  const float sig[9] = {si1.x, si1.w, si2.x, si1.w, si1.y, si2.y, si2.x, si2.y, si1.z};
-  float E[9], Om[9];
-#pragma unroll
-  for (int r = 0; r < 3; ++r)
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      E[3 * r + c] = 0.5f * (L[3 * r + c] + L[3 * c + r]);
-      Om[3 * r + c] = 0.5f * (L[3 * r + c] - L[3 * c + r]);
-    }
-  const float tr = E[0] + E[4] + E[8];
-  float ds[6];
-  const int rr[6] = {0, 1, 2, 0, 0, 1}, cc[6] = {0, 1, 2, 1, 2, 2};
-#pragma unroll
-  for (int k = 0; k < 6; ++k) {
-    const int r = rr[k], c = cc[k];
-    float v = 0.f;
-#pragma unroll
-    for (int t = 0; t < 3; ++t) v += Om[3 * r + t] * sig[3 * t + c] - sig[3 * r + t] * Om[3 * t + c];
-    v += 2.0f * ph.G * E[3 * r + c];
-    if (r == c) v += (ph.K - 2.0f * ph.G / 3.0f) * tr;
-    ds[k] = v;
-  }
-  if (dbg_on) {
-    dbg.drho[STAGE][i] = drho;
-    dbg.acc[STAGE][i] = make_float4(a[0], a[1], a[2], 0.f);
-    dbg.ds1[STAGE][i] = make_float4(ds[0], ds[1], ds[2], ds[3]);
-    dbg.ds2[STAGE][i] = make_float2(ds[4], ds[5]);
-  }
-  if (STAGE == 0) {
-    const float hd = 0.5f * dt;
-    YP[i] = make_float4(pi.x + hd * ui.x, pi.y + hd * ui.y, pi.z + hd * ui.z, pi.w + hd * drho);
-    YU[i] = make_float4(ui.x + hd * a[0], ui.y + hd * a[1], ui.z + hd * a[2], ui.w);
-    YS1[i] = make_float4(si1.x + hd * ds[0], si1.y + hd * ds[1], si1.z + hd * ds[2], si1.w + hd * ds[3]);
-    YS2[i] = make_float2(si2.x + hd * ds[4], si2.y + hd * ds[5]);
-  } else {
-    const float4 p0 = YP[i];
-    const float4 u0 = YU[i];
-    const float4 s01 = YS1[i];
-    const float2 s02 = YS2[i];
-    const float sn[6] = {s01.x, s01.y, s01.z, s01.w, s02.x, s02.y};
-    float s[6] = {s01.x + dt * ds[0], s01.y + dt * ds[1], s01.z + dt * ds[2],
-                  s01.w + dt * ds[3], s02.x + dt * ds[4], s02.y + dt * ds[5]};
-    return_map(s, sn, ph, dt);
-    const float4 pn = make_float4(p0.x + dt * ui.x, p0.y + dt * ui.y, p0.z + dt * ui.z, p0.w + dt * drho);
-    const float4 un = make_float4(u0.x + dt * a[0], u0.y + dt * a[1], u0.z + dt * a[2], u0.w);
-    YP[i] = pn;
-    YU[i] = un;
-    YS1[i] = make_float4(s[0], s[1], s[2], s[3]);
-    YS2[i] = make_float2(s[4], s[5]);
-    const float chk = pn.x + pn.y + pn.z + pn.w + un.x + un.y + un.z + s[0] + s[1] + s[2] + s[3] + s[4] + s[5];
-    if (!isfinite(chk)) latch_error(err, -3 /*CRM_E_NONFINITE*/, (long long)ids[i], step, 0);
-  }
 }
 
 // ------------------------------------------------------------------------------------

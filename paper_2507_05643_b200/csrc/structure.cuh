@@ -7,8 +7,7 @@
 //   k_scatter    slot = cellStart[c] + arrival  (arrival order is not deterministic)
 //   k_reorder    rank inside the cell by id -> final (cell, id) position; moves the
 //                56-B state with float4/float2 vector loads/stores
-//   k_neighbors  Alg. 1 over the 9 contiguous index runs of the 27-cell stencil, strict
-//                r^2 < (2h)^2 evaluated in fp32 exactly as B2; ELL list k-major
+// The Alg. 1 filter itself runs inside the tiled kernels (tiled.cuh), fused with the pair loops.
 #pragma once
 #include "common.cuh"
 
@@ -159,52 +158,6 @@ __global__ void k_reorder(int n, const uint32_t* __restrict__ tmp_src, const uin
   ids_n[d] = myid;
   cell_of[d] = c;
   slot_of_id[myid] = d;
-}
-
-// ---------------------------------------------------------------------------------------
-// Alg. 1 on the sorted state.  With c = cx*(Ny*Nz) + cy*Nz + cz the 27-cell
-// stencil is 9 runs of 3 consecutive cells, i.e. 9 contiguous particle index ranges.
-// Fluid i stores every neighbour; a marker stores only its fluid neighbours (the only ones
-// it uses) unless store_all.  count_all = |P(i)| (fluid + BCE) for the parity check.
-__global__ void __launch_bounds__(256) k_neighbors(int n, Grid g, const float4* __restrict__ P,
-                            const float4* __restrict__ U, const uint32_t* __restrict__ cell_of,
-                            const uint32_t* __restrict__ cell_start, uint32_t* __restrict__ list,
-                            uint32_t* __restrict__ nlist, uint32_t* __restrict__ count_all, int cap,
-                            int store_all, ErrLatch* err, const uint32_t* __restrict__ ids, long long step) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const float4 pi = P[i];
-  const bool i_bce = tag_is_bce(tag_of(U[i].w));
-  const uint32_t c = cell_of[i];
-  const int Nz = g.dims[2], Ny = g.dims[1], Nx = g.dims[0];
-  const int cz = (int)(c % (uint32_t)Nz);
-  const int cy = (int)((c / (uint32_t)Nz) % (uint32_t)Ny);
-  const int cx = (int)(c / (uint32_t)(Ny * Nz));
-  const int zlo = max(cz - 1, 0), zhi = min(cz + 1, Nz - 1);
-  uint32_t cnt = 0, k = 0;
-  const size_t stride = (size_t)n;
-  for (int a = -1; a <= 1; ++a) {
-    const int x = cx + a;
-    if (x < 0 || x >= Nx) continue;
-    for (int b = -1; b <= 1; ++b) {
-      const int y = cy + b;
-      if (y < 0 || y >= Ny) continue;
-      const uint32_t base = (uint32_t)x * (uint32_t)(Ny * Nz) + (uint32_t)y * (uint32_t)Nz;
-      const uint32_t jb = cell_start[base + zlo], je = cell_start[base + zhi + 1];
-      for (uint32_t j = jb; j < je; ++j) {
-        if (j == (uint32_t)i) continue;
-        const float4 pj = P[j];
-        if (!b2_pred(pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, g.R2)) continue;
-        ++cnt;
-        if (i_bce && !store_all && tag_is_bce(tag_of(U[j].w))) continue;
-        if (k < (uint32_t)cap) list[(size_t)k * stride + i] = j;
-        ++k;
-      }
-    }
-  }
-  count_all[i] = cnt;
-  nlist[i] = min(k, (uint32_t)cap);
-  if (k > (uint32_t)cap) latch_error(err, -9 /*CRM_E_CAPACITY*/, (long long)ids[i], step, (long long)k);
 }
 
 }  // namespace crmk

@@ -1,0 +1,468 @@
+// tiled.cuh — the hot kernels: one CTA per cell tile, window staged in shared memory.
+//
+//   k_bce_t<0>   markers: Alg. 1 filter over the window (fluid neighbours stored, all counted),
+//                Adami extrapolation at y_n                       -> U, S of markers
+//   k_rates_t<0> fluid: Alg. 1 filter (all neighbours stored) + pair loop at y_n
+//                + y_mid = y_n + dt/2 f; markers copied to the mid state
+//   k_bce_t<1>   markers: extrapolation at y_mid with the stored lists
+//   k_rates_t<1> fluid: pair loop at y_mid with the same lists (A17) + y_{n+1} = y_n + dt f
+//                + mu(I) return map; moving-body markers: loads (A13)
+#pragma once
+#include "common.cuh"
+#include "physics.cuh"
+#include "structure.cuh"
+#include "tiles.cuh"
+
+namespace crmk {
+
+// ---------------------------------------------------------------------------------------
+template <bool STAGED>
+__device__ __forceinline__ void load_pos(const TileSmem& sm, const float4* __restrict__ P, uint32_t off, float4& p) {
+  if (STAGED) p = sm.P[off];
+  else p = P[window_to_global(sm, off)];
+}
+
+template <bool STAGED>
+__device__ __forceinline__ void load_all(const TileSmem& sm, const float4* __restrict__ P, const float4* __restrict__ U,
+                                         const float4* __restrict__ S1, const float2* __restrict__ S2, uint32_t off,
+                                         float4& p, float4& u, float4& s1, float2& s2) {
+  if (STAGED) {
+    p = sm.P[off]; u = sm.U[off]; s1 = sm.S1[off]; s2 = sm.S2[off];
+  } else {
+    const uint32_t g = window_to_global(sm, off);
+    p = P[g]; u = U[g]; s1 = S1[g]; s2 = S2[g];
+  }
+}
+
+// Alg. 1 filter for particle i (window offset self) over its 9 candidate runs; stores window
+// offsets (all neighbours if store_bce, else fluid ones only); returns |P(i)|.  The candidate
+// order (runs in (da, db) order, offsets ascending) fixes the list order, hence the summation
+// order of the pair loops (deterministic).
+template <bool STAGED>
+__device__ __forceinline__ void filter_range(const Grid& g, const TileSmem& sm, const float4* __restrict__ P,
+                                             const float4* __restrict__ U, uint32_t ob, uint32_t oe, uint32_t gshift,
+                                             const float4& pi, bool store_bce, uint32_t& cnt, ListWriter& w) {
+  // chunks of 32 candidates: a branch-free predicate sweep builds a bitmask, then the set bits
+  // are appended in ascending order (same order as a plain loop)
+  for (uint32_t base = ob; base < oe; base += 32) {
+    const uint32_t nc = min(32u, oe - base);
+    uint32_t m = 0;
+#pragma unroll 4
+    for (uint32_t k = 0; k < nc; ++k) {
+      const float4 pj = STAGED ? sm.P[base + k] : P[base + k + gshift];
+      m |= (b2_pred(pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, g.R2) ? 1u : 0u) << k;
+    }
+    cnt += __popc(m);
+    while (m) {
+      const uint32_t b = __ffs(m) - 1;
+      m &= m - 1;
+      const uint32_t off = base + b;
+      if (store_bce || !tag_is_bce(tag_of(STAGED ? sm.U[off].w : U[off + gshift].w))) w.push(off);
+    }
+  }
+}
+
+template <bool STAGED>
+__device__ __forceinline__ uint32_t filter(const Grid& g, const TileSmem& sm, const float4* __restrict__ P,
+                                           const float4* __restrict__ U, int q, int cz, uint32_t self, float4 pi,
+                                           bool store_bce, ListWriter& w) {
+  uint32_t cnt = 0;
+#pragma unroll 1
+  for (int da = -1; da <= 1; ++da) {
+#pragma unroll 1
+    for (int db = -1; db <= 1; ++db) {
+      uint32_t ob, oe;
+      int r;
+      cand_range(sm, q, da, db, cz, ob, oe, r);
+      const uint32_t gshift = sm.run_start[r] - sm.run_base[r];
+      if (da == 0 && db == 0) {   // the own run holds i itself (j != i, A18)
+        filter_range<STAGED>(g, sm, P, U, ob, self, gshift, pi, store_bce, cnt, w);
+        filter_range<STAGED>(g, sm, P, U, self + 1, oe, gshift, pi, store_bce, cnt, w);
+      } else {
+        filter_range<STAGED>(g, sm, P, U, ob, oe, gshift, pi, store_bce, cnt, w);
+      }
+    }
+  }
+  return cnt;
+}
+
+// ---------------------------------------------------------------------------------------
+template <int STAGE, bool STAGED>
+__device__ __forceinline__ void bce_tile(const Grid& g, const Phys& ph, TileSmem& sm, const float4* __restrict__ P,
+                                         float4* __restrict__ U, float4* __restrict__ S1, float2* __restrict__ S2,
+                                         uint16_t* __restrict__ list, uint32_t* __restrict__ nlist,
+                                         uint32_t* __restrict__ count_all, const uint32_t* __restrict__ cell_of,
+                                         const Pose* __restrict__ pose, int cap, int store_all, Debug dbg, int dbg_on,
+                                         ErrLatch* err, const uint32_t* __restrict__ ids, long long step) {
+  const uint32_t n_i = sm.col_pref[NCOL];
+  for (uint32_t t = threadIdx.x; t < n_i; t += blockDim.x) {
+    int q;
+    const uint32_t i = tile_particle(sm, t, q);
+    const float4 ui = U[i];
+    const uint32_t tag = tag_of(ui.w);
+    if (!tag_is_bce(tag)) continue;
+    const float4 pa = P[i];
+    uint32_t nl;
+    if (STAGE == 0) {
+      const int r_self = (1 + q / TY) * WRY + (1 + q % TY);
+      const uint32_t self = sm.run_base[r_self] + (i - sm.run_start[r_self]);
+      const int cz = (int)(cell_of[i] % (uint32_t)g.dims[2]);
+      ListWriter w;
+      w.init(list, i, cap);
+      const uint32_t cnt = filter<STAGED>(g, sm, P, U, q, cz, self, pa, store_all != 0, w);
+      w.flush(self);
+      nl = (uint32_t)min(w.k, cap);
+      nlist[i] = nl;
+      count_all[i] = cnt;
+      if (w.k > cap) latch_error(err, -9 /*CRM_E_CAPACITY*/, (long long)ids[i], step, (long long)w.k);
+    } else {
+      nl = nlist[i];
+    }
+    float ub[3] = {0.f, 0.f, 0.f}, ab[3] = {0.f, 0.f, 0.f};
+    if (tag_moving(tag)) body_kinematics(pose[tag_body(tag)], pa.x, pa.y, pa.z, ub, ab);
+    const float ga[3] = {ph.g[0] - ab[0], ph.g[1] - ab[1], ph.g[2] - ab[2]};
+    float SW = 0.f, su[3] = {0.f, 0.f, 0.f}, ss[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, sh = 0.f;
+    const uint4* seg = reinterpret_cast<const uint4*>(list + (size_t)i * cap);
+    // whole chunks of 8 (padded with the marker itself, excluded by the fluid mask): branch-free
+    for (uint32_t c = 0; c < ((nl + 7) >> 3); ++c) {
+      const uint4 v = seg[c];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const uint32_t off = list_entry(v, e);
+        float4 pf, uf, s1;
+        float2 s2;
+        load_all<STAGED>(sm, P, U, S1, S2, off, pf, uf, s1, s2);
+        const float dx = pa.x - pf.x, dy = pa.y - pf.y, dz = pa.z - pf.z;
+        const float r2 = dx * dx + dy * dy + dz * dz;
+        // fluid neighbours only; W = 0 beyond the support (A17)
+        const bool ok = !tag_is_bce(tag_of(uf.w)) && r2 < ph.R2;
+        const float r = (r2 > 0.f) ? r2 * rsqrt_approx(r2) : 0.f;
+        const float q = r * ph.hinv;
+        const float t = 2.0f - q;
+        const float Wv = q < 1.0f ? ph.wnorm * (1.0f - 1.5f * q * q + 0.75f * q * q * q) : ph.wnorm * 0.25f * t * t * t;
+        const float W = ok ? Wv : 0.f;
+        SW += W;
+        su[0] += uf.x * W; su[1] += uf.y * W; su[2] += uf.z * W;
+        ss[0] += s1.x * W; ss[1] += s1.y * W; ss[2] += s1.z * W;
+        ss[3] += s1.w * W; ss[4] += s2.x * W; ss[5] += s2.y * W;
+        sh += pf.w * (ga[0] * dx + ga[1] * dy + ga[2] * dz) * W;
+      }
+    }
+    float4 uo, s1o;
+    float2 s2o;
+    if (SW > 0.f) {
+      const float inv = 1.0f / SW;
+      uo = make_float4(2.f * ub[0] - su[0] * inv, 2.f * ub[1] - su[1] * inv, 2.f * ub[2] - su[2] * inv, ui.w);
+      const float hyd = sh * inv;
+      s1o = make_float4(ss[0] * inv - hyd, ss[1] * inv - hyd, ss[2] * inv - hyd, ss[3] * inv);
+      s2o = make_float2(ss[4] * inv, ss[5] * inv);
+    } else {   // A11
+      uo = make_float4(ub[0], ub[1], ub[2], ui.w);
+      s1o = make_float4(0.f, 0.f, 0.f, 0.f);
+      s2o = make_float2(0.f, 0.f);
+    }
+    U[i] = uo;
+    S1[i] = s1o;
+    S2[i] = s2o;
+    if (dbg_on) {
+      dbg.bu[STAGE][i] = uo;
+      dbg.bs1[STAGE][i] = s1o;
+      dbg.bs2[STAGE][i] = s2o;
+    }
+  }
+}
+
+template <int STAGE>
+__global__ void __launch_bounds__(TILE_THREADS, 2)
+    k_bce_t(Grid g, Phys ph, const uint32_t* __restrict__ cell_start, const float4* __restrict__ P,
+            float4* __restrict__ U, float4* __restrict__ S1, float2* __restrict__ S2, uint16_t* __restrict__ list,
+            uint32_t* __restrict__ nlist, uint32_t* __restrict__ count_all, const uint32_t* __restrict__ cell_of,
+            const Pose* __restrict__ pose, int cap, int store_all, Debug dbg, int dbg_on, ErrLatch* err,
+            const uint32_t* __restrict__ ids, long long step) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
+  const TileGeom G = tile_geom(g, blockIdx.x);
+  tile_setup(g, G, cell_start, sm);
+  const uint32_t n_i = sm.col_pref[NCOL];
+  if (n_i == 0) return;
+  int has = 0;
+  for (uint32_t t = threadIdx.x; t < n_i; t += blockDim.x) {
+    int q;
+    has |= tag_is_bce(tag_of(U[tile_particle(sm, t, q)].w)) ? 1 : 0;
+  }
+  if (!__syncthreads_or(has)) return;
+  if (sm.run_base[WR] > 65535u) {
+    if (threadIdx.x == 0) latch_error(err, -9, -1, step, (long long)sm.run_base[WR]);
+    return;
+  }
+  tile_stage(P, U, S1, S2, sm);
+  tile_stage_wait();
+  __syncthreads();
+  if (sm.staged)
+    bce_tile<STAGE, true>(g, ph, sm, P, U, S1, S2, list, nlist, count_all, cell_of, pose, cap, store_all, dbg,
+                          dbg_on, err, ids, step);
+  else
+    bce_tile<STAGE, false>(g, ph, sm, P, U, S1, S2, list, nlist, count_all, cell_of, pose, cap, store_all, dbg,
+                           dbg_on, err, ids, step);
+}
+
+// ---------------------------------------------------------------------------------------
+struct PairAcc {
+  float L[9], Gs[3], Ms[3], Pi[3];
+};
+
+__device__ __forceinline__ void pair_terms(PairAcc& A, const Phys& ph, const float4& pi, const float4& ui,
+                                           const float4& pj, const float4& uj, const float4& sj1, const float2& sj2,
+                                           bool with_L, bool okj) {
+  const float dx = pi.x - pj.x, dy = pi.y - pj.y, dz = pi.z - pj.z;   // x_ij = x_i - x_j
+  const float r2 = dx * dx + dy * dy + dz * dz;
+  // branch-free: invalid pairs (r >= 2h, A17; r = 0 incl. the self padding, A18; a marker when
+  // only fluid counts) get F = 0, hence a zero contribution to every sum
+  const bool ok = r2 < ph.R2 && r2 > 0.f && okj;
+  // W'(r)/r of the cubic spline (A1): kin_a r + kin_b for r < h, kout (2 - r/h)^2 / r otherwise
+  const float rinv = rsqrt_approx(r2);
+  const float r = r2 * rinv;
+  const float t = fmaf(-ph.hinv, r, 2.0f);
+  const float Fv = (r < ph.h) ? fmaf(ph.kin_a, r, ph.kin_b) : ph.kout * t * t * rinv;
+  const float F = ok ? Fv : 0.f;
+  const float w = ph.m * rcp_approx(pj.w) * F;                         // V_j W'/r (A7)
+  const float gx = w * dx, gy = w * dy, gz = w * dz;                  // V_j grad_i W_ij
+  const float dux = uj.x - ui.x, duy = uj.y - ui.y, duz = uj.z - ui.z; // u_ji
+  if (with_L) {   // velocity gradient L_ab += V_j u_ji,a gradW_b (F2, A4)
+    A.L[0] += dux * gx; A.L[1] += dux * gy; A.L[2] += dux * gz;
+    A.L[3] += duy * gx; A.L[4] += duy * gy; A.L[5] += duy * gz;
+    A.L[6] += duz * gx; A.L[7] += duz * gy; A.L[8] += duz * gz;
+  }
+  // F3 momentum: sum V_j (sigma_i + sigma_j) gradW = sigma_i sum V_j gradW + sum V_j sigma_j gradW
+  A.Gs[0] += gx; A.Gs[1] += gy; A.Gs[2] += gz;
+  A.Ms[0] += sj1.x * gx + sj1.w * gy + sj2.x * gz;
+  A.Ms[1] += sj1.w * gx + sj1.y * gy + sj2.y * gz;
+  A.Ms[2] += sj2.x * gx + sj2.y * gy + sj1.z * gz;
+  // artificial viscosity (Eq. 13/14, sign of reading A9): v_ij . r_ij with v_ij = u_i - u_j
+  const float vr = -(dux * dx + duy * dy + duz * dz);
+  // gamma_a h c_s (m_j / rho_bar_ij) (v_ij . r_ij) / (r^2 + xi^2) W'/r, rho_bar = (rho_i + rho_j)/2
+  const float cv = ph.c_av * vr * F * rcp_approx((pi.w + pj.w) * (r2 + ph.xi2));
+  const float coef = (!ph.unilateral || vr < 0.f) ? cv : 0.f;
+  A.Pi[0] += coef * dx; A.Pi[1] += coef * dy; A.Pi[2] += coef * dz;
+}
+
+template <bool STAGED>
+__device__ __forceinline__ void pair_loop(PairAcc& A, const Phys& ph, const TileSmem& sm, const float4* __restrict__ P,
+                                          const float4* __restrict__ U, const float4* __restrict__ S1,
+                                          const float2* __restrict__ S2, const uint16_t* __restrict__ list,
+                                          uint32_t i, int cap, uint32_t nl, const float4& pi, const float4& ui,
+                                          bool with_L, bool fluid_only) {
+  const uint4* seg = reinterpret_cast<const uint4*>(list + (size_t)i * cap);
+  for (uint32_t c = 0; c < ((nl + 7) >> 3); ++c) {   // whole padded chunks of 8, branch-free
+    const uint4 v = seg[c];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      float4 pj, uj, s1;
+      float2 s2;
+      load_all<STAGED>(sm, P, U, S1, S2, list_entry(v, e), pj, uj, s1, s2);
+      pair_terms(A, ph, pi, ui, pj, uj, s1, s2, with_L, !(fluid_only && tag_is_bce(tag_of(uj.w))));
+    }
+  }
+}
+
+template <int STAGE, bool STAGED>
+__device__ __forceinline__ void rates_tile(const Grid& g, const Phys& ph, float dt, TileSmem& sm,
+                                           const float4* __restrict__ P, const float4* __restrict__ U,
+                                           const float4* __restrict__ S1, const float2* __restrict__ S2,
+                                           float4* __restrict__ YP, float4* __restrict__ YU, float4* __restrict__ YS1,
+                                           float2* __restrict__ YS2, uint16_t* __restrict__ list,
+                                           uint32_t* __restrict__ nlist, uint32_t* __restrict__ count_all,
+                                           const uint32_t* __restrict__ cell_of, int cap, float4* __restrict__ macc,
+                                           Debug dbg, int dbg_on, ErrLatch* err, const uint32_t* __restrict__ ids,
+                                           long long step) {
+  const uint32_t n_i = sm.col_pref[NCOL];
+  for (uint32_t t = threadIdx.x; t < n_i; t += blockDim.x) {
+    int q;
+    const uint32_t i = tile_particle(sm, t, q);
+    const float4 ui = U[i];
+    const uint32_t tag = tag_of(ui.w);
+    const bool bce = tag_is_bce(tag);
+    if (bce && !(STAGE == 1 && tag_moving(tag))) continue;
+    const float4 pi = P[i];
+    uint32_t nl;
+    if (STAGE == 0) {
+      const int r_self = (1 + q / TY) * WRY + (1 + q % TY);
+      const uint32_t self = sm.run_base[r_self] + (i - sm.run_start[r_self]);
+      const int cz = (int)(cell_of[i] % (uint32_t)g.dims[2]);
+      ListWriter w;
+      w.init(list, i, cap);
+      const uint32_t cnt = filter<STAGED>(g, sm, P, U, q, cz, self, pi, true, w);
+      w.flush(self);
+      nl = (uint32_t)min(w.k, cap);
+      nlist[i] = nl;
+      count_all[i] = cnt;
+      if (w.k > cap) latch_error(err, -9 /*CRM_E_CAPACITY*/, (long long)ids[i], step, (long long)w.k);
+    } else {
+      nl = nlist[i];
+    }
+    PairAcc A;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) A.L[k] = 0.f;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) { A.Gs[k] = 0.f; A.Ms[k] = 0.f; A.Pi[k] = 0.f; }
+    const float4 si1 = S1[i];
+    const float2 si2 = S2[i];
+    if (bce) {   // STAGE 1, moving-body marker: m a_s over fluid neighbours, no gravity (A13)
+      pair_loop<STAGED>(A, ph, sm, P, U, S1, S2, list, i, cap, nl, pi, ui, false, true);
+      const float rinv_i = 1.0f / pi.w;
+      float a[3];
+      a[0] = (si1.x * A.Gs[0] + si1.w * A.Gs[1] + si2.x * A.Gs[2] + A.Ms[0]) * rinv_i + A.Pi[0];
+      a[1] = (si1.w * A.Gs[0] + si1.y * A.Gs[1] + si2.y * A.Gs[2] + A.Ms[1]) * rinv_i + A.Pi[1];
+      a[2] = (si2.x * A.Gs[0] + si2.y * A.Gs[1] + si1.z * A.Gs[2] + A.Ms[2]) * rinv_i + A.Pi[2];
+      macc[i] = make_float4(ph.m * a[0], ph.m * a[1], ph.m * a[2], 0.f);
+      if (dbg_on) dbg.acc[1][i] = make_float4(a[0], a[1], a[2], 0.f);
+      continue;
+    }
+    pair_loop<STAGED>(A, ph, sm, P, U, S1, S2, list, i, cap, nl, pi, ui, true, false);
+    const float rinv_i = 1.0f / pi.w;
+    float a[3];
+    a[0] = (si1.x * A.Gs[0] + si1.w * A.Gs[1] + si2.x * A.Gs[2] + A.Ms[0]) * rinv_i + A.Pi[0] + ph.g[0];
+    a[1] = (si1.w * A.Gs[0] + si1.y * A.Gs[1] + si2.y * A.Gs[2] + A.Ms[1]) * rinv_i + A.Pi[1] + ph.g[1];
+    a[2] = (si2.x * A.Gs[0] + si2.y * A.Gs[1] + si1.z * A.Gs[2] + A.Ms[2]) * rinv_i + A.Pi[2] + ph.g[2];
+    // continuity (Eq. continuity_dis): drho = -rho_i sum (u_j - u_i) . gradW V_j = -rho_i tr L
+    const float drho = -pi.w * (A.L[0] + A.L[4] + A.L[8]);
+    // Jaumann stress rate (Eq. stress_rate with Eq. 3; readings A4–A6)
+    const float sig[9] = {si1.x, si1.w, si2.x, si1.w, si1.y, si2.y, si2.x, si2.y, si1.z};
+    float E[9], Om[9];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        E[3 * r + c] = 0.5f * (A.L[3 * r + c] + A.L[3 * c + r]);
+        Om[3 * r + c] = 0.5f * (A.L[3 * r + c] - A.L[3 * c + r]);
+      }
+    const float tr = E[0] + E[4] + E[8];
+    float ds[6];
+    const int rr[6] = {0, 1, 2, 0, 0, 1}, cc[6] = {0, 1, 2, 1, 2, 2};
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      const int r = rr[k], c = cc[k];
+      float v = 0.f;
+#pragma unroll
+      for (int s = 0; s < 3; ++s) v += Om[3 * r + s] * sig[3 * s + c] - sig[3 * r + s] * Om[3 * s + c];
+      v += 2.0f * ph.G * E[3 * r + c];
+      if (r == c) v += (ph.K - 2.0f * ph.G / 3.0f) * tr;
+      ds[k] = v;
+    }
+    if (dbg_on) {
+      dbg.drho[STAGE][i] = drho;
+      dbg.acc[STAGE][i] = make_float4(a[0], a[1], a[2], 0.f);
+      dbg.ds1[STAGE][i] = make_float4(ds[0], ds[1], ds[2], ds[3]);
+      dbg.ds2[STAGE][i] = make_float2(ds[4], ds[5]);
+    }
+    if (STAGE == 0) {
+      const float hd = 0.5f * dt;
+      YP[i] = make_float4(pi.x + hd * ui.x, pi.y + hd * ui.y, pi.z + hd * ui.z, pi.w + hd * drho);
+      YU[i] = make_float4(ui.x + hd * a[0], ui.y + hd * a[1], ui.z + hd * a[2], ui.w);
+      YS1[i] = make_float4(si1.x + hd * ds[0], si1.y + hd * ds[1], si1.z + hd * ds[2], si1.w + hd * ds[3]);
+      YS2[i] = make_float2(si2.x + hd * ds[4], si2.y + hd * ds[5]);
+    } else {
+      const float4 p0 = YP[i];
+      const float4 u0 = YU[i];
+      const float4 s01 = YS1[i];
+      const float2 s02 = YS2[i];
+      const float sn[6] = {s01.x, s01.y, s01.z, s01.w, s02.x, s02.y};
+      float s[6] = {s01.x + dt * ds[0], s01.y + dt * ds[1], s01.z + dt * ds[2],
+                    s01.w + dt * ds[3], s02.x + dt * ds[4], s02.y + dt * ds[5]};
+      return_map(s, sn, ph, dt);
+      const float4 pn = make_float4(p0.x + dt * ui.x, p0.y + dt * ui.y, p0.z + dt * ui.z, p0.w + dt * drho);
+      const float4 un = make_float4(u0.x + dt * a[0], u0.y + dt * a[1], u0.z + dt * a[2], u0.w);
+      YP[i] = pn;
+      YU[i] = un;
+      YS1[i] = make_float4(s[0], s[1], s[2], s[3]);
+      YS2[i] = make_float2(s[4], s[5]);
+      const float chk = pn.x + pn.y + pn.z + pn.w + un.x + un.y + un.z + s[0] + s[1] + s[2] + s[3] + s[4] + s[5];
+      if (!isfinite(chk)) latch_error(err, -3 /*CRM_E_NONFINITE*/, (long long)ids[i], step, 0);
+    }
+  }
+}
+
+// STAGE 0: (P,U,S) = y_n, (YP..) = mid (out).  STAGE 1: (P,U,S) = y_mid, (YP..) = y_n in / y_{n+1} out.
+template <int STAGE>
+__global__ void __launch_bounds__(TILE_THREADS, 2)
+    k_rates_t(Grid g, Phys ph, float dt, const uint32_t* __restrict__ cell_start, const float4* __restrict__ P,
+              const float4* __restrict__ U, const float4* __restrict__ S1, const float2* __restrict__ S2,
+              float4* __restrict__ YP, float4* __restrict__ YU, float4* __restrict__ YS1, float2* __restrict__ YS2,
+              uint16_t* __restrict__ list, uint32_t* __restrict__ nlist, uint32_t* __restrict__ count_all,
+              const uint32_t* __restrict__ cell_of, int cap, float4* __restrict__ macc, Debug dbg, int dbg_on,
+              ErrLatch* err, const uint32_t* __restrict__ ids, long long step) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
+  const TileGeom G = tile_geom(g, blockIdx.x);
+  tile_setup(g, G, cell_start, sm);
+  const uint32_t n_i = sm.col_pref[NCOL];
+  if (n_i == 0) return;
+  // marker bookkeeping that needs no window; detect whether the tile has pair work
+  int work = 0;
+  for (uint32_t t = threadIdx.x; t < n_i; t += blockDim.x) {
+    int q;
+    const uint32_t i = tile_particle(sm, t, q);
+    const float4 ui = U[i];
+    const uint32_t tag = tag_of(ui.w);
+    if (!tag_is_bce(tag)) {
+      work = 1;
+    } else if (STAGE == 0) {
+      YP[i] = P[i];     // markers: x at t_n (moving ones are re-placed at t_n + dt/2 afterwards)
+      YU[i] = ui;       // tag; u and sigma are replaced by the stage-B extrapolation
+    } else {
+      YU[i] = ui;       // y_{n+1} of a marker: its stage-B extrapolated u and sigma
+      YS1[i] = S1[i];
+      YS2[i] = S2[i];
+      if (tag_moving(tag)) work = 1;
+    }
+  }
+  if (!__syncthreads_or(work)) return;
+  if (sm.run_base[WR] > 65535u) {
+    if (threadIdx.x == 0) latch_error(err, -9, -1, step, (long long)sm.run_base[WR]);
+    return;
+  }
+  tile_stage(P, U, S1, S2, sm);
+  tile_stage_wait();
+  __syncthreads();
+  if (sm.staged)
+    rates_tile<STAGE, true>(g, ph, dt, sm, P, U, S1, S2, YP, YU, YS1, YS2, list, nlist, count_all, cell_of, cap, macc,
+                            dbg, dbg_on, err, ids, step);
+  else
+    rates_tile<STAGE, false>(g, ph, dt, sm, P, U, S1, S2, YP, YU, YS1, YS2, list, nlist, count_all, cell_of, cap, macc,
+                             dbg, dbg_on, err, ids, step);
+}
+
+// ---------------------------------------------------------------------------------------
+// debug: hot-path lists (window offsets) -> global sorted indices, ELL k-major u32
+__global__ void k_decode_lists(int n, Grid g, const uint32_t* __restrict__ cell_start,
+                               const uint32_t* __restrict__ cell_of, const uint16_t* __restrict__ list,
+                               const uint32_t* __restrict__ nlist, int cap, uint32_t* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t c = cell_of[i];
+  const int Nz = g.dims[2], Ny = g.dims[1];
+  const int cz = (int)(c % (uint32_t)Nz), cy = (int)((c / (uint32_t)Nz) % (uint32_t)Ny), cx = (int)(c / (uint32_t)(Ny * Nz));
+  const long long t = ((long long)(cx / TX) * tiles_y(g) + cy / TY) * tiles_z(g) + cz / TZ;
+  const TileGeom G = tile_geom(g, t);
+  const int nzw = G.zhi - G.zlo + 1;
+  uint32_t rs[WR], rb[WR + 1];
+  uint32_t acc = 0;
+  for (int r = 0; r < WR; ++r) {
+    const int x = G.X0 - 1 + r / WRY, y = G.Y0 - 1 + r % WRY;
+    const bool valid = x >= 0 && x < g.dims[0] && y >= 0 && y < g.dims[1];
+    const uint32_t c0 = valid ? cell_id(g, x, y, G.zlo) : 0u;
+    rs[r] = valid ? cell_start[c0] : 0u;
+    const uint32_t re = valid ? cell_start[c0 + nzw] : 0u;
+    rb[r] = acc;
+    acc += re - rs[r];
+  }
+  rb[WR] = acc;
+  for (uint32_t k = 0; k < nlist[i]; ++k) {
+    const uint32_t off = list[(size_t)i * cap + k];
+    int r = 0;
+    for (int q = 1; q < WR; ++q) r += (rb[q] <= off) ? 1 : 0;
+    out[(size_t)k * n + i] = rs[r] + (off - rb[r]);
+  }
+}
+
+}  // namespace crmk

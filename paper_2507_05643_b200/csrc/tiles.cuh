@@ -1,0 +1,201 @@
+// tiles.cuh — shared-memory-staged cell tiles for the fused neighbour filter and pair loops.
+//
+// A tile is TX x TY cell columns x TZ cells along z.  With the B3 cell order (z fastest) the
+// particles of one column segment are one contiguous index range, so a tile's "window" — every
+// particle of the 27-cell neighbourhoods of the tile's particles — is WR = (TX+2)(TY+2)
+// contiguous runs.  One CTA per tile stages the window's 56-B states into shared memory once,
+// filters candidates there (Alg. 1) and runs the pair loops from shared memory.
+// Neighbour lists store 16-bit window offsets (list entry = position in the tile window), per
+// particle contiguous (cap entries, 16-B aligned chunks of 8), so they are read and written
+// with 16-B vector accesses.  Windows larger than WMAX are read from global memory instead
+// (same list format, slower; "global mode").
+#pragma once
+#include <cuda_pipeline.h>
+
+#include "common.cuh"
+
+namespace crmk {
+
+constexpr int TX = 2, TY = 2, TZ = 4;
+constexpr int WRX = TX + 2, WRY = TY + 2, WR = WRX * WRY;   // 16 window runs
+constexpr int NCOL = TX * TY;                               // i columns per tile
+constexpr int TILE_THREADS = 288;
+constexpr int WMAX = 1920;                                  // staged window capacity (particles)
+
+struct TileSmem {
+  float4 P[WMAX];
+  float4 U[WMAX];
+  float4 S1[WMAX];
+  float2 S2[WMAX];
+  uint32_t run_start[WR];       // first global index of each window run
+  uint32_t run_base[WR + 1];    // window offset of each run (prefix of lengths)
+  uint32_t wcs[WR][TZ + 3];     // cellStart of the run's cells zlo..zhi, plus the end
+  uint32_t col_start[NCOL];     // first i of each tile column
+  uint32_t col_pref[NCOL + 1];  // prefix of i counts
+  int zlo, zhi, staged, any;
+};
+
+struct TileGeom {
+  int X0, Y0, z0, z1, zlo, zhi;
+};
+
+__host__ __device__ inline int tiles_x(const Grid& g) { return (g.dims[0] + TX - 1) / TX; }
+__host__ __device__ inline int tiles_y(const Grid& g) { return (g.dims[1] + TY - 1) / TY; }
+__host__ __device__ inline int tiles_z(const Grid& g) { return (g.dims[2] + TZ - 1) / TZ; }
+__host__ inline long long num_tiles(const Grid& g) { return (long long)tiles_x(g) * tiles_y(g) * tiles_z(g); }
+
+__device__ __forceinline__ uint32_t cell_id(const Grid& g, int cx, int cy, int cz) {
+  return (uint32_t)cx * (uint32_t)(g.dims[1] * g.dims[2]) + (uint32_t)cy * (uint32_t)g.dims[2] + (uint32_t)cz;
+}
+
+__device__ __forceinline__ TileGeom tile_geom(const Grid& g, long long t) {
+  const int ntz = tiles_z(g), nty = tiles_y(g);
+  TileGeom G;
+  const int tz = (int)(t % ntz);
+  const int ty = (int)((t / ntz) % nty);
+  const int tx = (int)(t / ((long long)ntz * nty));
+  G.X0 = tx * TX;
+  G.Y0 = ty * TY;
+  G.z0 = tz * TZ;
+  G.z1 = min(G.z0 + TZ, g.dims[2]);
+  G.zlo = max(G.z0 - 1, 0);
+  G.zhi = min(G.z1, g.dims[2] - 1);
+  return G;
+}
+
+// Fill the tile geometry in shared memory (all threads call; contains __syncthreads).
+__device__ __forceinline__ void tile_setup(const Grid& g, const TileGeom& G, const uint32_t* __restrict__ cell_start,
+                                          TileSmem& sm) {
+  const int nzw = G.zhi - G.zlo + 1;
+  if (threadIdx.x < WR) {
+    const int r = threadIdx.x;
+    const int cx = G.X0 - 1 + r / WRY, cy = G.Y0 - 1 + r % WRY;
+    const bool valid = cx >= 0 && cx < g.dims[0] && cy >= 0 && cy < g.dims[1];
+    const uint32_t c0 = valid ? cell_id(g, cx, cy, G.zlo) : 0u;
+    for (int k = 0; k <= nzw; ++k) sm.wcs[r][k] = valid ? cell_start[c0 + k] : 0u;
+    sm.run_start[r] = sm.wcs[r][0];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t acc = 0;
+    for (int r = 0; r < WR; ++r) {
+      sm.run_base[r] = acc;
+      acc += sm.wcs[r][nzw] - sm.wcs[r][0];
+    }
+    sm.run_base[WR] = acc;
+    uint32_t ip = 0;
+    for (int q = 0; q < NCOL; ++q) {
+      const int r = (1 + q / TY) * WRY + (1 + q % TY);
+      const uint32_t b = sm.wcs[r][G.z0 - G.zlo], e = sm.wcs[r][G.z1 - G.zlo];
+      sm.col_start[q] = b;
+      sm.col_pref[q] = ip;
+      ip += e - b;
+    }
+    sm.col_pref[NCOL] = ip;
+    sm.zlo = G.zlo;
+    sm.zhi = G.zhi;
+    sm.staged = acc <= (uint32_t)WMAX;
+    sm.any = 0;
+  }
+  __syncthreads();
+}
+
+// Copy the window of (P,U,S1,S2) into shared memory (only when it fits) with asynchronous
+// global->shared copies (LDGSTS): every copy of the block is in flight at once; the caller
+// waits with tile_stage_wait() + __syncthreads().
+__device__ __forceinline__ void tile_stage(const float4* __restrict__ P, const float4* __restrict__ U,
+                                           const float4* __restrict__ S1, const float2* __restrict__ S2, TileSmem& sm) {
+  if (!sm.staged) return;
+  const uint32_t W = sm.run_base[WR];
+  for (uint32_t idx = threadIdx.x; idx < W; idx += blockDim.x) {
+    int r = 0;
+#pragma unroll
+    for (int k = 1; k < WR; ++k) r += (sm.run_base[k] <= idx) ? 1 : 0;
+    const uint32_t gidx = sm.run_start[r] + (idx - sm.run_base[r]);
+    __pipeline_memcpy_async(&sm.P[idx], &P[gidx], sizeof(float4));
+    __pipeline_memcpy_async(&sm.U[idx], &U[gidx], sizeof(float4));
+    __pipeline_memcpy_async(&sm.S1[idx], &S1[gidx], sizeof(float4));
+    __pipeline_memcpy_async(&sm.S2[idx], &S2[gidx], sizeof(float2));
+  }
+  __pipeline_commit();
+}
+
+__device__ __forceinline__ void tile_stage_wait() { __pipeline_wait_prior(0); }
+
+// global index of a window offset (global mode)
+__device__ __forceinline__ uint32_t window_to_global(const TileSmem& sm, uint32_t off) {
+  int r = 0;
+#pragma unroll
+  for (int k = 1; k < WR; ++k) r += (sm.run_base[k] <= off) ? 1 : 0;
+  return sm.run_start[r] + (off - sm.run_base[r]);
+}
+
+// tile-local slot t -> (global i, column q)
+__device__ __forceinline__ uint32_t tile_particle(const TileSmem& sm, uint32_t t, int& q) {
+  q = 0;
+#pragma unroll
+  for (int k = 1; k < NCOL; ++k) q += (sm.col_pref[k] <= t) ? 1 : 0;
+  return sm.col_start[q] + (t - sm.col_pref[q]);
+}
+
+// candidate window-offset range of run (da, db) for a particle of column q at cell z = cz
+__device__ __forceinline__ void cand_range(const TileSmem& sm, int q, int da, int db, int cz, uint32_t& ob,
+                                           uint32_t& oe, int& r) {
+  r = (1 + q / TY + da) * WRY + (1 + q % TY + db);
+  const int klo = max(cz - 1, sm.zlo) - sm.zlo;
+  const int khi = min(cz + 1, sm.zhi) - sm.zlo + 1;
+  const uint32_t rs = sm.run_start[r], rb = sm.run_base[r];
+  ob = rb + (sm.wcs[r][klo] - rs);
+  oe = rb + (sm.wcs[r][khi] - rs);
+}
+
+// 16-bit list writer: 8 entries per 16-B store (funnel-shift register buffer)
+struct ListWriter {
+  uint4* dst;        // per-particle segment (cap entries)
+  uint32_t b0, b1, b2, b3;
+  int nb;            // entries in the buffer
+  int k;             // entries stored or buffered
+  int cap;
+  __device__ __forceinline__ void init(uint16_t* list, size_t i, int cap_) {
+    dst = reinterpret_cast<uint4*>(list + i * (size_t)cap_);
+    b0 = b1 = b2 = b3 = 0u;
+    nb = 0;
+    k = 0;
+    cap = cap_;
+  }
+  __device__ __forceinline__ void push(uint32_t off) {
+    if (k >= cap) { ++k; return; }
+    b0 = __funnelshift_r(b0, b1, 16);
+    b1 = __funnelshift_r(b1, b2, 16);
+    b2 = __funnelshift_r(b2, b3, 16);
+    b3 = __funnelshift_r(b3, off, 16);
+    ++nb;
+    ++k;
+    if (nb == 8) {
+      dst[(k - 8) >> 3] = make_uint4(b0, b1, b2, b3);
+      nb = 0;
+    }
+  }
+  // pad the last chunk with `fill` (the particle's own window offset: a zero-weight entry, so the
+  // pair loops run whole chunks of 8 without per-entry branches)
+  __device__ __forceinline__ void flush(uint32_t fill) {
+    if (nb == 0) return;
+    const int pad = 8 - nb;
+    for (int p = 0; p < pad; ++p) {
+      b0 = __funnelshift_r(b0, b1, 16);
+      b1 = __funnelshift_r(b1, b2, 16);
+      b2 = __funnelshift_r(b2, b3, 16);
+      b3 = __funnelshift_r(b3, fill, 16);
+    }
+    const int kk = min(k, cap);
+    dst[(kk - 1) >> 3] = make_uint4(b0, b1, b2, b3);
+    nb = 0;
+  }
+};
+
+__device__ __forceinline__ uint32_t list_entry(const uint4& v, int e) {
+  const uint32_t w = (e < 2) ? v.x : (e < 4) ? v.y : (e < 6) ? v.z : v.w;
+  return (e & 1) ? (w >> 16) : (w & 0xffffu);
+}
+
+}  // namespace crmk

@@ -53,7 +53,7 @@ def test_strerror_and_kernel_names(lib):
     assert lib.crm_strerror(0) == b"ok"
     assert lib.crm_strerror(-2) == b"particle outside the grid box"
     names = crm.kernel_names()
-    assert "k_rates_B" in names and "k_neighbors" in names
+    assert "k_rates_B" in names and "k_bce_A" in names
 
 
 def test_invalid_parameters_rejected_before_device(lib):

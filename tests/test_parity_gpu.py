@@ -233,3 +233,24 @@ def test_get_set_state_roundtrip(crm):
     g2.set_state(0, *st)
     for x, y in zip(g2.get_state(), st):
         assert np.array_equal(x, y)
+
+
+def test_dense_windows_global_mode(crm):
+    # h = 2 d0: ~64 particles per cell, tile windows exceed the shared-memory capacity, so the
+    # kernels read the window from global memory ("global mode"); results must not change
+    sc = workloads.rate_state_S0(workloads.block_settle(n=(12, 12, 12)))
+    sc.params["h"] = 2.0 * sc.params["d0"]
+    L = workloads.bce_layers(sc.params["h"], sc.params["d0"])
+    sc.wall_pos = workloads.f32(workloads.box_walls(12, 12, 12, sc.params["d0"], L, 2))
+    m = (L + 1) * sc.params["d0"]
+    sc.params["lo"] = (-m, -m, -m)
+    sc.params["hi"] = (12 * sc.params["d0"] + m, 12 * sc.params["d0"] + m, 24 * sc.params["d0"])
+    g, o = both(crm, sc)
+    assert_structure_equal(g, o)
+    g.debug_arm(True)
+    g.step(sc.dt, 1)
+    o.step(sc.dt, 1)
+    nf = sc.n_fluid
+    for stage in (0, 1):
+        for a, b in zip(g.last_rates(stage), o.last_rates(stage)):
+            assert rel_linf(a[:nf], b[:nf]) <= RATE_TOL
