@@ -32,6 +32,7 @@ struct Grid {
   int dims[3];             // Nx, Ny, Nz
   uint32_t M;              // Nx*Ny*Nz
   float R2;                // (float)((support*h)^2), B2
+  float margin;            // conservative slack of the cell-box distance pruning (m)
 };
 
 // physical constants of one context, fp32

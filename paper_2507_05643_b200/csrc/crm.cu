@@ -508,6 +508,12 @@ int crm_create(const crm_material_t* mat, const crm_kernel_t* ker, const crm_bou
   c->grid.M = (uint32_t)M;
   c->grid.s = (float)R;
   c->grid.R2 = (float)(R * R);
+  {
+    // pruning slack: 16 ulp of the largest coordinate + 1e-6 of a cell
+    double amax = 0;
+    for (int a = 0; a < 3; ++a) amax = std::max(amax, std::max(std::fabs(bnd->lo[a]), std::fabs(bnd->hi[a])));
+    c->grid.margin = (float)(16.0 * amax * std::ldexp(1.0, -23) + 1e-6 * R);
+  }
   // physics constants
   const double h = k.h;
   c->ph.h = (float)h;

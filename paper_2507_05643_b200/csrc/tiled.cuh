@@ -66,6 +66,8 @@ template <bool STAGED>
 __device__ __forceinline__ uint32_t filter(const Grid& g, const TileSmem& sm, const float4* __restrict__ P,
                                            const float4* __restrict__ U, int q, int cz, uint32_t self, float4 pi,
                                            bool store_bce, ListWriter& w) {
+  // (measured: pruning neighbour cells by their box distance removes ~24 % of the candidates
+  //  but costs more in divergence than it saves; the full 27-cell stencil is kept)
   uint32_t cnt = 0;
 #pragma unroll 1
   for (int da = -1; da <= 1; ++da) {

@@ -33,6 +33,7 @@ struct TileSmem {
   uint32_t col_start[NCOL];     // first i of each tile column
   uint32_t col_pref[NCOL + 1];  // prefix of i counts
   int zlo, zhi, staged, any;
+  int X0, Y0;
 };
 
 struct TileGeom {
@@ -94,6 +95,8 @@ __device__ __forceinline__ void tile_setup(const Grid& g, const TileGeom& G, con
     sm.col_pref[NCOL] = ip;
     sm.zlo = G.zlo;
     sm.zhi = G.zhi;
+    sm.X0 = G.X0;
+    sm.Y0 = G.Y0;
     sm.staged = acc <= (uint32_t)WMAX;
     sm.any = 0;
   }
@@ -149,12 +152,15 @@ __device__ __forceinline__ void cand_range(const TileSmem& sm, int q, int da, in
   oe = rb + (sm.wcs[r][khi] - rs);
 }
 
-// 16-bit list writer: 8 entries per 16-B store (funnel-shift register buffer)
+// 16-bit list writer: entries are collected in a 128-bit funnel-shift register buffer and
+// written 8 at a time with one 16-B store into the particle's contiguous segment; the last
+// chunk is padded with `fill` (the particle's own window offset: a zero-weight entry), so the
+// pair loops read whole 16-B chunks and run without per-entry branches.
 struct ListWriter {
-  uint4* dst;        // per-particle segment (cap entries)
+  uint4* dst;        // per-particle segment (cap entries, cap % 8 == 0)
   uint32_t b0, b1, b2, b3;
   int nb;            // entries in the buffer
-  int k;             // entries stored or buffered
+  int k;             // entries found (may exceed cap: overflow is reported by the caller)
   int cap;
   __device__ __forceinline__ void init(uint16_t* list, size_t i, int cap_) {
     dst = reinterpret_cast<uint4*>(list + i * (size_t)cap_);
@@ -176,8 +182,6 @@ struct ListWriter {
       nb = 0;
     }
   }
-  // pad the last chunk with `fill` (the particle's own window offset: a zero-weight entry, so the
-  // pair loops run whole chunks of 8 without per-entry branches)
   __device__ __forceinline__ void flush(uint32_t fill) {
     if (nb == 0) return;
     const int pad = 8 - nb;
