@@ -48,6 +48,8 @@ FLOPS_EPILOGUE = {"k_rates_A": 110, "k_rates_B": 170}
 BYTES_PER_FLUID_UPDATE = 404
 BYTES_PER_BCE_UPDATE = 72
 # per-kernel algorithmic bytes per particle (for HBM-bound kernels)
+# bounded oracle sample of the bed workload (~1M fluid; ~1 s per oracle step on a 16-core host)
+SAMPLE_BED = (128, 128, 64)
 KERNEL_BYTES = {"k_bin": 16 + 4 + 8 + 4, "k_scatter": 12 + 8, "k_reorder": 56 + 56 + 24 + 8}
 
 
@@ -135,8 +137,9 @@ def oracle_rate(name: str, steps: int):
     import oracle
     oracle.build()
     if name.startswith("bed"):
-        sample = workloads.bed(n=(64, 64, 64))
-        desc = "64x64x64-fluid sub-bed (262,144 fluid + walls) of the bed recipe (same d0, h, material, dt)"
+        sample = workloads.bed(n=SAMPLE_BED)
+        desc = (f"{SAMPLE_BED[0]}x{SAMPLE_BED[1]}x{SAMPLE_BED[2]}-fluid sub-bed of the bed recipe "
+                "(same d0, h, material, dt)")
     else:
         sample = scenario(name)
         desc = f"full {name} workload"
@@ -155,7 +158,7 @@ def run_reference(args):
     cb = oracle_rate(args.config, max(1, args.steps + args.warmup) if args.config == "block8k" else 1)
     # warm-up + timed steps of the oracle itself on the sample (bounded: one sample step per bench step)
     import oracle
-    sample = workloads.bed(n=(64, 64, 64)) if args.config.startswith("bed") else scenario(args.config)
+    sample = workloads.bed(n=SAMPLE_BED) if args.config.startswith("bed") else scenario(args.config)
     s = oracle.load_scenario(sample)
     s.step(sample.dt, args.warmup)
     t0 = time.perf_counter()
@@ -305,7 +308,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = oracle_rate(args.config, 1)
+        cpu = oracle_rate(args.config, 12)
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

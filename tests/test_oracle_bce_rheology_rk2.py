@@ -211,3 +211,30 @@ def test_rk2_self_convergence_order(oracle_mod):
     e = [np.abs(_blob_run(oracle_mod, dt0 / k, T) - ref).max() for k in (1, 2)]
     order = math.log2(e[0] / e[1])
     assert 1.7 <= order <= 2.3, (e, order)
+
+
+def test_body_loads_newton_third_law(oracle_mod):
+    # A13 / S:439: the force on a body equals minus the force its markers exert on the fluid, so with
+    # no gravity and no walls sum_f m a_f (stage B) + F_body = 0
+    rng = np.random.default_rng(21)
+    d0 = 0.01
+    pos = workloads.lattice_block(10, 10, 6, d0) + rng.uniform(-0.1, 0.1, (600, 3)) * d0
+    vel = rng.normal(0, 0.1, pos.shape)
+    sig = rng.normal(0, 300, (600, 6)) + np.array([-1500, -1500, -1500, 0, 0, 0])
+    blk = workloads.lattice_block(4, 4, 3, d0, origin=(3 * d0, 3 * d0, 6 * d0))
+    p = workloads.base_params(rho0=1500.0, mu_s=0.5, mu_2=0.5, I0=0.08, cohesion=0.0, grain_d=1e-3, d0=d0,
+                              h=1.3 * d0, visc_mode=0, gamma_a=0.2, lo=(-0.05,) * 3, hi=(0.2,) * 3,
+                              gravity=(0.0, 0.0, 0.0))
+    s = oracle_mod.OracleSim(p)
+    s.add_fluid(pos, vel, sig)
+    body = workloads.Body(mass=1.0, inertia=(1, 1, 1), pos=tuple(blk.mean(0)), vel=(0.0, 0.0, -0.2),
+                          motion=workloads.BODY_PRESCRIBED, markers=blk)
+    bid = s.add_body(body)
+    s.add_bce(bid, blk)
+    s.step(1e-5, 1)
+    _, acc, _ = s.last_rates(1)
+    m = p["rho0"] * d0 ** 3
+    F_fluid = m * acc[:600].sum(0)
+    F_body = s.get_body(bid)["force"]
+    assert np.abs(F_body).max() > 0
+    assert np.allclose(F_fluid + F_body, 0, atol=1e-10 * (np.abs(m * acc[:600]).sum()))
