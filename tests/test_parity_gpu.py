@@ -254,3 +254,29 @@ def test_dense_windows_global_mode(crm):
     for stage in (0, 1):
         for a, b in zip(g.last_rates(stage), o.last_rates(stage)):
             assert rel_linf(a[:nf], b[:nf]) <= RATE_TOL
+
+
+# ---------------------------------------------------------------- rigid bodies (A9, C2 shape)
+def test_crater_body_loads_and_penetration(crm):
+    # desk-scale cratering (d0 = 5 mm): 28 x 20 x 30 soil, R = 12.5 mm sphere (rho_s = 2200)
+    # entering at sqrt(2 g H), H = 0.1 m.  Stage-B marker accelerations (A13) and the body force at
+    # 1e-4; 100-step penetration within 2 %.
+    sc = workloads.cratering(rho_s=2200.0, H_drop=0.1, d0=5e-3)
+    g, o = both(crm, sc)
+    g.debug_arm(True)
+    g.step(sc.dt, 1)
+    o.step(sc.dt, 1)
+    nf, nw = sc.n_fluid, sc.wall_pos.shape[0]
+    ag = g.last_rates(1)[1][nf + nw:]
+    ao = o.last_rates(1)[1][nf + nw:]
+    assert np.abs(ao).max() > 0
+    assert rel_linf(ag, ao) <= RATE_TOL
+    bg, bo = g.get_body(1), o.get_body(1)
+    assert rel_linf(bg["force"], bo["force"]) <= RATE_TOL
+    g.step(sc.dt, 99)
+    o.step(sc.dt, 99)
+    z0 = sc.bodies[0].pos[2]
+    dg = z0 - g.get_body(1)["pos"][2]
+    do = z0 - o.get_body(1)["pos"][2]
+    assert do > 0.002
+    assert abs(dg - do) <= 0.02 * do
