@@ -45,7 +45,7 @@ extern "C" {
 #define CRM_E_INVALID     -1   /* bad argument: h <= 0, d0 <= 0, h < d0, dt <= 0, mu_s > mu_2, K/G <= 0 ... */
 #define CRM_E_DOMAIN      -2   /* a particle left the fixed grid box (reading A19) */
 #define CRM_E_NONFINITE   -3   /* non-finite fluid state after a step */
-#define CRM_E_UNSUPPORTED -4   /* Wendland kernel / Holmes extrapolation / world > 1 not built */
+#define CRM_E_UNSUPPORTED -4   /* Wendland kernel / Holmes extrapolation / ps_freq > 1 not built */
 #define CRM_E_STATE       -5   /* crm_add_* after the first step, debug data not available */
 #define CRM_E_OOM         -6   /* device or host allocation failed */
 #define CRM_E_CUDA        -7   /* CUDA runtime error, or no sm_100 device */
@@ -130,8 +130,26 @@ int  crm_add_bce(crm_t* ctx, int32_t body, int64_t n, const double* pos_world, i
 
 /* Advance nsteps explicit RK2 steps of size dt (synchronous).  Returns the first error latched
  * on the device (CRM_E_DOMAIN, CRM_E_NONFINITE, CRM_E_CAPACITY) with the id and step in
- * crm_last_error. */
+ * crm_last_error.  With world > 1 and an NCCL id, every rank calls crm_step with the same
+ * arguments; ghost planes are exchanged with NCCL point-to-point transfers (CRM_E_COMM). */
 int  crm_step(crm_t* ctx, double dt, int64_t nsteps);
+
+/* ---- multi-GPU slab decomposition along x ----
+ * A context created with crm_dist_t.world > 1 owns the cell planes [x_lo, x_hi) chosen from a
+ * prefix sum of per-plane particle counts of the (identical) global crm_add_* input.  Every rank
+ * passes the same global arrays; the library keeps its slab.  crm_get_state then fills only the
+ * rows of owned ids (other rows are NaN) and crm_count(ctx, CRM_OWNED) counts them.  Moving
+ * bodies and the debug exports are single-GPU only in this build (CRM_E_UNSUPPORTED). */
+/* Step `world` contexts of ranks 0..world-1 living in one process on one device and stream
+ * (nccl_id NULL): exchanges become device copies ("loopback"); used to test the decomposition
+ * on one GPU.  Owned particles follow bit-identical trajectories to a one-context run. */
+int  crm_group_step(crm_t** ctxs, int world, double dt, int64_t nsteps);
+/* 128-byte ncclUniqueId for crm_dist_t.nccl_id (call on one rank, broadcast to the others). */
+int  crm_nccl_unique_id(void* out128);
+/* Pure host helper: slab boundaries bounds[0..world] (bounds[0] = 0, bounds[world] = nplanes,
+ * interior ones multiples of `align`) balancing the per-plane particle counts.  CRM_E_INVALID if
+ * nplanes < world * align. */
+int  crm_slab_partition(const int64_t* plane_counts, int nplanes, int world, int align, int* bounds);
 
 /* Copy state of ids [first_id, first_id + count) to host fp64 arrays (any pointer may be NULL).
  * For markers: the last extrapolated u and sigma, rho = rho0. */

@@ -22,12 +22,27 @@ def _sources():
                   + [os.path.join(ROOT, "include", "crm.h")])
 
 
+def nccl_paths():
+    """(include dir, library path) of the NCCL shipped with the environment (nvidia-nccl wheel).
+    Only the header is needed to build; libnccl.so.2 is dlopen'ed at run time for world > 1."""
+    try:
+        import nvidia.nccl
+        base = list(nvidia.nccl.__path__)[0]
+        return os.path.join(base, "include"), os.path.join(base, "lib", "libnccl.so.2")
+    except Exception:
+        return None, None
+
+
 def build_library(force: bool = False, verbose: bool = False) -> str:
     srcs = _sources()
     if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= max(os.path.getmtime(s) for s in srcs):
         return LIB
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, "-o", LIB + ".tmp", os.path.join(CSRC, "crm.cu")]
+    inc, lib = nccl_paths()
+    if inc is None:
+        raise RuntimeError("nccl.h not found (nvidia-nccl wheel)")
+    cmd = [nvcc, *NVCC_FLAGS, "-I", inc, f'-DCRM_NCCL_DEFAULT="{lib}"', "-o", LIB + ".tmp",
+           os.path.join(CSRC, "crm.cu"), "-ldl"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.check_call(cmd, cwd=ROOT)

@@ -24,7 +24,7 @@ EXPORTS = [
     "crm_get_state", "crm_set_state", "crm_get_body", "crm_count", "crm_last_error", "crm_strerror",
     "crm_stream", "crm_launch_count", "crm_profile_enable", "crm_profile_read", "crm_profile_reset",
     "crm_kernel_name", "crm_set_graphs", "crm_debug_arm", "crm_debug_structure", "crm_debug_neighbors",
-    "crm_debug_rates", "crm_debug_bce",
+    "crm_debug_rates", "crm_debug_bce", "crm_group_step", "crm_nccl_unique_id", "crm_slab_partition",
 ]
 
 
@@ -95,8 +95,39 @@ def load_library(path: str = LIB_PATH):
     L.crm_debug_neighbors.argtypes = [vp, _I64, _I64]
     L.crm_debug_rates.argtypes = [vp, C.c_int, _D, _D, _D]
     L.crm_debug_bce.argtypes = [vp, C.c_int, _D, _D]
+    L.crm_group_step.argtypes = [C.POINTER(vp), C.c_int, C.c_double, C.c_int64]
+    L.crm_nccl_unique_id.argtypes = [C.c_void_p]
+    L.crm_slab_partition.argtypes = [_I64, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int)]
     _lib = L
     return L
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId (rank 0 creates it, torch.distributed broadcasts it)."""
+    buf = C.create_string_buffer(128)
+    rc = load_library().crm_nccl_unique_id(buf)
+    if rc:
+        raise CrmError(rc, "crm_nccl_unique_id")
+    return buf.raw
+
+
+def slab_partition(plane_counts, world: int, align: int = 2) -> np.ndarray:
+    """Slab boundaries (world + 1 plane indices) balancing per-plane counts (host only)."""
+    pc = np.ascontiguousarray(plane_counts, dtype=np.int64)
+    out = (C.c_int * (world + 1))()
+    rc = load_library().crm_slab_partition(pc.ctypes.data_as(_I64), len(pc), world, align, out)
+    if rc:
+        raise CrmError(rc, "crm_slab_partition")
+    return np.array(out[:], dtype=np.int64)
+
+
+def group_step(ctxs, dt: float, n: int = 1):
+    """Step in-process slab contexts (ranks 0..W-1 on one device/stream) with loopback halos."""
+    arr = (C.c_void_p * len(ctxs))(*[c.h.value for c in ctxs])
+    rc = load_library().crm_group_step(arr, len(ctxs), float(dt), int(n))
+    if rc:
+        msgs = "; ".join(c._L.crm_last_error(c.h).decode() for c in ctxs)
+        raise CrmError(rc, f"crm_group_step: {msgs}")
 
 
 class CrmError(RuntimeError):
@@ -130,7 +161,8 @@ def kernel_names() -> list[str]:
 class Crm:
     """One simulation context on one GPU (crm_create ... crm_destroy)."""
 
-    def __init__(self, params: dict, *, device: int = 0, stream: int | None = None, max_neighbors: int = 0):
+    def __init__(self, params: dict, *, device: int = 0, stream: int | None = None, max_neighbors: int = 0,
+                 rank: int = 0, world: int = 1, nccl_id: bytes | None = None):
         self._L = load_library()
         m = Material(params["rho0"], params["K"], params["G"], params["mu_s"], params["mu_2"], params["I0"],
                      params["cohesion"], params["grain_d"])
@@ -144,7 +176,8 @@ class Crm:
         b = Boundary()
         b.method = 0; b.n_layers = 0
         b.lo = (C.c_double * 3)(*params["lo"]); b.hi = (C.c_double * 3)(*params["hi"]); b.slab_axis = 0
-        d = Dist(0, 1, device, None, stream)
+        self._nccl_id = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+        d = Dist(rank, world, device, C.cast(self._nccl_id, C.c_void_p) if self._nccl_id is not None else None, stream)
         h = C.c_void_p()
         rc = self._L.crm_create(C.byref(m), C.byref(k), C.byref(b), C.byref(d), C.byref(h))
         if rc:

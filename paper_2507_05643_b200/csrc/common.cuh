@@ -20,10 +20,15 @@ namespace crmk {
 __host__ __device__ __forceinline__ uint32_t make_tag(uint32_t kind, uint32_t body, uint32_t moving) {
   return (kind & 1u) | ((body & 0x7fffu) << 1) | ((moving & 1u) << 16);
 }
+//   bit 17     : ghost copy of a neighbour slab's particle (multi-GPU)
+//   bit 18     : dropped at the next sort (migrated to a neighbour slab)
+constexpr uint32_t TAG_GHOST = 1u << 17;
+constexpr uint32_t TAG_DROP = 1u << 18;
 __device__ __forceinline__ uint32_t tag_of(float w) { return __float_as_uint(w); }
 __device__ __forceinline__ bool tag_is_bce(uint32_t t) { return t & 1u; }
 __device__ __forceinline__ uint32_t tag_body(uint32_t t) { return (t >> 1) & 0x7fffu; }
 __device__ __forceinline__ bool tag_moving(uint32_t t) { return (t >> 16) & 1u; }
+__device__ __forceinline__ bool tag_ghost(uint32_t t) { return (t & TAG_GHOST) != 0u; }
 
 // fixed grid (reading A19); cells of size s = support*h
 struct Grid {

@@ -1,220 +1,16 @@
 // crm.cu — libcrm.so: the C-ABI of include/crm.h and the host orchestration of one step.
 //
-// One crm_step(dt, n) issues, per step, on the context's stream (DESIGN.md §Step):
+// One crm_step(dt, n) issues, per step, on the context's stream (DESIGN.md §1, §6):
 //   memset counts | k_bin | scan (k_scan_tiles, k_scan_add) | k_scatter | k_reorder |
 //   k_bce_t<0> (marker filter + extrapolation) | k_rates_t<0> (fluid filter + rates + half step) |
 //   [k_markers_place(mid)] | k_bce_t<1> | k_rates_t<1> (rates + full step + return map) |
 //   [k_body_update | k_body_poses | k_markers_place]
-// and synchronises once at the end to read the device error latch.  The step sequence can
-// be captured once in a CUDA graph per (dt, buffer parity) and replayed.
-#include <cuda_runtime.h>
-
-#include <algorithm>
-#include <cmath>
-#include <cstdio>
-#include <cstring>
-#include <string>
-#include <vector>
-
-#include "../../include/crm.h"
-#include "common.cuh"
-#include "physics.cuh"
-#include "structure.cuh"
-#include "tiled.cuh"
-
-using namespace crmk;
+// and synchronises once at the end to read the device error latch.  With world > 1 the same
+// kernels run per slab, interleaved with halo exchanges (dist.cuh).
+#include "context.cuh"
+#include "dist.cuh"
 
 namespace {
-
-enum KernelId {
-  KID_MARKERS = 0, KID_BIN, KID_SCAN, KID_SCAN_ADD, KID_SCATTER, KID_REORDER,
-  KID_BCE_A, KID_RATES_A, KID_BCE_B, KID_RATES_B, KID_BODY, KID_POSES, KID_STATE, KID_COPY, KID_DECODE,
-  KID_COUNT
-};
-const char* kKernelNames[KID_COUNT] = {"k_markers_place", "k_bin", "k_scan_tiles", "k_scan_add", "k_scatter",
-                                       "k_reorder", "k_bce_A", "k_rates_A", "k_bce_B", "k_rates_B",
-                                       "k_body_update", "k_body_poses", "k_get_set_state", "k_copy_u32",
-                                       "k_decode_lists"};
-
-struct ProfRec {
-  int kid;
-  cudaEvent_t a, b;
-};
-
-}  // namespace
-
-struct crm {
-  crm_material_t mat{};
-  crm_kernel_t ker{};
-  crm_boundary_t bnd{};
-  Grid grid{};
-  Phys ph{};
-  double support = 2.0;
-  int cap = 0;
-  int device = 0;
-  cudaStream_t stream = nullptr;
-  bool own_stream = false;
-
-  // host staging (id order) until the first device use
-  std::vector<float4> hP, hU, hS1;
-  std::vector<float2> hS2;
-  std::vector<int32_t> hBody;   // -1 for fluid
-  std::vector<BodyState> bodies;
-  int64_t n = 0, n_fluid = 0, n_bce = 0;
-  bool committed = false;
-  int64_t steps_done = 0;
-
-  // device state
-  float4 *P[2] = {nullptr, nullptr}, *U[2] = {nullptr, nullptr}, *S1[2] = {nullptr, nullptr};
-  float2* S2[2] = {nullptr, nullptr};
-  uint32_t* ids[2] = {nullptr, nullptr};
-  int cur = 0;
-  float4 *Pm = nullptr, *Um = nullptr, *S1m = nullptr;
-  float2* S2m = nullptr;
-  uint32_t *key = nullptr, *arrival = nullptr, *cell_count = nullptr, *cell_start = nullptr;
-  uint32_t *tmp_src = nullptr, *tmp_id = nullptr, *cell_of = nullptr, *slot_of_id = nullptr;
-  uint16_t* list = nullptr;             // hot-path lists: window offsets, cap per particle
-  uint32_t *nlist = nullptr, *count_all = nullptr;
-  uint32_t* list32 = nullptr;           // debug only: global indices, ELL k-major
-  long long ntiles = 0;
-  bool attrs_set = false;
-  std::vector<uint32_t*> scan_sums, scan_sums_x;
-  std::vector<long long> scan_len;
-  BodyState* d_bodies = nullptr;
-  Pose *d_pose0 = nullptr, *d_posem = nullptr;
-  uint32_t* d_moving_ids = nullptr;
-  float4* d_xlocal = nullptr;
-  uint32_t* d_mstart = nullptr;
-  int* d_moving_bodies = nullptr;
-  int n_moving_markers = 0, n_moving_bodies = 0;
-  float4* macc = nullptr;
-  ErrLatch* d_err = nullptr;
-  ErrLatch* h_err = nullptr;
-  Debug dbg{};
-  uint32_t* dbg_ids = nullptr;
-  bool dbg_on = false, dbg_valid = false;
-  double* d_stage = nullptr;
-  size_t stage_cap = 0;
-  double poses_dt = -1.0;
-
-  // graphs
-  bool graphs = true;
-  cudaGraphExec_t gexec[2] = {nullptr, nullptr};
-  double graph_dt[2] = {-1.0, -1.0};
-  bool graph_dbg[2] = {false, false};
-  long long* d_step = nullptr;
-
-  // profiling
-  bool prof = false;
-  std::vector<ProfRec> recs;
-  std::vector<cudaEvent_t> ev_pool;
-  double prof_ms[KID_COUNT] = {0};
-  int64_t prof_n[KID_COUNT] = {0};
-  int64_t launches = 0;
-
-  std::string err;
-};
-
-// ---------------------------------------------------------------------------------------
-namespace {
-
-int fail(crm_t* c, int code, const std::string& msg) {
-  if (c) c->err = msg;
-  return code;
-}
-
-#define CK(call)                                                                          \
-  do {                                                                                    \
-    cudaError_t e_ = (call);                                                              \
-    if (e_ != cudaSuccess) {                                                              \
-      return fail(c, e_ == cudaErrorMemoryAllocation ? CRM_E_OOM : CRM_E_CUDA,            \
-                  std::string(#call) + ": " + cudaGetErrorString(e_));                    \
-    }                                                                                     \
-  } while (0)
-
-cudaEvent_t get_event(crm_t* c) {
-  if (!c->ev_pool.empty()) {
-    cudaEvent_t e = c->ev_pool.back();
-    c->ev_pool.pop_back();
-    return e;
-  }
-  cudaEvent_t e;
-  cudaEventCreate(&e);
-  return e;
-}
-
-void prof_flush(crm_t* c) {
-  if (c->recs.empty()) return;
-  cudaStreamSynchronize(c->stream);
-  for (auto& r : c->recs) {
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, r.a, r.b);
-    c->prof_ms[r.kid] += ms;
-    c->prof_n[r.kid] += 1;
-    c->ev_pool.push_back(r.a);
-    c->ev_pool.push_back(r.b);
-  }
-  c->recs.clear();
-}
-
-template <typename Kern, typename... Args>
-void launch(crm_t* c, int kid, Kern kern, dim3 grid, dim3 block, Args... args) {
-  if (grid.x == 0) return;
-  cudaEvent_t a = nullptr, b = nullptr;
-  if (c->prof) {
-    a = get_event(c);
-    cudaEventRecord(a, c->stream);
-  }
-  kern<<<grid, block, 0, c->stream>>>(args...);
-  c->launches++;
-  if (c->prof) {
-    b = get_event(c);
-    cudaEventRecord(b, c->stream);
-    c->recs.push_back({kid, a, b});
-    if (c->recs.size() > 4096) prof_flush(c);
-  }
-}
-
-template <typename Kern, typename... Args>
-void launch_smem(crm_t* c, int kid, Kern kern, dim3 grid, dim3 block, size_t smem, Args... args) {
-  if (grid.x == 0) return;
-  cudaEvent_t a = nullptr, b = nullptr;
-  if (c->prof) {
-    a = get_event(c);
-    cudaEventRecord(a, c->stream);
-  }
-  kern<<<grid, block, smem, c->stream>>>(args...);
-  c->launches++;
-  if (c->prof) {
-    b = get_event(c);
-    cudaEventRecord(b, c->stream);
-    c->recs.push_back({kid, a, b});
-    if (c->recs.size() > 4096) prof_flush(c);
-  }
-}
-
-inline float u2f(uint32_t u) {
-  float f;
-  std::memcpy(&f, &u, 4);
-  return f;
-}
-
-inline unsigned blocks(long long n, int bs) { return (unsigned)((n + bs - 1) / bs); }
-
-template <typename T>
-int dalloc(crm_t* c, T** p, size_t count) {
-  if (count == 0) count = 1;
-  cudaError_t e = cudaMalloc((void**)p, count * sizeof(T));
-  if (e != cudaSuccess) return fail(c, CRM_E_OOM, std::string("cudaMalloc failed: ") + cudaGetErrorString(e));
-  return CRM_OK;
-}
-
-void host_quat_R(const double q[4], double R[9]) {
-  const double w = q[0], x = q[1], y = q[2], z = q[3];
-  R[0] = 1 - 2 * (y * y + z * z); R[1] = 2 * (x * y - w * z);     R[2] = 2 * (x * z + w * y);
-  R[3] = 2 * (x * y + w * z);     R[4] = 1 - 2 * (x * x + z * z); R[5] = 2 * (y * z - w * x);
-  R[6] = 2 * (x * z - w * y);     R[7] = 2 * (y * z + w * x);     R[8] = 1 - 2 * (x * x + y * y);
-}
 
 // exclusive scan out[0..n] (out[n] = total) of in[0..n) using preallocated level buffers
 void scan_u32(crm_t* c, const uint32_t* in, uint32_t* out, long long n, int level) {
@@ -231,7 +27,7 @@ void scan_u32(crm_t* c, const uint32_t* in, uint32_t* out, long long n, int leve
 
 int alloc_debug(crm_t* c) {
   if (c->dbg.drho[0]) return CRM_OK;
-  const size_t n = (size_t)c->n;
+  const size_t n = (size_t)c->ncap;
   int r = 0;
   for (int s = 0; s < 2; ++s) {
     r |= dalloc(c, &c->dbg.drho[s], n); r |= dalloc(c, &c->dbg.acc[s], n);
@@ -242,13 +38,55 @@ int alloc_debug(crm_t* c) {
   return r ? CRM_E_OOM : CRM_OK;
 }
 
-void set_attrs(crm_t* c);
+void set_attrs(crm_t* c) {
+  if (c->attrs_set) return;
+  const int sm = (int)sizeof(TileSmem);
+  cudaFuncSetAttribute(k_bce_t<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  cudaFuncSetAttribute(k_bce_t<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  cudaFuncSetAttribute(k_rates_t<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  cudaFuncSetAttribute(k_rates_t<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  c->attrs_set = true;
+}
 
 int commit(crm_t* c) {
   if (c->committed) return CRM_OK;
   if (c->n <= 0) return fail(c, CRM_E_STATE, "no particles added");
   if (c->n >= (int64_t)0xffffffffLL) return fail(c, CRM_E_INVALID, "too many particles for 32-bit indices");
-  const size_t n = (size_t)c->n;
+  // ---- which particles are local (slab mode: the owned planes only; ghosts come with step 1)
+  std::vector<uint32_t> owned;
+  if (c->slab) {
+    for (size_t b = 1; b < c->bodies.size(); ++b)
+      if (c->bodies[b].motion != CRM_BODY_FIXED)
+        return fail(c, CRM_E_UNSUPPORTED, "moving bodies are not supported with world > 1 in this build");
+    const int Nx = c->grid.dims[0];
+    std::vector<int64_t> counts(Nx, 0);
+    std::vector<int> plane(c->n);
+    for (int64_t i = 0; i < c->n; ++i) {
+      const int p = host_plane(c->grid, c->hP[i].x);
+      if (p < 0 || p >= Nx) return fail(c, CRM_E_DOMAIN, "particle id " + std::to_string(i) + " outside the grid box");
+      plane[i] = p;
+      counts[p]++;
+    }
+    std::vector<int> bounds(c->world + 1);
+    if (slab_partition(counts.data(), Nx, c->world, TX, bounds.data()))
+      return fail(c, CRM_E_INVALID, "grid too narrow for the number of slabs");
+    c->x_lo = bounds[c->rank];
+    c->x_hi = bounds[c->rank + 1];
+    int64_t maxp = 0, own = 0;
+    for (int p = 0; p < Nx; ++p) maxp = std::max(maxp, counts[p]);
+    for (int p = c->x_lo; p < c->x_hi; ++p) own += counts[p];
+    owned.reserve(own);
+    for (int64_t i = 0; i < c->n; ++i)
+      if (plane[i] >= c->x_lo && plane[i] < c->x_hi) owned.push_back((uint32_t)i);
+    c->ncap = own + own / 4 + 6 * maxp + 4096;
+  } else {
+    c->x_lo = 0;
+    c->x_hi = c->grid.dims[0];
+    c->ncap = c->n;
+  }
+  c->nl = c->slab ? (int64_t)owned.size() : c->n;
+  c->n_owned = c->nl;
+  const size_t n = (size_t)c->ncap;
   int r = 0;
   for (int b = 0; b < 2; ++b) {
     r |= dalloc(c, &c->P[b], n); r |= dalloc(c, &c->U[b], n); r |= dalloc(c, &c->S1[b], n);
@@ -256,28 +94,32 @@ int commit(crm_t* c) {
   }
   r |= dalloc(c, &c->Pm, n); r |= dalloc(c, &c->Um, n); r |= dalloc(c, &c->S1m, n); r |= dalloc(c, &c->S2m, n);
   r |= dalloc(c, &c->key, n); r |= dalloc(c, &c->arrival, n);
-  r |= dalloc(c, &c->cell_count, (size_t)c->grid.M); r |= dalloc(c, &c->cell_start, (size_t)c->grid.M + 1);
+  r |= dalloc(c, &c->cell_count, (size_t)c->grid.M + 1); r |= dalloc(c, &c->cell_start, (size_t)c->grid.M + 2);
   r |= dalloc(c, &c->tmp_src, n); r |= dalloc(c, &c->tmp_id, n); r |= dalloc(c, &c->cell_of, n);
-  r |= dalloc(c, &c->slot_of_id, n);
+  r |= dalloc(c, &c->slot_of_id, (size_t)c->n);
   r |= dalloc(c, &c->list, n * (size_t)c->cap); r |= dalloc(c, &c->nlist, n); r |= dalloc(c, &c->count_all, n);
-  c->ntiles = num_tiles(c->grid);
   r |= dalloc(c, &c->d_err, 1);
-  r |= dalloc(c, &c->d_step, 1);
+  r |= dalloc(c, &c->d_xcount, 8);
   if (r) return CRM_E_OOM;
-  // scan level buffers
-  long long len = c->grid.M;
+  // tiles over the owned planes
+  {
+    const long long per_x = (long long)tiles_y(c->grid) * tiles_z(c->grid);
+    c->tile_base = (long long)(c->x_lo / TX) * per_x;
+    c->ntiles = (long long)((c->x_hi - c->x_lo + TX - 1) / TX) * per_x;
+  }
+  // scan level buffers (M + 1 entries: the last one counts dropped particles)
+  long long len = (long long)c->grid.M + 1;
   while (true) {
     const long long tiles = (len + SCAN_TILE - 1) / SCAN_TILE;
     uint32_t *s = nullptr, *sx = nullptr;
     if (dalloc(c, &s, (size_t)tiles) || dalloc(c, &sx, (size_t)tiles + 1)) return CRM_E_OOM;
     c->scan_sums.push_back(s);
     c->scan_sums_x.push_back(sx);
-    c->scan_len.push_back(len);
     if (tiles == 1) break;
     len = tiles;
   }
-  cudaError_t e = cudaMallocHost((void**)&c->h_err, sizeof(ErrLatch));
-  if (e != cudaSuccess) return fail(c, CRM_E_OOM, "cudaMallocHost failed");
+  CK(cudaMallocHost((void**)&c->h_err, sizeof(ErrLatch)));
+  CK(cudaMallocHost((void**)&c->h_pin, 64 * sizeof(uint32_t)));
   // bodies and moving markers
   const int nb = (int)c->bodies.size();
   if (dalloc(c, &c->d_bodies, nb) || dalloc(c, &c->d_pose0, nb) || dalloc(c, &c->d_posem, nb)) return CRM_E_OOM;
@@ -315,15 +157,37 @@ int commit(crm_t* c) {
     CK(cudaMemsetAsync(c->macc, 0, n * sizeof(float4), c->stream));
   }
   CK(cudaMemcpyAsync(c->d_bodies, c->bodies.data(), nb * sizeof(BodyState), cudaMemcpyHostToDevice, c->stream));
-  // state, id order
-  CK(cudaMemcpyAsync(c->P[0], c->hP.data(), n * 16, cudaMemcpyHostToDevice, c->stream));
-  CK(cudaMemcpyAsync(c->U[0], c->hU.data(), n * 16, cudaMemcpyHostToDevice, c->stream));
-  CK(cudaMemcpyAsync(c->S1[0], c->hS1.data(), n * 16, cudaMemcpyHostToDevice, c->stream));
-  CK(cudaMemcpyAsync(c->S2[0], c->hS2.data(), n * 8, cudaMemcpyHostToDevice, c->stream));
-  std::vector<uint32_t> iota(n);
-  for (size_t i = 0; i < n; ++i) iota[i] = (uint32_t)i;
-  CK(cudaMemcpyAsync(c->ids[0], iota.data(), n * 4, cudaMemcpyHostToDevice, c->stream));
-  CK(cudaMemcpyAsync(c->slot_of_id, iota.data(), n * 4, cudaMemcpyHostToDevice, c->stream));
+  // local state (id order)
+  const size_t nl = (size_t)c->nl;
+  std::vector<uint32_t> idv(nl);
+  if (c->slab) {
+    std::vector<float4> P(nl), U(nl), S1(nl);
+    std::vector<float2> S2(nl);
+    for (size_t k = 0; k < nl; ++k) {
+      const uint32_t i = owned[k];
+      P[k] = c->hP[i]; U[k] = c->hU[i]; S1[k] = c->hS1[i]; S2[k] = c->hS2[i];
+      idv[k] = i;
+    }
+    CK(cudaMemcpyAsync(c->P[0], P.data(), nl * 16, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->U[0], U.data(), nl * 16, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->S1[0], S1.data(), nl * 16, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->S2[0], S2.data(), nl * 8, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    launch(c, KID_SLAB, k_fill_u32, dim3(blocks(c->n, 256)), dim3(256), c->slot_of_id, (long long)c->n, 0xffffffffu);
+    std::vector<uint32_t> slots(c->n, 0xffffffffu);
+    for (size_t k = 0; k < nl; ++k) slots[owned[k]] = (uint32_t)k;
+    CK(cudaMemcpyAsync(c->slot_of_id, slots.data(), (size_t)c->n * 4, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->ids[0], idv.data(), nl * 4, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  } else {
+    for (size_t i = 0; i < nl; ++i) idv[i] = (uint32_t)i;
+    CK(cudaMemcpyAsync(c->P[0], c->hP.data(), nl * 16, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->U[0], c->hU.data(), nl * 16, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->S1[0], c->hS1.data(), nl * 16, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->S2[0], c->hS2.data(), nl * 8, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->ids[0], idv.data(), nl * 4, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->slot_of_id, idv.data(), nl * 4, cudaMemcpyHostToDevice, c->stream));
+  }
   CK(cudaMemsetAsync(c->d_err, 0, sizeof(ErrLatch), c->stream));
   CK(cudaStreamSynchronize(c->stream));
   c->cur = 0;
@@ -331,76 +195,94 @@ int commit(crm_t* c) {
   set_attrs(c);
   c->hP.clear(); c->hP.shrink_to_fit(); c->hU.clear(); c->hU.shrink_to_fit();
   c->hS1.clear(); c->hS1.shrink_to_fit(); c->hS2.clear(); c->hS2.shrink_to_fit();
+  // NCCL communicator (collective: every rank commits at the same point)
+  if (c->slab && c->has_nccl_id) {
+    NcclApi& api = nccl();
+    if (!api.ok) return fail(c, CRM_E_COMM, "libnccl.so.2 not found (set CRM_NCCL_LIB)");
+    ncclUniqueId id;
+    std::memcpy(&id, c->nccl_id, sizeof(id));
+    ncclComm_t comm;
+    ncclResult_t nr = api.commInitRank(&comm, c->world, id, c->rank);
+    if (nr != ncclSuccess) return fail(c, CRM_E_COMM, std::string("ncclCommInitRank: ") + api.errorString(nr));
+    c->nccl_comm = comm;
+  }
   return CRM_OK;
 }
 
-// sort phase of a step on the current state: bin, scan, scatter, reorder
-void issue_sort(crm_t* c, long long step) {
-  const int n = (int)c->n;
+}  // namespace
+
+namespace {
+
+// sort phase on the local particles: bin, scan, scatter, reorder; particles whose tag
+// matches drop_mask leave the local set
+void issue_sort(crm_t* c, long long step, uint32_t drop_mask) {
+  const int n = (int)c->nl;
   const int a = c->cur, b = 1 - c->cur;
-  cudaMemsetAsync(c->cell_count, 0, (size_t)c->grid.M * 4, c->stream);
-  launch(c, KID_BIN, k_bin, dim3(blocks(n, 256)), dim3(256), n, (const float4*)c->P[a], (const uint32_t*)c->ids[a],
-         c->grid, c->key, c->arrival, c->cell_count, c->d_err, step);
-  scan_u32(c, c->cell_count, c->cell_start, c->grid.M, 0);
+  cudaMemsetAsync(c->cell_count, 0, ((size_t)c->grid.M + 1) * 4, c->stream);
+  launch(c, KID_BIN, k_bin, dim3(blocks(n, 256)), dim3(256), n, (const float4*)c->P[a], (const float4*)c->U[a],
+         (const uint32_t*)c->ids[a], c->grid, drop_mask, c->key, c->arrival, c->cell_count, c->d_err, step);
+  scan_u32(c, c->cell_count, c->cell_start, (long long)c->grid.M + 1, 0);
   launch(c, KID_SCATTER, k_scatter, dim3(blocks(n, 256)), dim3(256), n, (const uint32_t*)c->key,
          (const uint32_t*)c->arrival, (const uint32_t*)c->cell_start, (const uint32_t*)c->ids[a], c->tmp_src, c->tmp_id);
+  if (c->slab)
+    launch(c, KID_SLAB, k_fill_u32, dim3(blocks(c->n, 256)), dim3(256), c->slot_of_id, (long long)c->n, 0xffffffffu);
   launch(c, KID_REORDER, k_reorder, dim3(blocks(n, 256)), dim3(256), n, (const uint32_t*)c->tmp_src,
          (const uint32_t*)c->tmp_id, (const uint32_t*)c->key, (const uint32_t*)c->cell_start,
          (const float4*)c->P[a], (const float4*)c->U[a], (const float4*)c->S1[a], (const float2*)c->S2[a],
-         c->P[b], c->U[b], c->S1[b], c->S2[b], c->ids[b], c->cell_of, c->slot_of_id);
+         c->P[b], c->U[b], c->S1[b], c->S2[b], c->ids[b], c->cell_of, c->slot_of_id, c->grid.M);
   c->cur = b;
 }
 
-void set_attrs(crm_t* c) {
-  if (c->attrs_set) return;
-  const int sm = (int)sizeof(TileSmem);
-  cudaFuncSetAttribute(k_bce_t<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-  cudaFuncSetAttribute(k_bce_t<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-  cudaFuncSetAttribute(k_rates_t<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-  cudaFuncSetAttribute(k_rates_t<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-  c->attrs_set = true;
-}
-
-// stage A (filter + BCE + rates at y_n -> y_mid); store_all keeps marker-marker pairs (debug)
-void issue_stage_a(crm_t* c, float dt, long long step, int store_all) {
+// BCE extrapolation: stage 0 at y_n (with the marker filter), stage 1 at y_mid
+void issue_bce(crm_t* c, int stage, float dt, long long step, int store_all) {
+  (void)dt;
+  if (!c->n_bce) return;
   const int y = c->cur;
   const int dbg = c->dbg_on ? 1 : 0;
   const dim3 tg((unsigned)c->ntiles), tb(TILE_THREADS);
   const size_t sm = sizeof(TileSmem);
-  if (c->n_bce)
+  if (stage == 0)
     launch_smem(c, KID_BCE_A, k_bce_t<0>, tg, tb, sm, c->grid, c->ph, (const uint32_t*)c->cell_start,
                 (const float4*)c->P[y], c->U[y], c->S1[y], c->S2[y], c->list, c->nlist, c->count_all,
                 (const uint32_t*)c->cell_of, (const Pose*)c->d_pose0, c->cap, store_all, c->dbg, dbg, c->d_err,
-                (const uint32_t*)c->ids[y], step);
-  launch_smem(c, KID_RATES_A, k_rates_t<0>, tg, tb, sm, c->grid, c->ph, dt, (const uint32_t*)c->cell_start,
-              (const float4*)c->P[y], (const float4*)c->U[y], (const float4*)c->S1[y], (const float2*)c->S2[y], c->Pm,
-              c->Um, c->S1m, c->S2m, c->list, c->nlist, c->count_all, (const uint32_t*)c->cell_of, c->cap, c->macc,
-              c->dbg, dbg, c->d_err, (const uint32_t*)c->ids[y], step);
+                (const uint32_t*)c->ids[y], step, c->tile_base);
+  else
+    launch_smem(c, KID_BCE_B, k_bce_t<1>, tg, tb, sm, c->grid, c->ph, (const uint32_t*)c->cell_start,
+                (const float4*)c->Pm, c->Um, c->S1m, c->S2m, c->list, c->nlist, c->count_all,
+                (const uint32_t*)c->cell_of, (const Pose*)c->d_posem, c->cap, 0, c->dbg, dbg, c->d_err,
+                (const uint32_t*)c->ids[y], step, c->tile_base);
 }
 
-// one RK2 step (everything on the stream, no host sync)
-void issue_step(crm_t* c, float dt, long long step) {
-  issue_sort(c, step);
-  issue_stage_a(c, dt, step, 0);
+// rates: stage 0 (fluid filter + rates at y_n -> y_mid), stage 1 (rates at y_mid -> y_{n+1})
+void issue_rates(crm_t* c, int stage, float dt, long long step) {
   const int y = c->cur;
   const int dbg = c->dbg_on ? 1 : 0;
   const dim3 tg((unsigned)c->ntiles), tb(TILE_THREADS);
   const size_t sm = sizeof(TileSmem);
+  if (stage == 0)
+    launch_smem(c, KID_RATES_A, k_rates_t<0>, tg, tb, sm, c->grid, c->ph, dt, (const uint32_t*)c->cell_start,
+                (const float4*)c->P[y], (const float4*)c->U[y], (const float4*)c->S1[y], (const float2*)c->S2[y], c->Pm,
+                c->Um, c->S1m, c->S2m, c->list, c->nlist, c->count_all, (const uint32_t*)c->cell_of, c->cap, c->macc,
+                c->dbg, dbg, c->d_err, (const uint32_t*)c->ids[y], step, c->tile_base);
+  else
+    launch_smem(c, KID_RATES_B, k_rates_t<1>, tg, tb, sm, c->grid, c->ph, dt, (const uint32_t*)c->cell_start,
+                (const float4*)c->Pm, (const float4*)c->Um, (const float4*)c->S1m, (const float2*)c->S2m, c->P[y],
+                c->U[y], c->S1[y], c->S2[y], c->list, c->nlist, c->count_all, (const uint32_t*)c->cell_of, c->cap,
+                c->macc, c->dbg, dbg, c->d_err, (const uint32_t*)c->ids[y], step, c->tile_base);
+}
+
+// one RK2 step on one GPU (everything on the stream, no host sync)
+void issue_step(crm_t* c, float dt, long long step) {
+  issue_sort(c, step, 0);
+  issue_bce(c, 0, dt, step, 0);
+  issue_rates(c, 0, dt, step);
+  const int y = c->cur;
   if (c->n_moving_markers)
     launch(c, KID_MARKERS, k_markers_place, dim3(blocks(c->n_moving_markers, 128)), dim3(128), c->n_moving_markers,
            (const uint32_t*)c->d_moving_ids, (const float4*)c->d_xlocal, (const uint32_t*)c->slot_of_id,
            (const Pose*)c->d_posem, c->Pm, (const float4*)c->Um);
-  // ---- stage B at y_mid, same lists
-  if (c->n_bce)
-    launch_smem(c, KID_BCE_B, k_bce_t<1>, tg, tb, sm, c->grid, c->ph, (const uint32_t*)c->cell_start,
-                (const float4*)c->Pm, c->Um, c->S1m, c->S2m, c->list, c->nlist, c->count_all,
-                (const uint32_t*)c->cell_of, (const Pose*)c->d_posem, c->cap, 0, c->dbg, dbg, c->d_err,
-                (const uint32_t*)c->ids[y], step);
-  launch_smem(c, KID_RATES_B, k_rates_t<1>, tg, tb, sm, c->grid, c->ph, dt, (const uint32_t*)c->cell_start,
-              (const float4*)c->Pm, (const float4*)c->Um, (const float4*)c->S1m, (const float2*)c->S2m, c->P[y],
-              c->U[y], c->S1[y], c->S2[y], c->list, c->nlist, c->count_all, (const uint32_t*)c->cell_of, c->cap,
-              c->macc, c->dbg, dbg, c->d_err, (const uint32_t*)c->ids[y], step);
-  // ---- bodies
+  issue_bce(c, 1, dt, step, 0);
+  issue_rates(c, 1, dt, step);
   if (c->n_moving_bodies) {
     launch(c, KID_BODY, k_body_update, dim3(c->n_moving_bodies), dim3(BODY_BS), (const int*)c->d_moving_bodies,
            (const uint32_t*)c->d_mstart, (const uint32_t*)c->d_moving_ids, (const uint32_t*)c->slot_of_id,
@@ -411,7 +293,7 @@ void issue_step(crm_t* c, float dt, long long step) {
            (const uint32_t*)c->d_moving_ids, (const float4*)c->d_xlocal, (const uint32_t*)c->slot_of_id,
            (const Pose*)c->d_pose0, c->P[y], (const float4*)c->U[y]);
   }
-  if (dbg) cudaMemcpyAsync(c->dbg_ids, c->ids[y], (size_t)c->n * 4, cudaMemcpyDeviceToDevice, c->stream);
+  if (c->dbg_on) cudaMemcpyAsync(c->dbg_ids, c->ids[y], (size_t)c->nl * 4, cudaMemcpyDeviceToDevice, c->stream);
 }
 
 int read_latch(crm_t* c) {
@@ -420,10 +302,14 @@ int read_latch(crm_t* c) {
   if (c->h_err->code) {
     const ErrLatch e = *c->h_err;
     char buf[256];
-    if (e.code == CRM_E_DOMAIN)
+    if (e.code == CRM_E_DOMAIN && e.aux == 1)
+      snprintf(buf, sizeof buf, "particle id %lld crossed more than one cell plane in step %lld", e.id, e.step);
+    else if (e.code == CRM_E_DOMAIN)
       snprintf(buf, sizeof buf, "particle id %lld outside the grid box at step %lld", e.id, e.step);
     else if (e.code == CRM_E_NONFINITE)
       snprintf(buf, sizeof buf, "non-finite state at particle id %lld after step %lld", e.id, e.step);
+    else if (e.code == CRM_E_CAPACITY && e.id < 0)
+      snprintf(buf, sizeof buf, "tile window of %lld particles exceeds 16-bit offsets at step %lld", e.aux, e.step);
     else if (e.code == CRM_E_CAPACITY)
       snprintf(buf, sizeof buf, "particle id %lld has %lld neighbours > max_neighbors %d at step %lld", e.id, e.aux,
                c->cap, e.step);
@@ -445,6 +331,29 @@ int ensure_stage(crm_t* c, size_t doubles) {
   if (dalloc(c, &c->d_stage, doubles)) return CRM_E_OOM;
   c->stage_cap = doubles;
   return CRM_OK;
+}
+
+int begin_steps(crm_t* c, double dt) {
+  cudaSetDevice(c->device);
+  int r = commit(c);
+  if (r) return r;
+  if (c->poses_dt != dt) {
+    launch(c, KID_POSES, k_body_poses, dim3(1), dim3(64), (int)c->bodies.size(), (const BodyState*)c->d_bodies,
+           0.5 * dt, c->d_pose0, c->d_posem);
+    c->poses_dt = dt;
+  }
+  return CRM_OK;
+}
+
+int end_steps(crm_t* c, int64_t nsteps) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(c, CRM_E_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+  c->steps_done += nsteps;
+  c->dbg_valid = c->dbg_on;
+  int r = read_latch(c);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(c, CRM_E_CUDA, std::string("step: ") + cudaGetErrorString(e));
+  return r;
 }
 
 }  // namespace
@@ -485,7 +394,9 @@ int crm_create(const crm_material_t* mat, const crm_kernel_t* ker, const crm_bou
   if (k.ps_freq > 1) return CRM_E_UNSUPPORTED;
   if (k.ps_freq < 0) return CRM_E_INVALID;
   if (k.visc_mode != CRM_VISC_BILATERAL && k.visc_mode != CRM_VISC_UNILATERAL) return CRM_E_INVALID;
-  if (dist && dist->world > 1) return CRM_E_UNSUPPORTED;
+  if (dist && (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world)) return CRM_E_INVALID;
+  if (dist && dist->world > 1 && bnd->slab_axis != 0) return CRM_E_UNSUPPORTED;
+  if (k.max_neighbors > 0 && (k.max_neighbors % 8) != 0) return CRM_E_INVALID;
   for (int a = 0; a < 3; ++a)
     if (!(bnd->hi[a] > bnd->lo[a])) return CRM_E_INVALID;
   crm_t* c = new crm();
@@ -501,7 +412,7 @@ int crm_create(const crm_material_t* mat, const crm_kernel_t* ker, const crm_bou
     c->grid.dims[a] = (int)std::ceil((bnd->hi[a] - bnd->lo[a]) / R);
     M *= c->grid.dims[a];
   }
-  if (M >= 0xffffffffLL) {
+  if (M >= 0xfffffff0LL) {
     delete c;
     return CRM_E_INVALID;
   }
@@ -509,12 +420,11 @@ int crm_create(const crm_material_t* mat, const crm_kernel_t* ker, const crm_bou
   c->grid.s = (float)R;
   c->grid.R2 = (float)(R * R);
   {
-    // pruning slack: 16 ulp of the largest coordinate + 1e-6 of a cell
     double amax = 0;
     for (int a = 0; a < 3; ++a) amax = std::max(amax, std::max(std::fabs(bnd->lo[a]), std::fabs(bnd->hi[a])));
     c->grid.margin = (float)(16.0 * amax * std::ldexp(1.0, -23) + 1e-6 * R);
   }
-  // physics constants
+  // physics constants (fp32 copies)
   const double h = k.h;
   c->ph.h = (float)h;
   c->ph.hinv = (float)(1.0 / h);
@@ -549,6 +459,16 @@ int crm_create(const crm_material_t* mat, const crm_kernel_t* ker, const crm_bou
     const double ball = 4.0 / 3.0 * M_PI * std::pow(R / k.d0, 3.0);
     c->cap = std::max(32, (int)(32 * std::ceil(2.0 * ball / 32.0)));
   }
+  // distribution
+  if (dist && dist->world > 1) {
+    c->rank = dist->rank;
+    c->world = dist->world;
+    c->slab = true;
+    if (dist->nccl_id) {
+      std::memcpy(c->nccl_id, dist->nccl_id, 128);
+      c->has_nccl_id = true;
+    }
+  }
   // device
   c->device = dist ? dist->device : 0;
   int ndev = 0;
@@ -571,8 +491,7 @@ int crm_create(const crm_material_t* mat, const crm_kernel_t* ker, const crm_bou
     }
     c->own_stream = true;
   }
-  // body 0: static walls
-  BodyState walls{};
+  BodyState walls{};   // body 0: static walls
   walls.quat[0] = 1.0;
   walls.motion = CRM_BODY_FIXED;
   c->bodies.push_back(walls);
@@ -584,11 +503,11 @@ void crm_destroy(crm_t* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->nccl_comm && nccl().commDestroy) nccl().commDestroy((ncclComm_t)c->nccl_comm);
   for (auto& r : c->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   for (int b = 0; b < 2; ++b) {
     cudaFree(c->P[b]); cudaFree(c->U[b]); cudaFree(c->S1[b]); cudaFree(c->S2[b]); cudaFree(c->ids[b]);
-    if (c->gexec[b]) cudaGraphExecDestroy(c->gexec[b]);
     cudaFree(c->dbg.drho[b]); cudaFree(c->dbg.acc[b]); cudaFree(c->dbg.ds1[b]); cudaFree(c->dbg.ds2[b]);
     cudaFree(c->dbg.bu[b]); cudaFree(c->dbg.bs1[b]); cudaFree(c->dbg.bs2[b]);
   }
@@ -600,8 +519,9 @@ void crm_destroy(crm_t* c) {
   for (auto p : c->scan_sums_x) cudaFree(p);
   cudaFree(c->d_bodies); cudaFree(c->d_pose0); cudaFree(c->d_posem);
   cudaFree(c->d_moving_ids); cudaFree(c->d_xlocal); cudaFree(c->d_mstart); cudaFree(c->d_moving_bodies);
-  cudaFree(c->macc); cudaFree(c->d_err); cudaFree(c->d_step); cudaFree(c->dbg_ids); cudaFree(c->d_stage);
+  cudaFree(c->macc); cudaFree(c->d_err); cudaFree(c->d_xcount); cudaFree(c->dbg_ids); cudaFree(c->d_stage);
   if (c->h_err) cudaFreeHost(c->h_err);
+  if (c->h_pin) cudaFreeHost(c->h_pin);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -676,6 +596,7 @@ int64_t crm_count(const crm_t* c, int which) {
   switch (which) {
     case CRM_FLUID: return c->n_fluid;
     case CRM_BCE: return c->n_bce;
+    case CRM_OWNED: return c->committed ? c->n_owned : (c->slab ? 0 : c->n);
     default: return c->n;
   }
 }
@@ -711,11 +632,12 @@ int crm_set_graphs(crm_t* c, int on) {
 
 int crm_debug_arm(crm_t* c, int on) {
   if (!c) return CRM_E_INVALID;
+  if (c->slab) return fail(c, CRM_E_UNSUPPORTED, "debug capture is single-GPU only");
   int r = commit(c);
   if (r) return r;
   if (on) {
     if (alloc_debug(c)) return fail(c, CRM_E_OOM, "debug buffers");
-    const size_t n = (size_t)c->n;
+    const size_t n = (size_t)c->ncap;
     for (int s = 0; s < 2; ++s) {
       cudaMemsetAsync(c->dbg.drho[s], 0, n * 4, c->stream); cudaMemsetAsync(c->dbg.acc[s], 0, n * 16, c->stream);
       cudaMemsetAsync(c->dbg.ds1[s], 0, n * 16, c->stream); cudaMemsetAsync(c->dbg.ds2[s], 0, n * 8, c->stream);
@@ -731,26 +653,67 @@ int crm_debug_arm(crm_t* c, int on) {
 int crm_step(crm_t* c, double dt, int64_t nsteps) {
   if (!c) return CRM_E_INVALID;
   if (!(dt > 0) || nsteps < 0) return fail(c, CRM_E_INVALID, "dt must be > 0 and nsteps >= 0");
-  cudaSetDevice(c->device);
-  int r = commit(c);
+  if (c->slab && !c->has_nccl_id) return fail(c, CRM_E_STATE, "in-process slab contexts step with crm_group_step");
+  int r = begin_steps(c, dt);
   if (r) return r;
   if (nsteps == 0) return CRM_OK;
-  if (c->poses_dt != dt) {
-    launch(c, KID_POSES, k_body_poses, dim3(1), dim3(64), (int)c->bodies.size(), (const BodyState*)c->d_bodies,
-           0.5 * dt, c->d_pose0, c->d_posem);
-    c->poses_dt = dt;
-  }
   for (int64_t s = 0; s < nsteps; ++s) {
-    issue_step(c, (float)dt, (long long)(c->steps_done + s));
+    const long long step = (long long)(c->steps_done + s);
+    if (!c->slab) {
+      issue_step(c, (float)dt, step);
+      continue;
+    }
+    for (int k = 0; k < kSlabPhases; ++k) {
+      if ((r = slab_phase(c, k, (float)dt, step))) return r;
+      if ((r = nccl_flush(c))) return r;
+    }
   }
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return fail(c, CRM_E_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
-  c->steps_done += nsteps;
-  c->dbg_valid = c->dbg_on;
-  r = read_latch(c);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return fail(c, CRM_E_CUDA, std::string("step: ") + cudaGetErrorString(e));
-  return r;
+  return end_steps(c, nsteps);
+}
+
+int crm_group_step(crm_t** cs, int world, double dt, int64_t nsteps) {
+  if (!cs || world < 1) return CRM_E_INVALID;
+  for (int a = 0; a < world; ++a) {
+    if (!cs[a] || cs[a]->world != world || cs[a]->rank != a || cs[a]->has_nccl_id)
+      return fail(cs[a], CRM_E_INVALID, "crm_group_step: contexts must be ranks 0..world-1 without an NCCL id");
+    if (cs[a]->stream != cs[0]->stream || cs[a]->device != cs[0]->device)
+      return fail(cs[a], CRM_E_INVALID, "crm_group_step: contexts must share one device and stream");
+  }
+  if (!(dt > 0) || nsteps < 0) return fail(cs[0], CRM_E_INVALID, "dt must be > 0 and nsteps >= 0");
+  int r;
+  for (int a = 0; a < world; ++a)
+    if ((r = begin_steps(cs[a], dt))) return r;
+  for (int64_t s = 0; s < nsteps; ++s) {
+    for (int k = 0; k < kSlabPhases; ++k) {
+      for (int a = 0; a < world; ++a) {
+        const long long step = (long long)(cs[a]->steps_done + s);
+        if (world == 1) {
+          if (k == 0) issue_step(cs[a], (float)dt, step);
+          continue;
+        }
+        if ((r = slab_phase(cs[a], k, (float)dt, step))) return r;
+      }
+      if (world > 1 && (r = loopback_flush(cs, world))) return r;
+    }
+  }
+  for (int a = 0; a < world; ++a)
+    if ((r = end_steps(cs[a], nsteps))) return r;
+  return CRM_OK;
+}
+
+int crm_nccl_unique_id(void* out128) {
+  if (!out128) return CRM_E_INVALID;
+  NcclApi& api = nccl();
+  if (!api.ok) return CRM_E_COMM;
+  ncclUniqueId id;
+  if (api.getUniqueId(&id) != ncclSuccess) return CRM_E_COMM;
+  std::memcpy(out128, &id, 128);
+  return CRM_OK;
+}
+
+int crm_slab_partition(const int64_t* plane_counts, int nplanes, int world, int align, int* bounds) {
+  if (!plane_counts || !bounds) return CRM_E_INVALID;
+  return slab_partition(plane_counts, nplanes, world, align, bounds);
 }
 
 int crm_get_state(crm_t* c, int64_t first, int64_t count, double* pos, double* vel, double* rho, double* sig6) {
@@ -765,6 +728,7 @@ int crm_get_state(crm_t* c, int64_t first, int64_t count, double* pos, double* v
   double* dv = dp + 3 * count;
   double* dr = dv + 3 * count;
   double* ds = dr + count;
+  if (c->slab) CK(cudaMemsetAsync(dp, 0xff, (size_t)count * 13 * 8, c->stream));   // NaN rows: not owned here
   const int y = c->cur;
   launch(c, KID_STATE, k_get_state, dim3(blocks(count, 256)), dim3(256), (long long)first, (long long)count,
          (const uint32_t*)c->slot_of_id, (const float4*)c->P[y], (const float4*)c->U[y], (const float4*)c->S1[y],
@@ -786,7 +750,6 @@ int crm_set_state(crm_t* c, int64_t first, int64_t count, const double* pos, con
   if (first < 0 || count < 0 || first + count > c->n) return fail(c, CRM_E_INVALID, "id range out of bounds");
   if (count == 0) return CRM_OK;
   if (pos && c->n_moving_markers) {
-    // positions of moving-body markers are owned by their body
     std::vector<uint32_t> mids(c->n_moving_markers);
     CK(cudaMemcpy(mids.data(), c->d_moving_ids, mids.size() * 4, cudaMemcpyDeviceToHost));
     for (uint32_t id : mids)
@@ -836,13 +799,15 @@ int crm_get_body(crm_t* c, int32_t body, crm_body_t* st, double force[3], double
 int crm_debug_structure(crm_t* c, uint32_t* cell_by_id, int64_t* sorted_ids, uint32_t* nbr_count_by_id,
                         uint32_t* cell_start, int64_t* n_cells) {
   if (!c) return CRM_E_INVALID;
+  if (c->slab) return fail(c, CRM_E_UNSUPPORTED, "debug exports are single-GPU only");
   cudaSetDevice(c->device);
   int r = commit(c);
   if (r) return r;
   if (n_cells) *n_cells = c->grid.M;
   if (!cell_by_id && !sorted_ids && !nbr_count_by_id && !cell_start) return CRM_OK;
-  issue_sort(c, c->steps_done);
-  issue_stage_a(c, 0.0f, c->steps_done, 0);
+  issue_sort(c, c->steps_done, 0);
+  issue_bce(c, 0, 0.0f, c->steps_done, 0);
+  issue_rates(c, 0, 0.0f, c->steps_done);
   r = read_latch(c);
   if (r) return r;
   const size_t n = (size_t)c->n;
@@ -861,11 +826,13 @@ int crm_debug_structure(crm_t* c, uint32_t* cell_by_id, int64_t* sorted_ids, uin
 
 int crm_debug_neighbors(crm_t* c, int64_t* offsets, int64_t* list) {
   if (!c || !offsets) return CRM_E_INVALID;
+  if (c->slab) return fail(c, CRM_E_UNSUPPORTED, "debug exports are single-GPU only");
   cudaSetDevice(c->device);
   int r = commit(c);
   if (r) return r;
-  issue_sort(c, c->steps_done);
-  issue_stage_a(c, 0.0f, c->steps_done, 1);
+  issue_sort(c, c->steps_done, 0);
+  issue_bce(c, 0, 0.0f, c->steps_done, 1);
+  issue_rates(c, 0, 0.0f, c->steps_done);
   const size_t n = (size_t)c->n;
   if (!c->list32 && dalloc(c, &c->list32, n * (size_t)c->cap)) return CRM_E_OOM;
   launch(c, KID_DECODE, k_decode_lists, dim3(blocks((long long)n, 256)), dim3(256), (int)n, c->grid,

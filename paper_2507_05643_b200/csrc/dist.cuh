@@ -1,0 +1,319 @@
+// dist.cuh — multi-GPU slab decomposition along x.
+//
+// Each rank owns the cell planes [x_lo, x_hi) (boundaries from a prefix sum of per-plane particle
+// counts, aligned to the tile width) and keeps one ghost plane (one 2h cell) on each interior
+// face.  With the B3 cell order a plane is one contiguous index range of the sorted state, so
+// every exchange is a handful of contiguous slices (zero pack).  Per step:
+//   P0  sort (previous ghosts dropped); emigrants = particles now outside [x_lo, x_hi)
+//   E0  counts of emigrants                      E1  emigrant payloads (id + 56 B state)
+//   P2  emigrants marked dropped, immigrants checked to sit in the boundary plane
+//   E2  counts of boundary planes                E3  boundary planes -> neighbour ghost planes
+//   P4  sort (ghosts in, emigrants out), BCE extrapolation at y_n on owned tiles
+//   E4  boundary planes (markers now extrapolated) -> ghosts
+//   P5  rates + half step on owned tiles         E5  y_mid boundary planes -> ghosts
+//   P6  BCE extrapolation at y_mid               E6  y_mid boundary planes -> ghosts
+//   P7  rates + full step + return map on owned tiles
+// Neighbour iteration order is the global (cell, id) order restricted to the local planes, so
+// owned particles follow bit-identical trajectories to a one-GPU run.
+// Transports: NCCL point-to-point (ncclSend/ncclRecv in a group, on the context stream; NCCL is
+// loaded at run time) or an in-process loopback between contexts of one process (crm_group_step;
+// used to test the decomposition on one GPU).
+#pragma once
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include "context.cuh"
+
+namespace {
+
+// ---------------------------------------------------------------------------------------
+struct NcclApi {
+  bool ok = false;
+  decltype(&ncclGetUniqueId) getUniqueId = nullptr;
+  decltype(&ncclCommInitRank) commInitRank = nullptr;
+  decltype(&ncclCommDestroy) commDestroy = nullptr;
+  decltype(&ncclSend) send = nullptr;
+  decltype(&ncclRecv) recv = nullptr;
+  decltype(&ncclGroupStart) groupStart = nullptr;
+  decltype(&ncclGroupEnd) groupEnd = nullptr;
+  decltype(&ncclGetErrorString) errorString = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (tried) return api;
+  tried = true;
+  const char* cands[] = {getenv("CRM_NCCL_LIB"), "libnccl.so.2",
+#ifdef CRM_NCCL_DEFAULT
+                         CRM_NCCL_DEFAULT,
+#endif
+                         nullptr};
+  void* h = nullptr;
+  for (const char* p : cands)
+    if (p && (h = dlopen(p, RTLD_NOW | RTLD_GLOBAL))) break;
+  if (!h) return api;
+#define LD(field, sym) api.field = reinterpret_cast<decltype(api.field)>(dlsym(h, #sym))
+  LD(getUniqueId, ncclGetUniqueId); LD(commInitRank, ncclCommInitRank); LD(commDestroy, ncclCommDestroy);
+  LD(send, ncclSend); LD(recv, ncclRecv); LD(groupStart, ncclGroupStart); LD(groupEnd, ncclGroupEnd);
+  LD(errorString, ncclGetErrorString);
+#undef LD
+  api.ok = api.getUniqueId && api.commInitRank && api.send && api.recv && api.groupStart && api.groupEnd;
+  return api;
+}
+
+// ---------------------------------------------------------------------------------------
+void post(crm_t* c, int peer, bool send, const void* ptr, size_t bytes) {
+  if (bytes == 0 || peer < 0 || peer >= c->world) return;
+  c->posts.push_back({peer, send, const_cast<void*>(ptr), bytes});
+}
+
+// state slice [b, e) of buffer set `y` (ids included when with_ids)
+void post_slice(crm_t* c, int peer, bool send, int y, uint32_t b, uint32_t e, bool with_ids) {
+  if (e <= b) return;
+  const size_t k = e - b;
+  post(c, peer, send, c->P[y] + b, k * 16);
+  post(c, peer, send, c->U[y] + b, k * 16);
+  post(c, peer, send, c->S1[y] + b, k * 16);
+  post(c, peer, send, c->S2[y] + b, k * 8);
+  if (with_ids) post(c, peer, send, c->ids[y] + b, k * 4);
+}
+
+void post_mid_slice(crm_t* c, int peer, bool send, uint32_t b, uint32_t e) {
+  if (e <= b) return;
+  const size_t k = e - b;
+  post(c, peer, send, c->Pm + b, k * 16);
+  post(c, peer, send, c->Um + b, k * 16);
+  post(c, peer, send, c->S1m + b, k * 16);
+  post(c, peer, send, c->S2m + b, k * 8);
+}
+
+// NCCL transport: issue every pending transfer of this rank as one group on the stream
+int nccl_flush(crm_t* c) {
+  if (c->posts.empty()) return CRM_OK;
+  NcclApi& api = nccl();
+  ncclComm_t comm = (ncclComm_t)c->nccl_comm;
+  ncclResult_t r = api.groupStart();
+  for (const Post& p : c->posts) {
+    if (r != ncclSuccess) break;
+    r = p.send ? api.send(p.ptr, p.bytes, ncclUint8, p.peer, comm, c->stream)
+               : api.recv(p.ptr, p.bytes, ncclUint8, p.peer, comm, c->stream);
+  }
+  ncclResult_t r2 = api.groupEnd();
+  c->posts.clear();
+  if (r != ncclSuccess || r2 != ncclSuccess)
+    return fail(c, CRM_E_COMM, std::string("NCCL: ") + (api.errorString ? api.errorString(r != ncclSuccess ? r : r2) : "error"));
+  return CRM_OK;
+}
+
+// loopback transport: match every send of rank a to rank b with b's receives from a (FIFO)
+int loopback_flush(crm_t** cs, int world) {
+  std::vector<std::vector<size_t>> used(world);
+  for (int a = 0; a < world; ++a) used[a].assign(cs[a]->posts.size(), 0);
+  for (int a = 0; a < world; ++a) {
+    crm_t* c = cs[a];
+    for (const Post& s : c->posts) {
+      if (!s.send) continue;
+      crm_t* d = cs[s.peer];
+      bool found = false;
+      for (size_t k = 0; k < d->posts.size(); ++k) {
+        const Post& r = d->posts[k];
+        if (r.send || r.peer != a || used[s.peer][k]) continue;
+        if (r.bytes != s.bytes)
+          return fail(c, CRM_E_COMM, "loopback: size mismatch " + std::to_string(s.bytes) + " vs " + std::to_string(r.bytes));
+        used[s.peer][k] = 1;
+        CK(cudaMemcpyAsync(r.ptr, s.ptr, s.bytes, cudaMemcpyDeviceToDevice, c->stream));
+        found = true;
+        break;
+      }
+      if (!found) return fail(c, CRM_E_COMM, "loopback: unmatched send");
+    }
+  }
+  for (int a = 0; a < world; ++a) {
+    for (size_t k = 0; k < cs[a]->posts.size(); ++k)
+      if (!cs[a]->posts[k].send && !used[a][k]) return fail(cs[a], CRM_E_COMM, "loopback: unmatched receive");
+    cs[a]->posts.clear();
+  }
+  return CRM_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// slab partition: boundaries at multiples of `align` with ~equal particle counts
+int slab_partition(const int64_t* counts, int nplanes, int world, int align, int* bounds) {
+  if (world < 1 || align < 1 || nplanes < world * align) return CRM_E_INVALID;
+  std::vector<int64_t> cum(nplanes + 1, 0);
+  for (int p = 0; p < nplanes; ++p) cum[p + 1] = cum[p] + counts[p];
+  const int64_t total = cum[nplanes];
+  bounds[0] = 0;
+  for (int k = 1; k < world; ++k) {
+    const int64_t target = (total * k + world / 2) / world;
+    const int lo = bounds[k - 1] + align;
+    const int hi = ((nplanes - (world - k) * align) / align) * align;
+    int b = lo;
+    while (b + align <= hi && cum[b] < target) b += align;
+    // take the closer of b and b - align
+    if (b - align >= lo && target - cum[b - align] < cum[b] - target) b -= align;
+    bounds[k] = std::min(std::max(b, lo), hi);
+  }
+  bounds[world] = nplanes;
+  return CRM_OK;
+}
+
+uint32_t plane_start_index(const crm_t* c, int p) {   // cell index of the first cell of plane p
+  const long long NyNz = (long long)c->grid.dims[1] * c->grid.dims[2];
+  if (p <= 0) return 0;
+  if (p >= c->grid.dims[0]) return c->grid.M;
+  return (uint32_t)(p * NyNz);
+}
+
+// read cellStart at the first cell of planes ps[0..k) (k <= 8) into out
+int read_plane_starts(crm_t* c, const int* ps, int k, uint32_t* out) {
+  for (int j = 0; j < k; ++j)
+    CK(cudaMemcpyAsync(c->h_pin + j, c->cell_start + plane_start_index(c, ps[j]), 4, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  for (int j = 0; j < k; ++j) out[j] = c->h_pin[j];
+  return CRM_OK;
+}
+
+// count exchange: two words per direction (d_xcount: send L[2], send R[2], recv L[2], recv R[2])
+int read_counts(crm_t* c, uint32_t* l0, uint32_t* l1, uint32_t* r0, uint32_t* r1) {
+  CK(cudaMemcpyAsync(c->h_pin + 16, c->d_xcount + 4, 16, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  const bool hl = c->rank > 0, hr = c->rank < c->world - 1;
+  *l0 = hl ? c->h_pin[16] : 0;
+  if (l1) *l1 = hl ? c->h_pin[17] : 0;
+  *r0 = hr ? c->h_pin[18] : 0;
+  if (r1) *r1 = hr ? c->h_pin[19] : 0;
+  return CRM_OK;
+}
+
+int post_counts(crm_t* c, uint32_t l0, uint32_t l1, uint32_t r0, uint32_t r1) {
+  c->h_pin[24] = l0; c->h_pin[25] = l1; c->h_pin[26] = r0; c->h_pin[27] = r1;
+  CK(cudaMemcpyAsync(c->d_xcount, c->h_pin + 24, 16, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemsetAsync(c->d_xcount + 4, 0, 16, c->stream));
+  post(c, c->rank - 1, true, c->d_xcount + 0, 8);
+  post(c, c->rank + 1, true, c->d_xcount + 2, 8);
+  post(c, c->rank - 1, false, c->d_xcount + 4, 8);
+  post(c, c->rank + 1, false, c->d_xcount + 6, 8);
+  return CRM_OK;
+}
+
+void issue_sort(crm_t* c, long long step, uint32_t drop_mask);
+void issue_bce(crm_t* c, int stage, float dt, long long step, int store_all);
+void issue_rates(crm_t* c, int stage, float dt, long long step);
+
+// ---------------------------------------------------------------------------------------
+// the phases of one slab step (each ends with posts; the transport flushes between phases)
+int slab_phase(crm_t* c, int k, float dt, long long step) {
+  const int L = c->rank - 1, R = c->rank + 1;
+  switch (k) {
+    case 0: {   // sort owned particles (drop last step's ghosts), count emigrants
+      issue_sort(c, step, TAG_GHOST | TAG_DROP);
+      const int ps[4] = {c->x_lo, c->x_lo + 1, c->x_hi - 1, c->x_hi};
+      uint32_t st[4], nk;
+      if (int r = read_plane_starts(c, ps, 4, st)) return r;
+      const int pm[1] = {c->grid.dims[0]};
+      if (int r = read_plane_starts(c, pm, 1, &nk)) return r;
+      c->nl = nk;
+      c->s_lo = st[0]; c->s_lo1 = st[1]; c->s_hi1 = st[2]; c->s_hi = st[3];
+      c->mig_l = c->s_lo;
+      c->mig_r = (uint32_t)c->nl - c->s_hi;
+      return post_counts(c, c->mig_l, 0, c->mig_r, 0);
+    }
+    case 1: {   // emigrant payloads: [0, s_lo) -> left, [s_hi, nl) -> right; immigrants appended
+      if (int r = read_counts(c, &c->rcv_l, nullptr, &c->rcv_r, nullptr)) return r;
+      const uint32_t nl = (uint32_t)c->nl;
+      if ((int64_t)nl + c->rcv_l + c->rcv_r > c->ncap) return fail(c, CRM_E_CAPACITY, "slab capacity exceeded (immigrants)");
+      const int y = c->cur;
+      post_slice(c, L, true, y, 0, c->mig_l, true);
+      post_slice(c, R, true, y, c->s_hi, nl, true);
+      post_slice(c, L, false, y, nl, nl + c->rcv_l, true);
+      post_slice(c, R, false, y, nl + c->rcv_l, nl + c->rcv_l + c->rcv_r, true);
+      return CRM_OK;
+    }
+    case 2: {   // mark emigrants dropped, check immigrants, count boundary planes
+      const int y = c->cur;
+      const uint32_t nl = (uint32_t)c->nl;
+      if (c->mig_l) launch(c, KID_SLAB, k_or_tag, dim3(blocks(c->mig_l, 256)), dim3(256), c->U[y], 0u, c->mig_l, TAG_DROP);
+      if (c->mig_r) launch(c, KID_SLAB, k_or_tag, dim3(blocks(c->mig_r, 256)), dim3(256), c->U[y], c->s_hi, nl, TAG_DROP);
+      if (c->rcv_l)
+        launch(c, KID_SLAB, k_check_plane, dim3(blocks(c->rcv_l, 256)), dim3(256), (const float4*)c->P[y],
+               (const uint32_t*)c->ids[y], nl, nl + c->rcv_l, c->grid, c->x_lo, c->d_err, step);
+      if (c->rcv_r)
+        launch(c, KID_SLAB, k_check_plane, dim3(blocks(c->rcv_r, 256)), dim3(256), (const float4*)c->P[y],
+               (const uint32_t*)c->ids[y], nl + c->rcv_l, nl + c->rcv_l + c->rcv_r, c->grid, c->x_hi - 1, c->d_err, step);
+      c->n_app = nl + c->rcv_l + c->rcv_r;
+      // boundary plane = (owned particles of the plane, immigrants into it): two parts per side
+      return post_counts(c, c->s_lo1 - c->s_lo, c->rcv_l, c->s_hi - c->s_hi1, c->rcv_r);
+    }
+    case 3: {   // boundary planes -> neighbours' ghost planes (appended, flagged in phase 4)
+      uint32_t la, lb, ra, rb;
+      if (int r = read_counts(c, &la, &lb, &ra, &rb)) return r;
+      c->gh_l = la + lb;
+      c->gh_r = ra + rb;
+      if ((int64_t)c->n_app + c->gh_l + c->gh_r > c->ncap) return fail(c, CRM_E_CAPACITY, "slab capacity exceeded (ghosts)");
+      const int y = c->cur;
+      const uint32_t nl = (uint32_t)c->nl;
+      post_slice(c, L, true, y, c->s_lo, c->s_lo1, true);
+      post_slice(c, L, true, y, nl, nl + c->rcv_l, true);
+      post_slice(c, R, true, y, c->s_hi1, c->s_hi, true);
+      post_slice(c, R, true, y, nl + c->rcv_l, nl + c->rcv_l + c->rcv_r, true);
+      const uint32_t a0 = c->n_app, a1 = a0 + la, a2 = a1 + lb, a3 = a2 + ra, a4 = a3 + rb;
+      post_slice(c, L, false, y, a0, a1, true);
+      post_slice(c, L, false, y, a1, a2, true);
+      post_slice(c, R, false, y, a2, a3, true);
+      post_slice(c, R, false, y, a3, a4, true);
+      return CRM_OK;
+    }
+    case 4: {   // ghosts flagged, local sort, BCE at y_n; boundary planes -> ghosts
+      const int y0 = c->cur;
+      const uint32_t ng = c->gh_l + c->gh_r;
+      if (ng) launch(c, KID_SLAB, k_or_tag, dim3(blocks(ng, 256)), dim3(256), c->U[y0], c->n_app, c->n_app + ng, TAG_GHOST);
+      c->nl = c->n_app + ng;
+      issue_sort(c, step, TAG_DROP);
+      const int ps[6] = {c->x_lo - 1, c->x_lo, c->x_lo + 1, c->x_hi - 1, c->x_hi, c->x_hi + 1};
+      uint32_t st[6], nk;
+      if (int r = read_plane_starts(c, ps, 6, st)) return r;
+      const int pm[1] = {c->grid.dims[0]};
+      if (int r = read_plane_starts(c, pm, 1, &nk)) return r;
+      c->nl = nk;
+      c->s_lom1 = c->rank > 0 ? st[0] : st[1];
+      c->s_lo = st[1]; c->s_lo1 = st[2]; c->s_hi1 = st[3]; c->s_hi = st[4];
+      c->s_hip1 = c->rank < c->world - 1 ? st[5] : st[4];
+      c->n_owned = c->s_hi - c->s_lo;
+      issue_bce(c, 0, dt, step, 0);
+      const int y = c->cur;
+      post_slice(c, L, true, y, c->s_lo, c->s_lo1, false);
+      post_slice(c, R, true, y, c->s_hi1, c->s_hi, false);
+      post_slice(c, L, false, y, c->s_lom1, c->s_lo, false);
+      post_slice(c, R, false, y, c->s_hi, c->s_hip1, false);
+      return CRM_OK;
+    }
+    case 5:   // rates + half step; y_mid boundary planes -> ghosts
+    case 6: { // BCE at y_mid; y_mid boundary planes -> ghosts
+      if (k == 5) {
+        // the copies of E4 carried the owners' tags: mark the ghost planes as ghosts again
+        const int y = c->cur;
+        if (c->s_lo > c->s_lom1)
+          launch(c, KID_SLAB, k_or_tag, dim3(blocks(c->s_lo - c->s_lom1, 256)), dim3(256), c->U[y], c->s_lom1, c->s_lo, TAG_GHOST);
+        if (c->s_hip1 > c->s_hi)
+          launch(c, KID_SLAB, k_or_tag, dim3(blocks(c->s_hip1 - c->s_hi, 256)), dim3(256), c->U[y], c->s_hi, c->s_hip1, TAG_GHOST);
+        issue_rates(c, 0, dt, step);
+      } else {
+        issue_bce(c, 1, dt, step, 0);
+      }
+      post_mid_slice(c, L, true, c->s_lo, c->s_lo1);
+      post_mid_slice(c, R, true, c->s_hi1, c->s_hi);
+      post_mid_slice(c, L, false, c->s_lom1, c->s_lo);
+      post_mid_slice(c, R, false, c->s_hi, c->s_hip1);
+      return CRM_OK;
+    }
+    case 7:
+      issue_rates(c, 1, dt, step);
+      return CRM_OK;
+  }
+  return CRM_OK;
+}
+constexpr int kSlabPhases = 8;
+
+}  // namespace

@@ -173,7 +173,9 @@ __global__ void k_get_state(long long first, long long count, const uint32_t* __
   const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= count) return;
   const uint32_t s = slot_of_id[first + k];
+  if (s == 0xffffffffu) return;                 // not on this rank (multi-GPU): row left as is
   const float4 p = P[s], u = U[s], s1 = S1[s];
+  if (tag_ghost(tag_of(u.w))) return;           // ghost copy: owned by a neighbour slab
   const float2 s2 = S2[s];
   pos[3 * k] = p.x; pos[3 * k + 1] = p.y; pos[3 * k + 2] = p.z;
   vel[3 * k] = u.x; vel[3 * k + 1] = u.y; vel[3 * k + 2] = u.z;
@@ -190,7 +192,9 @@ __global__ void k_set_state(long long first, long long count, const uint32_t* __
   const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= count) return;
   const uint32_t s = slot_of_id[first + k];
+  if (s == 0xffffffffu) return;
   float4 p = P[s], u = U[s];
+  if (tag_ghost(tag_of(u.w))) return;
   if (has_pos) { p.x = (float)pos[3 * k]; p.y = (float)pos[3 * k + 1]; p.z = (float)pos[3 * k + 2]; }
   if (has_rho && !tag_is_bce(tag_of(u.w))) p.w = (float)rho[k];
   if (has_vel) { u.x = (float)vel[3 * k]; u.y = (float)vel[3 * k + 1]; u.z = (float)vel[3 * k + 2]; }

@@ -48,12 +48,20 @@ __global__ void k_markers_place(int nm, const uint32_t* __restrict__ moving_ids,
   P[s] = p;
 }
 
-// hash + per-cell count; the error latch reports particles outside the grid
-__global__ void k_bin(int n, const float4* __restrict__ P, const uint32_t* __restrict__ ids, Grid g,
-                      uint32_t* __restrict__ key, uint32_t* __restrict__ arrival,
-                      uint32_t* __restrict__ cell_count, ErrLatch* err, long long step) {
+// hash + per-cell count; the error latch reports particles outside the grid.
+// Particles whose tag has a bit of drop_mask (multi-GPU ghosts / emigrants) get the sentinel key
+// M: they sort behind every cell and are not kept.
+__global__ void k_bin(int n, const float4* __restrict__ P, const float4* __restrict__ U,
+                      const uint32_t* __restrict__ ids, Grid g, uint32_t drop_mask, uint32_t* __restrict__ key,
+                      uint32_t* __restrict__ arrival, uint32_t* __restrict__ cell_count, ErrLatch* err,
+                      long long step) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
+  if (drop_mask && (tag_of(U[i].w) & drop_mask)) {
+    key[i] = g.M;
+    arrival[i] = atomicAdd(&cell_count[g.M], 1u);
+    return;
+  }
   const float4 p = P[i];
   float f[3] = {b1_floor(p.x, g.lo[0], g.s), b1_floor(p.y, g.lo[1], g.s), b1_floor(p.z, g.lo[2], g.s)};
   int c3[3];
@@ -124,6 +132,28 @@ __global__ void k_scan_add(uint32_t* __restrict__ out, const uint32_t* __restric
 __global__ void k_copy_u32(uint32_t* dst, const uint32_t* src) { *dst = *src; }
 
 // ---------------------------------------------------------------------------------------
+// multi-GPU helpers: OR bits into the tags of slots [b, e); check that particles of slots [b, e)
+// lie in x-plane `plane` (immigrants may cross at most one cell plane per step)
+__global__ void k_or_tag(float4* __restrict__ U, uint32_t b, uint32_t e, uint32_t bits) {
+  const uint32_t s = b + blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= e) return;
+  U[s].w = __uint_as_float(tag_of(U[s].w) | bits);
+}
+
+__global__ void k_check_plane(const float4* __restrict__ P, const uint32_t* __restrict__ ids, uint32_t b, uint32_t e,
+                              Grid g, int plane, ErrLatch* err, long long step) {
+  const uint32_t s = b + blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= e) return;
+  const float f = b1_floor(P[s].x, g.lo[0], g.s);
+  if (!(f == (float)plane)) latch_error(err, -2 /*CRM_E_DOMAIN*/, (long long)ids[s], step, 1);
+}
+
+__global__ void k_fill_u32(uint32_t* __restrict__ p, long long n, uint32_t v) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
+// ---------------------------------------------------------------------------------------
 __global__ void k_scatter(int n, const uint32_t* __restrict__ key, const uint32_t* __restrict__ arrival,
                           const uint32_t* __restrict__ cell_start, const uint32_t* __restrict__ ids,
                           uint32_t* __restrict__ tmp_src, uint32_t* __restrict__ tmp_id) {
@@ -141,12 +171,13 @@ __global__ void k_reorder(int n, const uint32_t* __restrict__ tmp_src, const uin
                           const float4* __restrict__ S1, const float2* __restrict__ S2,
                           float4* __restrict__ Pn, float4* __restrict__ Un, float4* __restrict__ S1n,
                           float2* __restrict__ S2n, uint32_t* __restrict__ ids_n, uint32_t* __restrict__ cell_of,
-                          uint32_t* __restrict__ slot_of_id) {
+                          uint32_t* __restrict__ slot_of_id, uint32_t M) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n) return;
   const uint32_t i = tmp_src[s];
   const uint32_t myid = tmp_id[s];
   const uint32_t c = key[i];
+  if (c == M) return;   // dropped (ghost of the previous step or emigrant)
   const uint32_t b = cell_start[c], e = cell_start[c + 1];
   uint32_t rank = 0;
   for (uint32_t t = b; t < e; ++t) rank += (tmp_id[t] < myid) ? 1u : 0u;
