@@ -168,7 +168,7 @@ def run_reference(args):
     cb = dict(cb, value=val, sample=cb["sample"].split(";")[0] + f"; {args.steps} timed steps in {t:.2f} s")
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": args.config, "sample_fluid": sample.n_fluid},
             "cpu_baseline": cb,
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -209,22 +209,30 @@ def main():
 
     sc = scenario(args.config)
     n_fluid, n_bce = sc.n_fluid, sc.n_bce
-    # replicas: each rank advances its own copy of the workload (slab decomposition: DESIGN.md §Multi-GPU)
-    g = crm.load_scenario(sc, device=local)
+    # N > 1: slab decomposition along x with NCCL halo exchanges inside libcrm;
+    # every rank passes the same global input and keeps its slab
+    if world > 1:
+        from paper_2507_05643_b200 import dist as cdist
+        nid = cdist.bootstrap_nccl_id(rank)
+        g = crm.load_scenario(sc, device=local, rank=rank, world=world, nccl_id=nid)
+    else:
+        g = crm.load_scenario(sc, device=local)
     stream = torch.cuda.ExternalStream(g.stream(), device=local)
 
     def barrier():
         if dist is not None:
             dist.barrier()
 
-    # warm-up
+    # warm-up (the first step also builds the NCCL communicator)
+    barrier()
     g.step(sc.dt, args.warmup)
-    # pair / candidate counts of the current state (algorithmic work of the rates kernels)
-    st = g.structure()
-    counts = st["counts"].astype(np.int64)
-    tags_fluid = np.zeros(n_fluid + n_bce, bool); tags_fluid[:n_fluid] = True
-    pairs_fluid = int(counts[:n_fluid].sum())
-    cs = st["cell_start"].astype(np.int64)
+    # directed fluid pairs of this rank (algorithmic work of the rates kernels)
+    pairs_local = g.pair_count()
+    pairs_fluid = pairs_local
+    if dist is not None:
+        t = torch.tensor([pairs_local], dtype=torch.int64, device=f"cuda:{local}")
+        dist.all_reduce(t)
+        pairs_fluid = int(t.item())
 
     g.profile(True)
     g.profile_reset()
@@ -249,7 +257,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_step = ms / args.steps
-    value = world * n_fluid / (ms_step * 1e-3)
+    value = n_fluid / (ms_step * 1e-3)     # the whole job: every fluid particle, once per step
 
     pk = peaks()
     # dominant kernel and its roofline
@@ -257,7 +265,8 @@ def main():
     dname, (dms, dl) = dom
     per_launch_s = dms / dl * 1e-3
     if dname in ("k_rates_A", "k_rates_B"):
-        flops = pairs_fluid * FLOPS_PER_PAIR + n_fluid * FLOPS_EPILOGUE[dname]
+        n_own = g.count(crm.CRM_OWNED) if world > 1 else n_fluid
+        flops = pairs_local * FLOPS_PER_PAIR + min(n_own, n_fluid) * FLOPS_EPILOGUE[dname]
         achieved = flops / per_launch_s / 1e12
         peak = fp32_peak_tflops(pk["sm_max_mhz"])
         roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
@@ -302,7 +311,7 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             te = float(t.item())
         nbytes = n * 13 * 8
-        e2e = {"value": world * n / (te / ke), "unit": UNIT, "h2d_bytes_per_step": nbytes,
+        e2e = {"value": n / (te / ke), "unit": UNIT, "h2d_bytes_per_step": nbytes,
                "d2h_bytes_per_step": nbytes, "steps": ke,
                "note": "per step: crm_set_state(all fluid, fp64 pinned) + crm_step(dt,1) + crm_get_state; host wall clock"}
 
@@ -312,13 +321,13 @@ def main():
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "config": {"workload": args.config, "n_fluid": n_fluid, "n_bce": n_bce, "d0": sc.params["d0"],
                            "h": sc.params["h"], "dt": sc.dt, "pairs_fluid": pairs_fluid,
-                           "particle_updates_incl_bce_per_s": world * (n_fluid + n_bce) / (ms_step * 1e-3),
+                           "particle_updates_incl_bce_per_s": (n_fluid + n_bce) / (ms_step * 1e-3),
                            "l2": "inputs larger than L2 (56 B x N state >> 126 MB), no flush",
-                           "parallelism": f"replica x{world}" if world > 1 else "single GPU"},
+                           "parallelism": f"x-slabs x{world}, NCCL ghost planes" if world > 1 else "single GPU"},
                 "roofline": roof, "hbm_roofline": hbm, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clocks}
         print(json.dumps(line), flush=True)

@@ -176,6 +176,10 @@ int     crm_profile_reset(crm_t* ctx);
 const char* crm_kernel_name(int kernel);        /* NULL past the last kernel */
 /* Use a CUDA graph for the per-step launch sequence (default on). */
 int     crm_set_graphs(crm_t* ctx, int on);
+/* Number of directed fluid-particle pairs |P(i)| summed over this rank's owned fluid particles,
+ * as built by the last step (the work of the rates loops; bench.py roofline).  CRM_E_STATE before
+ * the first step. */
+int     crm_pair_count(crm_t* ctx, int64_t* fluid_pairs);
 
 /* ---- test-only exports (parity harness) ---- */
 /* Arm/disarm capture of per-step rates and BCE values (costs extra HBM writes). */

@@ -25,6 +25,7 @@ EXPORTS = [
     "crm_stream", "crm_launch_count", "crm_profile_enable", "crm_profile_read", "crm_profile_reset",
     "crm_kernel_name", "crm_set_graphs", "crm_debug_arm", "crm_debug_structure", "crm_debug_neighbors",
     "crm_debug_rates", "crm_debug_bce", "crm_group_step", "crm_nccl_unique_id", "crm_slab_partition",
+    "crm_pair_count",
 ]
 
 
@@ -98,6 +99,7 @@ def load_library(path: str = LIB_PATH):
     L.crm_group_step.argtypes = [C.POINTER(vp), C.c_int, C.c_double, C.c_int64]
     L.crm_nccl_unique_id.argtypes = [C.c_void_p]
     L.crm_slab_partition.argtypes = [_I64, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int)]
+    L.crm_pair_count.argtypes = [vp, _I64]
     _lib = L
     return L
 
@@ -271,6 +273,11 @@ class Crm:
             if nl.value:
                 out[nm] = (ms.value, nl.value)
         return out
+
+    def pair_count(self) -> int:
+        v = C.c_int64()
+        self._chk(self._L.crm_pair_count(self.h, C.byref(v)), "crm_pair_count")
+        return v.value
 
     def set_graphs(self, on: bool):
         self._chk(self._L.crm_set_graphs(self.h, 1 if on else 0), "crm_set_graphs")

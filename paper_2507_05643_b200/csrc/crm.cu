@@ -711,6 +711,23 @@ int crm_nccl_unique_id(void* out128) {
   return CRM_OK;
 }
 
+int crm_pair_count(crm_t* c, int64_t* fluid_pairs) {
+  if (!c || !fluid_pairs) return CRM_E_INVALID;
+  if (!c->committed || c->steps_done == 0) return fail(c, CRM_E_STATE, "no step taken yet");
+  unsigned long long* d = nullptr;
+  CK(cudaMalloc(&d, 8));
+  CK(cudaMemsetAsync(d, 0, 8, c->stream));
+  const int n = (int)c->nl;
+  launch(c, KID_SLAB, k_pair_count, dim3(blocks(n, 256)), dim3(256), n, (const float4*)c->U[c->cur],
+         (const uint32_t*)c->count_all, d);
+  unsigned long long h = 0;
+  CK(cudaMemcpyAsync(&h, d, 8, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  cudaFree(d);
+  *fluid_pairs = (int64_t)h;
+  return CRM_OK;
+}
+
 int crm_slab_partition(const int64_t* plane_counts, int nplanes, int world, int align, int* bounds) {
   if (!plane_counts || !bounds) return CRM_E_INVALID;
   return slab_partition(plane_counts, nplanes, world, align, bounds);

@@ -148,6 +148,19 @@ __global__ void k_check_plane(const float4* __restrict__ P, const uint32_t* __re
   if (!(f == (float)plane)) latch_error(err, -2 /*CRM_E_DOMAIN*/, (long long)ids[s], step, 1);
 }
 
+// sum of |P(i)| over owned fluid particles (the directed pairs of the rates loops)
+__global__ void k_pair_count(int n, const float4* __restrict__ U, const uint32_t* __restrict__ count_all,
+                             unsigned long long* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long v = 0;
+  if (i < n) {
+    const uint32_t t = tag_of(U[i].w);
+    if (!tag_is_bce(t) && !tag_ghost(t)) v = count_all[i];
+  }
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd(out, v);
+}
+
 __global__ void k_fill_u32(uint32_t* __restrict__ p, long long n, uint32_t v) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) p[i] = v;
