@@ -186,6 +186,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-next", action="store_true", help="skip the ps_freq = 10 (Alg. 2) measurement")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -315,6 +316,39 @@ def main():
                "d2h_bytes_per_step": nbytes, "steps": ke,
                "note": "per step: crm_set_state(all fluid, fp64 pinned) + crm_step(dt,1) + crm_get_state; host wall clock"}
 
+    # the same workload with persistent neighbour lists (Alg. 2, ps_freq = 10);
+    # a separate context, timed the same way (reported beside the ps_freq = 1 headline, not instead)
+    nxt = None
+    if not args.no_next:
+        g.close()
+        sc10 = scenario(args.config)
+        sc10.params["ps_freq"] = 10
+        if world > 1:
+            g10 = crm.load_scenario(sc10, device=local, rank=rank, world=world, nccl_id=cdist.bootstrap_nccl_id(rank))
+        else:
+            g10 = crm.load_scenario(sc10, device=local)
+        s10 = torch.cuda.ExternalStream(g10.stream(), device=local)
+        barrier()
+        g10.step(sc10.dt, args.warmup)
+        barrier()
+        torch.cuda.synchronize()
+        k10 = 10 * max(1, args.steps // 10)
+        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(s10)
+        g10.step(sc10.dt, k10)
+        e1.record(s10)
+        torch.cuda.synchronize()
+        barrier()
+        t10 = e0.elapsed_time(e1)
+        if dist is not None:
+            t = torch.tensor([t10], device=f"cuda:{local}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            t10 = float(t.item())
+        nxt = {"ps_freq": 10, "steps": k10, "ms_per_step": t10 / k10, "value": n_fluid / (t10 / k10 * 1e-3),
+               "unit": UNIT, "speedup_vs_ps1": ms_step / (t10 / k10),
+               "note": "Alg. 2 persistent lists (P:770-806): rebuild every 10 steps; paper: 1.28-1.36x (P:866)"}
+        g10.close()
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = oracle_rate(args.config, 12)
@@ -329,7 +363,7 @@ def main():
                            "l2": "inputs larger than L2 (56 B x N state >> 126 MB), no flush",
                            "parallelism": f"x-slabs x{world}, NCCL ghost planes" if world > 1 else "single GPU"},
                 "roofline": roof, "hbm_roofline": hbm, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": launches, "clocks": clocks}
+                "gpu_launches": launches, "clocks": clocks, "next_alg2": nxt}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()

@@ -41,7 +41,7 @@ class Params(C.Structure):
                 ("grain_d", C.c_double), ("d0", C.c_double), ("h", C.c_double),
                 ("support", C.c_double), ("visc_mode", C.c_int), ("gamma_a", C.c_double),
                 ("xi2", C.c_double), ("cs", C.c_double), ("gravity", C.c_double * 3),
-                ("lo", C.c_double * 3), ("hi", C.c_double * 3)]
+                ("lo", C.c_double * 3), ("hi", C.c_double * 3), ("ps_freq", C.c_int)]
 
 
 class BodyS(C.Structure):
@@ -157,6 +157,7 @@ def make_params(p: dict) -> Params:
               "support", "gamma_a", "xi2", "cs"):
         setattr(P, k, float(p.get(k, 0.0)))
     P.visc_mode = int(p.get("visc_mode", 0))
+    P.ps_freq = int(p.get("ps_freq", 1))
     for k in ("gravity", "lo", "hi"):
         v = p.get(k, (0.0, 0.0, 0.0))
         setattr(P, k, (C.c_double * 3)(*[float(t) for t in v]))

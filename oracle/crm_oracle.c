@@ -207,6 +207,7 @@ struct oc_sim {
   double* xl;                 /* marker position in its body's frame */
   int nb; body_rec bodies[OC_MAX_BODIES];
   int64_t steps_done;
+  void* kept;                 /* structure_t of the last rebuild (Alg. 2) */
   double* rates[2];           /* per stage: n * 10 (drho, acc3, dsig6) */
   double* bce[2];             /* per stage: n * 9 (u3, sig6) */
   char err[256];
@@ -251,10 +252,13 @@ int oc_create(const oc_params* p, oc_sim** out) {
   return OC_OK;
 }
 
+static void drop_kept(oc_sim* s);
+
 void oc_destroy(oc_sim* s) {
   if (!s) return;
   free(s->kind); free(s->body); free(s->x); free(s->u); free(s->rho); free(s->sig); free(s->xl);
   free(s->rates[0]); free(s->rates[1]); free(s->bce[0]); free(s->bce[1]);
+  drop_kept(s);
   free(s);
 }
 
@@ -350,6 +354,13 @@ typedef struct {
 static void free_structure(structure_t* st) {
   free(st->cell); free(st->sorted); free(st->cell_start); free(st->offset); free(st->list);
   memset(st, 0, sizeof(*st));
+}
+
+static void drop_kept(oc_sim* s) {
+  if (!s->kept) return;
+  free_structure((structure_t*)s->kept);
+  free(s->kept);
+  s->kept = NULL;
 }
 
 static const uint32_t* g_sort_cell;   /* qsort context (single-threaded) */
@@ -620,9 +631,26 @@ static int check_finite(oc_sim* s) {
 static int step_once(oc_sim* s, double dt) {
   const int64_t n = s->n;
   int rc;
-  structure_t st;
-  /* neighbour lists at y_n, reused by both stages (Alg. 2 with ps_freq = 1; A17) */
-  if ((rc = build_structure(s, s->x, &st, 1)) != OC_OK) return rc;
+  /* Alg. 2: "if t mod ps_freq = 0: rebuild neighbor lists based on current positions";
+   * otherwise the (potentially stale) lists of the last rebuild are used as they are.
+   * Both RK stages use the same lists (A17). */
+  const int ps_freq = s->P.ps_freq > 0 ? s->P.ps_freq : 1;
+  structure_t* kept = (structure_t*)s->kept;
+  if (!kept || s->steps_done % ps_freq == 0) {
+    if (!kept) {
+      kept = (structure_t*)calloc(1, sizeof(structure_t));
+      if (!kept) return OC_E_OOM;
+      s->kept = kept;
+    } else {
+      free_structure(kept);
+    }
+    if ((rc = build_structure(s, s->x, kept, 1)) != OC_OK) {
+      free(kept);
+      s->kept = NULL;
+      return rc;
+    }
+  }
+  const structure_t st = *kept;
   double* xm = (double*)malloc((size_t)n * 3 * sizeof(double));
   double* um = (double*)malloc((size_t)n * 3 * sizeof(double));
   double* rm = (double*)malloc((size_t)n * sizeof(double));
@@ -755,7 +783,6 @@ static int step_once(oc_sim* s, double dt) {
   rc = check_finite(s);
 done:
   free(xm); free(um); free(rm); free(sm); free(ub); free(ab);
-  free_structure(&st);
   return rc;
 }
 
@@ -797,6 +824,7 @@ int oc_set_state(oc_sim* s, int64_t first, int64_t count, const double* pos, con
     if (rho && s->kind[i] == OC_FLUID) s->rho[i] = rho[k];
     if (sig6) for (int c = 0; c < 6; ++c) s->sig[6 * i + c] = sig6[6 * k + c];
   }
+  if (pos) drop_kept(s);   /* positions changed: the next step rebuilds the lists */
   return OC_OK;
 }
 

@@ -39,6 +39,7 @@ typedef struct {
   double gamma_a, xi2, cs;        /* xi2 <= 0 -> 0.01 h^2 (A10); cs <= 0 -> sqrt(K/rho0) (A10) */
   double gravity[3];              /* f_b for fluid */
   double lo[3], hi[3];            /* fixed grid box (A19) */
+  int    ps_freq;                 /* Alg. 2: lists rebuilt when t mod ps_freq = 0; <= 0 -> 1 */
 } oc_params;
 
 typedef struct {

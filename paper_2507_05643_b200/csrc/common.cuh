@@ -59,6 +59,7 @@ struct Phys {
   float kin_b;             // -3 fnorm
   float kout;              // -0.75 h fnorm       : W'/r = kout (2 - q)^2 / r       (1 <= q < 2)
   float c_av;              // 2 m gamma_a h c_s   : AV coefficient numerator (Eq. 13)
+  int build_lists;         // stage A filters and stores the lists (rebuild step of Alg. 2)
 };
 
 // MUFU approximations (no IEEE/denormal wrappers): max rel. error ~2^-22 (rsqrt, rcp)

@@ -100,6 +100,9 @@ struct crm {
   size_t stage_cap = 0;
   double poses_dt = -1.0;
   bool graphs = true;
+  int ps_freq = 1;                      // Alg. 2: lists rebuilt when step % ps_freq == 0
+  bool lists_valid = false;             // the stored lists/sort match the current slots
+  bool slab_rebuild = true;             // this slab step rebuilds (migration, ghosts, sort, lists)
 
   // multi-GPU slab decomposition along x
   int rank = 0, world = 1;

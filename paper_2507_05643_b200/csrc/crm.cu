@@ -273,7 +273,12 @@ void issue_rates(crm_t* c, int stage, float dt, long long step) {
 
 // one RK2 step on one GPU (everything on the stream, no host sync)
 void issue_step(crm_t* c, float dt, long long step) {
-  issue_sort(c, step, 0);
+  // Alg. 2: rebuild (sort + filtered lists) when t mod ps_freq == 0; otherwise the particles keep
+  // their slots and the stored lists are reused without a distance re-check (A17)
+  const bool rebuild = !c->lists_valid || (step % c->ps_freq) == 0;
+  if (rebuild) issue_sort(c, step, 0);
+  c->ph.build_lists = rebuild ? 1 : 0;
+  c->lists_valid = true;
   issue_bce(c, 0, dt, step, 0);
   issue_rates(c, 0, dt, step);
   const int y = c->cur;
@@ -391,7 +396,6 @@ int crm_create(const crm_material_t* mat, const crm_kernel_t* ker, const crm_bou
     return CRM_E_INVALID;
   if (k.kernel != CRM_KERNEL_CUBIC || (k.support != 0.0 && k.support != 2.0)) return CRM_E_UNSUPPORTED;
   if (bnd->method != CRM_BC_ADAMI) return CRM_E_UNSUPPORTED;
-  if (k.ps_freq > 1) return CRM_E_UNSUPPORTED;
   if (k.ps_freq < 0) return CRM_E_INVALID;
   if (k.visc_mode != CRM_VISC_BILATERAL && k.visc_mode != CRM_VISC_UNILATERAL) return CRM_E_INVALID;
   if (dist && (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world)) return CRM_E_INVALID;
@@ -445,6 +449,8 @@ int crm_create(const crm_material_t* mat, const crm_kernel_t* ker, const crm_bou
   c->ph.coh = (float)m.cohesion;
   c->ph.grain_d = (float)m.grain_d;
   c->ph.unilateral = k.visc_mode == CRM_VISC_UNILATERAL;
+  c->ph.build_lists = 1;
+  c->ps_freq = k.ps_freq > 0 ? k.ps_freq : 1;
   {
     const double fnorm = 1.0 / (M_PI * h * h * h * h * h);
     c->ph.kin_a = (float)(2.25 * fnorm / h);
@@ -779,6 +785,7 @@ int crm_set_state(crm_t* c, int64_t first, int64_t count, const double* pos, con
   double* dr = dv + 3 * count;
   double* ds = dr + count;
   if (pos) CK(cudaMemcpyAsync(dp, pos, count * 3 * 8, cudaMemcpyHostToDevice, c->stream));
+  if (pos) c->lists_valid = false;   // positions changed: the next step rebuilds the structure
   if (vel) CK(cudaMemcpyAsync(dv, vel, count * 3 * 8, cudaMemcpyHostToDevice, c->stream));
   if (rho) CK(cudaMemcpyAsync(dr, rho, count * 8, cudaMemcpyHostToDevice, c->stream));
   if (sig6) CK(cudaMemcpyAsync(ds, sig6, count * 6 * 8, cudaMemcpyHostToDevice, c->stream));
@@ -823,6 +830,8 @@ int crm_debug_structure(crm_t* c, uint32_t* cell_by_id, int64_t* sorted_ids, uin
   if (n_cells) *n_cells = c->grid.M;
   if (!cell_by_id && !sorted_ids && !nbr_count_by_id && !cell_start) return CRM_OK;
   issue_sort(c, c->steps_done, 0);
+  c->ph.build_lists = 1;
+  c->lists_valid = true;
   issue_bce(c, 0, 0.0f, c->steps_done, 0);
   issue_rates(c, 0, 0.0f, c->steps_done);
   r = read_latch(c);
@@ -848,6 +857,8 @@ int crm_debug_neighbors(crm_t* c, int64_t* offsets, int64_t* list) {
   int r = commit(c);
   if (r) return r;
   issue_sort(c, c->steps_done, 0);
+  c->ph.build_lists = 1;
+  c->lists_valid = true;
   issue_bce(c, 0, 0.0f, c->steps_done, 1);
   issue_rates(c, 0, 0.0f, c->steps_done);
   const size_t n = (size_t)c->n;

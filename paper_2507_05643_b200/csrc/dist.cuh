@@ -208,6 +208,9 @@ int slab_phase(crm_t* c, int k, float dt, long long step) {
   const int L = c->rank - 1, R = c->rank + 1;
   switch (k) {
     case 0: {   // sort owned particles (drop last step's ghosts), count emigrants
+      // Alg. 2: between rebuilds the slots, ghost sets and lists stay; only values move (phase 3)
+      c->slab_rebuild = !c->lists_valid || (step % c->ps_freq) == 0;
+      if (!c->slab_rebuild) return CRM_OK;
       issue_sort(c, step, TAG_GHOST | TAG_DROP);
       const int ps[4] = {c->x_lo, c->x_lo + 1, c->x_hi - 1, c->x_hi};
       uint32_t st[4], nk;
@@ -221,6 +224,7 @@ int slab_phase(crm_t* c, int k, float dt, long long step) {
       return post_counts(c, c->mig_l, 0, c->mig_r, 0);
     }
     case 1: {   // emigrant payloads: [0, s_lo) -> left, [s_hi, nl) -> right; immigrants appended
+      if (!c->slab_rebuild) return CRM_OK;
       if (int r = read_counts(c, &c->rcv_l, nullptr, &c->rcv_r, nullptr)) return r;
       const uint32_t nl = (uint32_t)c->nl;
       if ((int64_t)nl + c->rcv_l + c->rcv_r > c->ncap) return fail(c, CRM_E_CAPACITY, "slab capacity exceeded (immigrants)");
@@ -232,6 +236,7 @@ int slab_phase(crm_t* c, int k, float dt, long long step) {
       return CRM_OK;
     }
     case 2: {   // mark emigrants dropped, check immigrants, count boundary planes
+      if (!c->slab_rebuild) return CRM_OK;
       const int y = c->cur;
       const uint32_t nl = (uint32_t)c->nl;
       if (c->mig_l) launch(c, KID_SLAB, k_or_tag, dim3(blocks(c->mig_l, 256)), dim3(256), c->U[y], 0u, c->mig_l, TAG_DROP);
@@ -247,6 +252,14 @@ int slab_phase(crm_t* c, int k, float dt, long long step) {
       return post_counts(c, c->s_lo1 - c->s_lo, c->rcv_l, c->s_hi - c->s_hi1, c->rcv_r);
     }
     case 3: {   // boundary planes -> neighbours' ghost planes (appended, flagged in phase 4)
+      if (!c->slab_rebuild) {   // reuse step: refresh the ghost values y_n in place
+        const int y = c->cur;
+        post_slice(c, L, true, y, c->s_lo, c->s_lo1, false);
+        post_slice(c, R, true, y, c->s_hi1, c->s_hi, false);
+        post_slice(c, L, false, y, c->s_lom1, c->s_lo, false);
+        post_slice(c, R, false, y, c->s_hi, c->s_hip1, false);
+        return CRM_OK;
+      }
       uint32_t la, lb, ra, rb;
       if (int r = read_counts(c, &la, &lb, &ra, &rb)) return r;
       c->gh_l = la + lb;
@@ -266,21 +279,31 @@ int slab_phase(crm_t* c, int k, float dt, long long step) {
       return CRM_OK;
     }
     case 4: {   // ghosts flagged, local sort, BCE at y_n; boundary planes -> ghosts
-      const int y0 = c->cur;
-      const uint32_t ng = c->gh_l + c->gh_r;
-      if (ng) launch(c, KID_SLAB, k_or_tag, dim3(blocks(ng, 256)), dim3(256), c->U[y0], c->n_app, c->n_app + ng, TAG_GHOST);
-      c->nl = c->n_app + ng;
-      issue_sort(c, step, TAG_DROP);
-      const int ps[6] = {c->x_lo - 1, c->x_lo, c->x_lo + 1, c->x_hi - 1, c->x_hi, c->x_hi + 1};
-      uint32_t st[6], nk;
-      if (int r = read_plane_starts(c, ps, 6, st)) return r;
-      const int pm[1] = {c->grid.dims[0]};
-      if (int r = read_plane_starts(c, pm, 1, &nk)) return r;
-      c->nl = nk;
-      c->s_lom1 = c->rank > 0 ? st[0] : st[1];
-      c->s_lo = st[1]; c->s_lo1 = st[2]; c->s_hi1 = st[3]; c->s_hi = st[4];
-      c->s_hip1 = c->rank < c->world - 1 ? st[5] : st[4];
-      c->n_owned = c->s_hi - c->s_lo;
+      if (c->slab_rebuild) {
+        const int y0 = c->cur;
+        const uint32_t ng = c->gh_l + c->gh_r;
+        if (ng) launch(c, KID_SLAB, k_or_tag, dim3(blocks(ng, 256)), dim3(256), c->U[y0], c->n_app, c->n_app + ng, TAG_GHOST);
+        c->nl = c->n_app + ng;
+        issue_sort(c, step, TAG_DROP);
+        const int ps[6] = {c->x_lo - 1, c->x_lo, c->x_lo + 1, c->x_hi - 1, c->x_hi, c->x_hi + 1};
+        uint32_t st[6], nk;
+        if (int r = read_plane_starts(c, ps, 6, st)) return r;
+        const int pm[1] = {c->grid.dims[0]};
+        if (int r = read_plane_starts(c, pm, 1, &nk)) return r;
+        c->nl = nk;
+        c->s_lom1 = c->rank > 0 ? st[0] : st[1];
+        c->s_lo = st[1]; c->s_lo1 = st[2]; c->s_hi1 = st[3]; c->s_hi = st[4];
+        c->s_hip1 = c->rank < c->world - 1 ? st[5] : st[4];
+        c->n_owned = c->s_hi - c->s_lo;
+      } else {   // the refreshed ghost values carried the owners' tags
+        const int y0 = c->cur;
+        if (c->s_lo > c->s_lom1)
+          launch(c, KID_SLAB, k_or_tag, dim3(blocks(c->s_lo - c->s_lom1, 256)), dim3(256), c->U[y0], c->s_lom1, c->s_lo, TAG_GHOST);
+        if (c->s_hip1 > c->s_hi)
+          launch(c, KID_SLAB, k_or_tag, dim3(blocks(c->s_hip1 - c->s_hi, 256)), dim3(256), c->U[y0], c->s_hi, c->s_hip1, TAG_GHOST);
+      }
+      c->ph.build_lists = c->slab_rebuild ? 1 : 0;
+      c->lists_valid = true;
       issue_bce(c, 0, dt, step, 0);
       const int y = c->cur;
       post_slice(c, L, true, y, c->s_lo, c->s_lo1, false);

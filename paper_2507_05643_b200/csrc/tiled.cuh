@@ -105,7 +105,7 @@ __device__ __forceinline__ void bce_tile(const Grid& g, const Phys& ph, TileSmem
     if (!tag_is_bce(tag)) continue;
     const float4 pa = P[i];
     uint32_t nl;
-    if (STAGE == 0) {
+    if (STAGE == 0 && ph.build_lists) {   // Alg. 2: rebuild at t mod ps_freq == 0, else reuse
       const int r_self = (1 + q / TY) * WRY + (1 + q % TY);
       const uint32_t self = sm.run_base[r_self] + (i - sm.run_start[r_self]);
       const int cz = (int)(cell_of[i] % (uint32_t)g.dims[2]);
@@ -287,7 +287,7 @@ __device__ __forceinline__ void rates_tile(const Grid& g, const Phys& ph, float 
     if (bce && !(STAGE == 1 && tag_moving(tag))) continue;
     const float4 pi = P[i];
     uint32_t nl;
-    if (STAGE == 0) {
+    if (STAGE == 0 && ph.build_lists) {   // Alg. 2: rebuild at t mod ps_freq == 0, else reuse
       const int r_self = (1 + q / TY) * WRY + (1 + q % TY);
       const uint32_t self = sm.run_base[r_self] + (i - sm.run_start[r_self]);
       const int cz = (int)(cell_of[i] % (uint32_t)g.dims[2]);

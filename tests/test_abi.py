@@ -68,10 +68,10 @@ def test_invalid_parameters_rejected_before_device(lib):
     with pytest.raises(crm.CrmError) as e:
         crm.Crm(p)
     assert e.value.code == crm.CRM_E_INVALID
-    p = dict(sc.params, ps_freq=10)                   # Alg. 2 persistence: not in this build
+    p = dict(sc.params, ps_freq=-1)                   # Alg. 2 period must be >= 1
     with pytest.raises(crm.CrmError) as e:
         crm.Crm(p)
-    assert e.value.code == crm.CRM_E_UNSUPPORTED
+    assert e.value.code == crm.CRM_E_INVALID
 
 
 def test_no_cpu_fallback_without_gpu(lib):

@@ -52,3 +52,15 @@ def test_block_with_migration_bit_identical(crm):
     assert np.abs(got[0][: sc.n_fluid, 0] - x0).max() > 2e-3   # the block really moved
     for a, b in zip(got, ref.get_state()):
         assert np.array_equal(a, b)
+
+
+def test_slabs_with_persistent_lists_bit_identical(crm):
+    sc = workloads.block_settle()
+    sc.params["ps_freq"] = 5
+    sc.fluid_vel = np.zeros_like(sc.fluid_pos)
+    sc.fluid_vel[:, 0] = 1.0
+    ref = crm.load_scenario(sc)
+    ref.step(sc.dt, 23)
+    got, _ = run_slabs(crm, sc, 2, 23)
+    for a, b in zip(got, ref.get_state()):
+        assert np.array_equal(a, b)

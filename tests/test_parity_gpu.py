@@ -280,3 +280,38 @@ def test_crater_body_loads_and_penetration(crm):
     do = z0 - o.get_body(1)["pos"][2]
     assert do > 0.002
     assert abs(dg - do) <= 0.02 * do
+
+
+# ---------------------------------------------------------------- Alg. 2 persistent lists (NEXT #1)
+def test_alg2_stale_pairs_like_oracle(crm):
+    h = 0.01
+    p = workloads.base_params(rho0=1000.0, mu_s=0.5, mu_2=0.5, I0=0.08, cohesion=0.0, grain_d=1e-3, d0=h, h=h,
+                              visc_mode=0, gamma_a=0.5, lo=(-0.1,) * 3, hi=(0.1,) * 3, gravity=(0.0, 0.0, 0.0))
+    p["ps_freq"] = 10
+    x = np.array([[0.0, 0.0, 0.0], [2.02 * h, 0.0, 0.0]])
+    v = np.array([[1.0, 0.0, 0.0], [-1.0, 0.0, 0.0]])
+    g = crm.Crm(p)
+    g.add_fluid(x, v)
+    g.debug_arm(True)
+    for _ in range(10):
+        g.step(1e-4, 1)
+        assert np.abs(g.last_rates(0)[1]).max() == 0      # the step-0 list is empty and reused
+    g.step(1e-4, 1)                                        # t = 10: rebuild
+    assert np.abs(g.last_rates(0)[1]).max() > 0
+
+
+def test_alg2_ps10_trajectory_and_rates(crm):
+    sc = workloads.rate_state_S0(workloads.block_settle())
+    sc.params["ps_freq"] = 10
+    g, o = both(crm, sc)
+    g.step(sc.dt, 13)
+    o.step(sc.dt, 13)
+    g.debug_arm(True)
+    g.step(sc.dt, 1)          # t = 13: a reuse step
+    o.step(sc.dt, 1)
+    nf = sc.n_fluid
+    for a, b in zip(g.last_rates(0), o.last_rates(0)):
+        assert rel_linf(a[:nf], b[:nf]) <= 1e-3
+    xg = g.get_state()[0][:nf]
+    xo = o.get_state()[0][:nf]
+    assert np.abs(xg - xo).max() < 1e-3 * sc.params["d0"]
