@@ -865,12 +865,12 @@ int crm_debug_neighbors(crm_t* c, int64_t* offsets, int64_t* list) {
   if (!c->list32 && dalloc(c, &c->list32, n * (size_t)c->cap)) return CRM_E_OOM;
   launch(c, KID_DECODE, k_decode_lists, dim3(blocks((long long)n, 256)), dim3(256), (int)n, c->grid,
          (const uint32_t*)c->cell_start, (const uint32_t*)c->cell_of, (const uint16_t*)c->list,
-         (const uint32_t*)c->nlist, c->cap, c->list32);
+         (const uint32_t*)c->nlist, c->cap, c->list32, c->tmp_id /* decoded counts (scratch) */);
   r = read_latch(c);
   if (r) return r;
   std::vector<uint32_t> ids(n), nl(n);
   CK(cudaMemcpy(ids.data(), c->ids[c->cur], n * 4, cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(nl.data(), c->nlist, n * 4, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(nl.data(), c->tmp_id, n * 4, cudaMemcpyDeviceToHost));
   std::vector<uint32_t> cnt_by_id(n);
   for (size_t s = 0; s < n; ++s) cnt_by_id[ids[s]] = nl[s];
   offsets[0] = 0;

@@ -38,26 +38,31 @@ __device__ __forceinline__ void load_all(const TileSmem& sm, const float4* __res
 // offsets (all neighbours if store_bce, else fluid ones only); returns |P(i)|.  The candidate
 // order (runs in (da, db) order, offsets ascending) fixes the list order, hence the summation
 // order of the pair loops (deterministic).
-template <bool STAGED>
+template <bool STAGED, bool STORE_BCE>
 __device__ __forceinline__ void filter_range(const Grid& g, const TileSmem& sm, const float4* __restrict__ P,
                                              const float4* __restrict__ U, uint32_t ob, uint32_t oe, uint32_t gshift,
-                                             const float4& pi, bool store_bce, uint32_t& cnt, ListWriter& w) {
-  // chunks of 32 candidates: a branch-free predicate sweep builds a bitmask, then the set bits
-  // are appended in ascending order (same order as a plain loop)
+                                             const float4& pi, uint32_t self, uint32_t& cnt, ListWriter& w) {
+  // chunks of 32 candidates: a branch-free predicate sweep builds a bitmask (and, for marker
+  // lists, a mask of the fluid candidates), then the set bits are appended in ascending order
+  // two at a time (an odd last one is paired with `self`, a zero-weight entry)
   for (uint32_t base = ob; base < oe; base += 32) {
     const uint32_t nc = min(32u, oe - base);
-    uint32_t m = 0;
+    uint32_t m = 0, mf = 0;
 #pragma unroll 4
     for (uint32_t k = 0; k < nc; ++k) {
       const float4 pj = STAGED ? sm.P[base + k] : P[base + k + gshift];
-      m |= (b2_pred(pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, g.R2) ? 1u : 0u) << k;
+      const uint32_t bit = (b2_pred(pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, g.R2) ? 1u : 0u) << k;
+      m |= bit;
+      if (!STORE_BCE) {
+        const float tw = STAGED ? sm.U[base + k].w : U[base + k + gshift].w;
+        mf |= tag_is_bce(tag_of(tw)) ? 0u : bit;
+      }
     }
     cnt += __popc(m);
-    while (m) {
-      const uint32_t b = __ffs(m) - 1;
-      m &= m - 1;
-      const uint32_t off = base + b;
-      if (store_bce || !tag_is_bce(tag_of(STAGED ? sm.U[off].w : U[off + gshift].w))) w.push(off);
+    uint32_t s = STORE_BCE ? m : mf;
+    while (s) {   // (measured: branch-free funnel-shift appends beat paired/branchy appends)
+      w.push(base + (__ffs(s) - 1));
+      s &= s - 1;
     }
   }
 }
@@ -77,11 +82,20 @@ __device__ __forceinline__ uint32_t filter(const Grid& g, const TileSmem& sm, co
       int r;
       cand_range(sm, q, da, db, cz, ob, oe, r);
       const uint32_t gshift = sm.run_start[r] - sm.run_base[r];
-      if (da == 0 && db == 0) {   // the own run holds i itself (j != i, A18)
-        filter_range<STAGED>(g, sm, P, U, ob, self, gshift, pi, store_bce, cnt, w);
-        filter_range<STAGED>(g, sm, P, U, self + 1, oe, gshift, pi, store_bce, cnt, w);
+      if (store_bce) {
+        if (da == 0 && db == 0) {   // the own run holds i itself (j != i, A18)
+          filter_range<STAGED, true>(g, sm, P, U, ob, self, gshift, pi, self, cnt, w);
+          filter_range<STAGED, true>(g, sm, P, U, self + 1, oe, gshift, pi, self, cnt, w);
+        } else {
+          filter_range<STAGED, true>(g, sm, P, U, ob, oe, gshift, pi, self, cnt, w);
+        }
       } else {
-        filter_range<STAGED>(g, sm, P, U, ob, oe, gshift, pi, store_bce, cnt, w);
+        if (da == 0 && db == 0) {
+          filter_range<STAGED, false>(g, sm, P, U, ob, self, gshift, pi, self, cnt, w);
+          filter_range<STAGED, false>(g, sm, P, U, self + 1, oe, gshift, pi, self, cnt, w);
+        } else {
+          filter_range<STAGED, false>(g, sm, P, U, ob, oe, gshift, pi, self, cnt, w);
+        }
       }
     }
   }
@@ -438,7 +452,8 @@ __global__ void __launch_bounds__(TILE_THREADS, 2)
 // debug: hot-path lists (window offsets) -> global sorted indices, ELL k-major u32
 __global__ void k_decode_lists(int n, Grid g, const uint32_t* __restrict__ cell_start,
                                const uint32_t* __restrict__ cell_of, const uint16_t* __restrict__ list,
-                               const uint32_t* __restrict__ nlist, int cap, uint32_t* __restrict__ out) {
+                               const uint32_t* __restrict__ nlist, int cap, uint32_t* __restrict__ out,
+                               uint32_t* __restrict__ nout) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const uint32_t c = cell_of[i];
@@ -459,12 +474,17 @@ __global__ void k_decode_lists(int n, Grid g, const uint32_t* __restrict__ cell_
     acc += re - rs[r];
   }
   rb[WR] = acc;
+  uint32_t kk = 0;
   for (uint32_t k = 0; k < nlist[i]; ++k) {
     const uint32_t off = list[(size_t)i * cap + k];
     int r = 0;
     for (int q = 1; q < WR; ++q) r += (rb[q] <= off) ? 1 : 0;
-    out[(size_t)k * n + i] = rs[r] + (off - rb[r]);
+    const uint32_t j = rs[r] + (off - rb[r]);
+    if (j == (uint32_t)i) continue;   // zero-weight self padding
+    out[(size_t)kk * n + i] = j;
+    ++kk;
   }
+  nout[i] = kk;
 }
 
 }  // namespace crmk

@@ -168,6 +168,8 @@ struct ListWriter {
     nb = 0;
     k = 0;
     cap = cap_;
+    pend = 0u;
+    hp = false;
   }
   __device__ __forceinline__ void push(uint32_t off) {
     if (k >= cap) { ++k; return; }
@@ -182,7 +184,33 @@ struct ListWriter {
       nb = 0;
     }
   }
+  // one entry; entries are paired into words (the first of a pair waits in `pend`)
+  uint32_t pend;
+  bool hp = false;
+  __device__ __forceinline__ void push_half(uint32_t e) {
+    if (hp) push2(pend | (e << 16));
+    else pend = e;
+    hp = !hp;
+  }
+  // two entries packed in one word (entry e1 in the low half); keeps nb even
+  __device__ __forceinline__ void push2(uint32_t word) {
+    if (k >= cap) { k += 2; return; }
+    b0 = b1;
+    b1 = b2;
+    b2 = b3;
+    b3 = word;
+    nb += 2;
+    k += 2;
+    if (nb == 8) {
+      dst[(k - 8) >> 3] = make_uint4(b0, b1, b2, b3);
+      nb = 0;
+    }
+  }
   __device__ __forceinline__ void flush(uint32_t fill) {
+    if (hp) {
+      push2(pend | (fill << 16));
+      hp = false;
+    }
     if (nb == 0) return;
     const int pad = 8 - nb;
     for (int p = 0; p < pad; ++p) {
