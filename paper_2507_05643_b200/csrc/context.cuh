@@ -100,6 +100,11 @@ struct crm {
   size_t stage_cap = 0;
   double poses_dt = -1.0;
   bool graphs = true;
+  // captured single-GPU steps, keyed by (buffer parity before the step, rebuild step of Alg. 2)
+  cudaGraphExec_t gexec[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  float gdt[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
+  int gcur_after[2][2] = {{0, 0}, {0, 0}};
+  int64_t gkernels[2][2] = {{0, 0}, {0, 0}};
   int ps_freq = 1;                      // Alg. 2: lists rebuilt when step % ps_freq == 0
   bool lists_valid = false;             // the stored lists/sort match the current slots
   bool slab_rebuild = true;             // this slab step rebuilds (migration, ghosts, sort, lists)

@@ -301,6 +301,44 @@ void issue_step(crm_t* c, float dt, long long step) {
   if (c->dbg_on) cudaMemcpyAsync(c->dbg_ids, c->ids[y], (size_t)c->nl * 4, cudaMemcpyDeviceToDevice, c->stream);
 }
 
+// One single-GPU step, replayed from a CUDA graph when possible.  The launch sequence of a step
+// depends only on (buffer parity, rebuild step, dt), so it is captured once per key and replayed;
+// per-kernel profiling and debug capture run the kernels one by one instead.  Errors latched
+// inside a replayed step report step -1 (the host message names the crm_step call instead).
+int run_step(crm_t* c, float dt, long long step) {
+  const bool rebuild = !c->lists_valid || (step % c->ps_freq) == 0;
+  if (!c->graphs || c->prof || c->dbg_on) {
+    issue_step(c, dt, step);
+    return CRM_OK;
+  }
+  const int p = c->cur, q = rebuild ? 1 : 0;
+  if (!c->gexec[p][q] || c->gdt[p][q] != dt) {
+    if (c->gexec[p][q]) cudaGraphExecDestroy(c->gexec[p][q]);
+    c->gexec[p][q] = nullptr;
+    const int64_t l0 = c->launches;
+    const bool valid0 = c->lists_valid;
+    c->lists_valid = !rebuild;   // make issue_step take the same branch as the key
+    cudaGraph_t graph;
+    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    issue_step(c, dt, -1);
+    CK(cudaStreamEndCapture(c->stream, &graph));
+    cudaError_t e = cudaGraphInstantiate(&c->gexec[p][q], graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return fail(c, CRM_E_CUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(e));
+    c->gdt[p][q] = dt;
+    c->gcur_after[p][q] = c->cur;
+    c->gkernels[p][q] = c->launches - l0;
+    c->launches = l0;
+    c->cur = p;
+    c->lists_valid = valid0;
+  }
+  CK(cudaGraphLaunch(c->gexec[p][q], c->stream));
+  c->launches += c->gkernels[p][q];
+  c->cur = c->gcur_after[p][q];
+  c->lists_valid = true;
+  return CRM_OK;
+}
+
 int read_latch(crm_t* c) {
   CK(cudaMemcpyAsync(c->h_err, c->d_err, sizeof(ErrLatch), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
@@ -514,6 +552,8 @@ void crm_destroy(crm_t* c) {
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   for (int b = 0; b < 2; ++b) {
     cudaFree(c->P[b]); cudaFree(c->U[b]); cudaFree(c->S1[b]); cudaFree(c->S2[b]); cudaFree(c->ids[b]);
+    for (int q = 0; q < 2; ++q)
+      if (c->gexec[b][q]) cudaGraphExecDestroy(c->gexec[b][q]);
     cudaFree(c->dbg.drho[b]); cudaFree(c->dbg.acc[b]); cudaFree(c->dbg.ds1[b]); cudaFree(c->dbg.ds2[b]);
     cudaFree(c->dbg.bu[b]); cudaFree(c->dbg.bs1[b]); cudaFree(c->dbg.bs2[b]);
   }
@@ -666,7 +706,7 @@ int crm_step(crm_t* c, double dt, int64_t nsteps) {
   for (int64_t s = 0; s < nsteps; ++s) {
     const long long step = (long long)(c->steps_done + s);
     if (!c->slab) {
-      issue_step(c, (float)dt, step);
+      if ((r = run_step(c, (float)dt, step))) return r;
       continue;
     }
     for (int k = 0; k < kSlabPhases; ++k) {

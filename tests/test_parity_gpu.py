@@ -315,3 +315,17 @@ def test_alg2_ps10_trajectory_and_rates(crm):
     xg = g.get_state()[0][:nf]
     xo = o.get_state()[0][:nf]
     assert np.abs(xg - xo).max() < 1e-3 * sc.params["d0"]
+
+
+def test_cuda_graph_replay_bit_identical(crm):
+    # the captured step (default) equals the kernel-by-kernel step, also across Alg. 2 rebuilds
+    for ps in (1, 3):
+        sc = workloads.block_settle(jitter=0.05)
+        sc.params["ps_freq"] = ps
+        a = crm.load_scenario(sc)
+        b = crm.load_scenario(sc)
+        b.set_graphs(False)
+        a.step(sc.dt, 7)
+        b.step(sc.dt, 7)
+        for x, y in zip(a.get_state(), b.get_state()):
+            assert np.array_equal(x, y)
