@@ -47,10 +47,11 @@ FLOPS_EPILOGUE = {"k_rates_A": 110, "k_rates_B": 170}
 # algorithmic HBM bytes per fluid particle-update and per BCE marker
 BYTES_PER_FLUID_UPDATE = 404
 BYTES_PER_BCE_UPDATE = 72
-# per-kernel algorithmic bytes per particle (for HBM-bound kernels)
+# (the 56-B fp32 state of D4; the 16-B position compensation term L is this design's overhead)
 # bounded oracle sample of the bed workload (~1M fluid; ~1 s per oracle step on a 16-core host)
 SAMPLE_BED = (128, 128, 64)
-KERNEL_BYTES = {"k_bin": 16 + 4 + 8 + 4, "k_scatter": 12 + 8, "k_reorder": 56 + 56 + 24 + 8}
+# per-kernel bytes per particle of the HBM-bound kernels (reorder moves the 72-B state incl. L)
+KERNEL_BYTES = {"k_bin": 16 + 4 + 8 + 4, "k_scatter": 12 + 8, "k_reorder": 72 + 72 + 24 + 8}
 
 
 def peaks():

@@ -57,7 +57,7 @@ struct crm {
   bool own_stream = false;
 
   // host staging (id order) until the first device use
-  std::vector<float4> hP, hU, hS1;
+  std::vector<float4> hP, hL, hU, hS1;
   std::vector<float2> hS2;
   std::vector<int32_t> hBody;   // -1 for fluid
   std::vector<BodyState> bodies;
@@ -69,11 +69,13 @@ struct crm {
   int64_t steps_done = 0;
 
   // device state
-  float4 *P[2] = {nullptr, nullptr}, *U[2] = {nullptr, nullptr}, *S1[2] = {nullptr, nullptr};
+  // P = (x hi, rho), L = (x lo, 0): compensated positions x = hi + lo
+  float4 *P[2] = {nullptr, nullptr}, *L[2] = {nullptr, nullptr}, *U[2] = {nullptr, nullptr};
+  float4* S1[2] = {nullptr, nullptr};
   float2* S2[2] = {nullptr, nullptr};
   uint32_t* ids[2] = {nullptr, nullptr};
   int cur = 0;
-  float4 *Pm = nullptr, *Um = nullptr, *S1m = nullptr;
+  float4 *Pm = nullptr, *Lm = nullptr, *Um = nullptr, *S1m = nullptr;
   float2* S2m = nullptr;
   uint32_t *key = nullptr, *arrival = nullptr, *cell_count = nullptr, *cell_start = nullptr;
   uint32_t *tmp_src = nullptr, *tmp_id = nullptr, *cell_of = nullptr, *slot_of_id = nullptr;
@@ -227,6 +229,12 @@ inline int host_plane(const Grid& g, float x) {
   volatile float t = (x - g.lo[0]);
   volatile float q = t / g.s;
   return (int)std::floor((float)q);
+}
+
+// compensation term of an fp64 position: x - (float)x, per axis
+inline float4 host_lo(const double* x) {
+  return make_float4((float)(x[0] - (double)(float)x[0]), (float)(x[1] - (double)(float)x[1]),
+                     (float)(x[2] - (double)(float)x[2]), 0.f);
 }
 
 }  // namespace

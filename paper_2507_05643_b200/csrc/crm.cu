@@ -89,10 +89,10 @@ int commit(crm_t* c) {
   const size_t n = (size_t)c->ncap;
   int r = 0;
   for (int b = 0; b < 2; ++b) {
-    r |= dalloc(c, &c->P[b], n); r |= dalloc(c, &c->U[b], n); r |= dalloc(c, &c->S1[b], n);
-    r |= dalloc(c, &c->S2[b], n); r |= dalloc(c, &c->ids[b], n);
+    r |= dalloc(c, &c->P[b], n); r |= dalloc(c, &c->L[b], n); r |= dalloc(c, &c->U[b], n);
+    r |= dalloc(c, &c->S1[b], n); r |= dalloc(c, &c->S2[b], n); r |= dalloc(c, &c->ids[b], n);
   }
-  r |= dalloc(c, &c->Pm, n); r |= dalloc(c, &c->Um, n); r |= dalloc(c, &c->S1m, n); r |= dalloc(c, &c->S2m, n);
+  r |= dalloc(c, &c->Pm, n); r |= dalloc(c, &c->Lm, n); r |= dalloc(c, &c->Um, n); r |= dalloc(c, &c->S1m, n); r |= dalloc(c, &c->S2m, n);
   r |= dalloc(c, &c->key, n); r |= dalloc(c, &c->arrival, n);
   r |= dalloc(c, &c->cell_count, (size_t)c->grid.M + 1); r |= dalloc(c, &c->cell_start, (size_t)c->grid.M + 2);
   r |= dalloc(c, &c->tmp_src, n); r |= dalloc(c, &c->tmp_id, n); r |= dalloc(c, &c->cell_of, n);
@@ -161,14 +161,15 @@ int commit(crm_t* c) {
   const size_t nl = (size_t)c->nl;
   std::vector<uint32_t> idv(nl);
   if (c->slab) {
-    std::vector<float4> P(nl), U(nl), S1(nl);
+    std::vector<float4> P(nl), L(nl), U(nl), S1(nl);
     std::vector<float2> S2(nl);
     for (size_t k = 0; k < nl; ++k) {
       const uint32_t i = owned[k];
-      P[k] = c->hP[i]; U[k] = c->hU[i]; S1[k] = c->hS1[i]; S2[k] = c->hS2[i];
+      P[k] = c->hP[i]; L[k] = c->hL[i]; U[k] = c->hU[i]; S1[k] = c->hS1[i]; S2[k] = c->hS2[i];
       idv[k] = i;
     }
     CK(cudaMemcpyAsync(c->P[0], P.data(), nl * 16, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->L[0], L.data(), nl * 16, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->U[0], U.data(), nl * 16, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->S1[0], S1.data(), nl * 16, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->S2[0], S2.data(), nl * 8, cudaMemcpyHostToDevice, c->stream));
@@ -182,6 +183,7 @@ int commit(crm_t* c) {
   } else {
     for (size_t i = 0; i < nl; ++i) idv[i] = (uint32_t)i;
     CK(cudaMemcpyAsync(c->P[0], c->hP.data(), nl * 16, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->L[0], c->hL.data(), nl * 16, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->U[0], c->hU.data(), nl * 16, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->S1[0], c->hS1.data(), nl * 16, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->S2[0], c->hS2.data(), nl * 8, cudaMemcpyHostToDevice, c->stream));
@@ -193,7 +195,7 @@ int commit(crm_t* c) {
   c->cur = 0;
   c->committed = true;
   set_attrs(c);
-  c->hP.clear(); c->hP.shrink_to_fit(); c->hU.clear(); c->hU.shrink_to_fit();
+  c->hP.clear(); c->hP.shrink_to_fit(); c->hL.clear(); c->hL.shrink_to_fit(); c->hU.clear(); c->hU.shrink_to_fit();
   c->hS1.clear(); c->hS1.shrink_to_fit(); c->hS2.clear(); c->hS2.shrink_to_fit();
   // NCCL communicator (collective: every rank commits at the same point)
   if (c->slab && c->has_nccl_id) {
@@ -228,8 +230,9 @@ void issue_sort(crm_t* c, long long step, uint32_t drop_mask) {
     launch(c, KID_SLAB, k_fill_u32, dim3(blocks(c->n, 256)), dim3(256), c->slot_of_id, (long long)c->n, 0xffffffffu);
   launch(c, KID_REORDER, k_reorder, dim3(blocks(n, 256)), dim3(256), n, (const uint32_t*)c->tmp_src,
          (const uint32_t*)c->tmp_id, (const uint32_t*)c->key, (const uint32_t*)c->cell_start,
-         (const float4*)c->P[a], (const float4*)c->U[a], (const float4*)c->S1[a], (const float2*)c->S2[a],
-         c->P[b], c->U[b], c->S1[b], c->S2[b], c->ids[b], c->cell_of, c->slot_of_id, c->grid.M);
+         (const float4*)c->P[a], (const float4*)c->L[a], (const float4*)c->U[a], (const float4*)c->S1[a],
+         (const float2*)c->S2[a], c->P[b], c->L[b], c->U[b], c->S1[b], c->S2[b], c->ids[b], c->cell_of, c->slot_of_id,
+         c->grid.M);
   c->cur = b;
 }
 
@@ -243,13 +246,13 @@ void issue_bce(crm_t* c, int stage, float dt, long long step, int store_all) {
   const size_t sm = sizeof(TileSmem);
   if (stage == 0)
     launch_smem(c, KID_BCE_A, k_bce_t<0>, tg, tb, sm, c->grid, c->ph, (const uint32_t*)c->cell_start,
-                (const float4*)c->P[y], c->U[y], c->S1[y], c->S2[y], c->list, c->nlist, c->count_all,
-                (const uint32_t*)c->cell_of, (const Pose*)c->d_pose0, c->cap, store_all, c->dbg, dbg, c->d_err,
+                (const float4*)c->P[y], (const float4*)c->L[y], c->U[y], c->S1[y], c->S2[y], c->list, c->nlist,
+                c->count_all, (const uint32_t*)c->cell_of, (const Pose*)c->d_pose0, c->cap, store_all, c->dbg, dbg, c->d_err,
                 (const uint32_t*)c->ids[y], step, c->tile_base);
   else
     launch_smem(c, KID_BCE_B, k_bce_t<1>, tg, tb, sm, c->grid, c->ph, (const uint32_t*)c->cell_start,
-                (const float4*)c->Pm, c->Um, c->S1m, c->S2m, c->list, c->nlist, c->count_all,
-                (const uint32_t*)c->cell_of, (const Pose*)c->d_posem, c->cap, 0, c->dbg, dbg, c->d_err,
+                (const float4*)c->Pm, (const float4*)c->Lm, c->Um, c->S1m, c->S2m, c->list, c->nlist,
+                c->count_all, (const uint32_t*)c->cell_of, (const Pose*)c->d_posem, c->cap, 0, c->dbg, dbg, c->d_err,
                 (const uint32_t*)c->ids[y], step, c->tile_base);
 }
 
@@ -261,13 +264,13 @@ void issue_rates(crm_t* c, int stage, float dt, long long step) {
   const size_t sm = sizeof(TileSmem);
   if (stage == 0)
     launch_smem(c, KID_RATES_A, k_rates_t<0>, tg, tb, sm, c->grid, c->ph, dt, (const uint32_t*)c->cell_start,
-                (const float4*)c->P[y], (const float4*)c->U[y], (const float4*)c->S1[y], (const float2*)c->S2[y], c->Pm,
-                c->Um, c->S1m, c->S2m, c->list, c->nlist, c->count_all, (const uint32_t*)c->cell_of, c->cap, c->macc,
+                (const float4*)c->P[y], (const float4*)c->L[y], (const float4*)c->U[y], (const float4*)c->S1[y],
+                (const float2*)c->S2[y], c->Pm, c->Lm, c->Um, c->S1m, c->S2m, c->list, c->nlist, c->count_all, (const uint32_t*)c->cell_of, c->cap, c->macc,
                 c->dbg, dbg, c->d_err, (const uint32_t*)c->ids[y], step, c->tile_base);
   else
     launch_smem(c, KID_RATES_B, k_rates_t<1>, tg, tb, sm, c->grid, c->ph, dt, (const uint32_t*)c->cell_start,
-                (const float4*)c->Pm, (const float4*)c->Um, (const float4*)c->S1m, (const float2*)c->S2m, c->P[y],
-                c->U[y], c->S1[y], c->S2[y], c->list, c->nlist, c->count_all, (const uint32_t*)c->cell_of, c->cap,
+                (const float4*)c->Pm, (const float4*)c->Lm, (const float4*)c->Um, (const float4*)c->S1m,
+                (const float2*)c->S2m, c->P[y], c->L[y], c->U[y], c->S1[y], c->S2[y], c->list, c->nlist, c->count_all, (const uint32_t*)c->cell_of, c->cap,
                 c->macc, c->dbg, dbg, c->d_err, (const uint32_t*)c->ids[y], step, c->tile_base);
 }
 
@@ -285,18 +288,18 @@ void issue_step(crm_t* c, float dt, long long step) {
   if (c->n_moving_markers)
     launch(c, KID_MARKERS, k_markers_place, dim3(blocks(c->n_moving_markers, 128)), dim3(128), c->n_moving_markers,
            (const uint32_t*)c->d_moving_ids, (const float4*)c->d_xlocal, (const uint32_t*)c->slot_of_id,
-           (const Pose*)c->d_posem, c->Pm, (const float4*)c->Um);
+           (const Pose*)c->d_posem, c->Pm, c->Lm, (const float4*)c->Um);
   issue_bce(c, 1, dt, step, 0);
   issue_rates(c, 1, dt, step);
   if (c->n_moving_bodies) {
     launch(c, KID_BODY, k_body_update, dim3(c->n_moving_bodies), dim3(BODY_BS), (const int*)c->d_moving_bodies,
            (const uint32_t*)c->d_mstart, (const uint32_t*)c->d_moving_ids, (const uint32_t*)c->slot_of_id,
-           (const float4*)c->macc, (const float4*)c->Pm, c->d_bodies, (double)dt, c->ph.g[0], c->ph.g[1], c->ph.g[2]);
+           (const float4*)c->macc, (const float4*)c->Pm, (const float4*)c->Lm, c->d_bodies, (double)dt, c->ph.g[0], c->ph.g[1], c->ph.g[2]);
     launch(c, KID_POSES, k_body_poses, dim3(1), dim3(64), (int)c->bodies.size(), (const BodyState*)c->d_bodies,
            0.5 * (double)dt, c->d_pose0, c->d_posem);
     launch(c, KID_MARKERS, k_markers_place, dim3(blocks(c->n_moving_markers, 128)), dim3(128), c->n_moving_markers,
            (const uint32_t*)c->d_moving_ids, (const float4*)c->d_xlocal, (const uint32_t*)c->slot_of_id,
-           (const Pose*)c->d_pose0, c->P[y], (const float4*)c->U[y]);
+           (const Pose*)c->d_pose0, c->P[y], c->L[y], (const float4*)c->U[y]);
   }
   if (c->dbg_on) cudaMemcpyAsync(c->dbg_ids, c->ids[y], (size_t)c->nl * 4, cudaMemcpyDeviceToDevice, c->stream);
 }
@@ -551,13 +554,13 @@ void crm_destroy(crm_t* c) {
   for (auto& r : c->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   for (int b = 0; b < 2; ++b) {
-    cudaFree(c->P[b]); cudaFree(c->U[b]); cudaFree(c->S1[b]); cudaFree(c->S2[b]); cudaFree(c->ids[b]);
+    cudaFree(c->P[b]); cudaFree(c->L[b]); cudaFree(c->U[b]); cudaFree(c->S1[b]); cudaFree(c->S2[b]); cudaFree(c->ids[b]);
     for (int q = 0; q < 2; ++q)
       if (c->gexec[b][q]) cudaGraphExecDestroy(c->gexec[b][q]);
     cudaFree(c->dbg.drho[b]); cudaFree(c->dbg.acc[b]); cudaFree(c->dbg.ds1[b]); cudaFree(c->dbg.ds2[b]);
     cudaFree(c->dbg.bu[b]); cudaFree(c->dbg.bs1[b]); cudaFree(c->dbg.bs2[b]);
   }
-  cudaFree(c->Pm); cudaFree(c->Um); cudaFree(c->S1m); cudaFree(c->S2m);
+  cudaFree(c->Pm); cudaFree(c->Lm); cudaFree(c->Um); cudaFree(c->S1m); cudaFree(c->S2m);
   cudaFree(c->key); cudaFree(c->arrival); cudaFree(c->cell_count); cudaFree(c->cell_start);
   cudaFree(c->tmp_src); cudaFree(c->tmp_id); cudaFree(c->cell_of); cudaFree(c->slot_of_id);
   cudaFree(c->list); cudaFree(c->nlist); cudaFree(c->count_all); cudaFree(c->list32);
@@ -580,7 +583,8 @@ int crm_add_fluid(crm_t* c, int64_t n, const double* pos, const double* vel, con
   const float tag = u2f(make_tag(0, 0, 0));
   for (int64_t k = 0; k < n; ++k) {
     c->hP.push_back(make_float4((float)pos[3 * k], (float)pos[3 * k + 1], (float)pos[3 * k + 2], (float)c->mat.rho0));
-    c->hU.push_back(vel ? make_float4((float)vel[3 * k], (float)vel[3 * k + 1], (float)vel[3 * k + 2], tag)
+    c->hL.push_back(host_lo(pos + 3 * k));
+    c->hU.push_back(vel ?make_float4((float)vel[3 * k], (float)vel[3 * k + 1], (float)vel[3 * k + 2], tag)
                         : make_float4(0.f, 0.f, 0.f, tag));
     if (sig6) {
       c->hS1.push_back(make_float4((float)sig6[6 * k], (float)sig6[6 * k + 1], (float)sig6[6 * k + 2], (float)sig6[6 * k + 3]));
@@ -627,6 +631,7 @@ int crm_add_bce(crm_t* c, int32_t body, int64_t n, const double* pos, int64_t* f
   const float tag = u2f(make_tag(1, (uint32_t)body, moving ? 1 : 0));
   for (int64_t k = 0; k < n; ++k) {
     c->hP.push_back(make_float4((float)pos[3 * k], (float)pos[3 * k + 1], (float)pos[3 * k + 2], (float)c->mat.rho0));
+    c->hL.push_back(host_lo(pos + 3 * k));
     c->hU.push_back(make_float4(0.f, 0.f, 0.f, tag));
     c->hS1.push_back(make_float4(0.f, 0.f, 0.f, 0.f));
     c->hS2.push_back(make_float2(0.f, 0.f));
@@ -794,8 +799,8 @@ int crm_get_state(crm_t* c, int64_t first, int64_t count, double* pos, double* v
   if (c->slab) CK(cudaMemsetAsync(dp, 0xff, (size_t)count * 13 * 8, c->stream));   // NaN rows: not owned here
   const int y = c->cur;
   launch(c, KID_STATE, k_get_state, dim3(blocks(count, 256)), dim3(256), (long long)first, (long long)count,
-         (const uint32_t*)c->slot_of_id, (const float4*)c->P[y], (const float4*)c->U[y], (const float4*)c->S1[y],
-         (const float2*)c->S2[y], dp, dv, dr, ds);
+         (const uint32_t*)c->slot_of_id, (const float4*)c->P[y], (const float4*)c->L[y], (const float4*)c->U[y],
+         (const float4*)c->S1[y], (const float2*)c->S2[y], dp, dv, dr, ds);
   if (pos) CK(cudaMemcpyAsync(pos, dp, count * 3 * 8, cudaMemcpyDeviceToHost, c->stream));
   if (vel) CK(cudaMemcpyAsync(vel, dv, count * 3 * 8, cudaMemcpyDeviceToHost, c->stream));
   if (rho) CK(cudaMemcpyAsync(rho, dr, count * 8, cudaMemcpyDeviceToHost, c->stream));
@@ -831,7 +836,7 @@ int crm_set_state(crm_t* c, int64_t first, int64_t count, const double* pos, con
   if (sig6) CK(cudaMemcpyAsync(ds, sig6, count * 6 * 8, cudaMemcpyHostToDevice, c->stream));
   const int y = c->cur;
   launch(c, KID_STATE, k_set_state, dim3(blocks(count, 256)), dim3(256), (long long)first, (long long)count,
-         (const uint32_t*)c->slot_of_id, c->P[y], c->U[y], c->S1[y], c->S2[y], (const double*)dp, (const double*)dv,
+         (const uint32_t*)c->slot_of_id, c->P[y], c->L[y], c->U[y], c->S1[y], c->S2[y], (const double*)dp, (const double*)dv,
          (const double*)dr, (const double*)ds, pos ? 1 : 0, vel ? 1 : 0, rho ? 1 : 0, sig6 ? 1 : 0);
   CK(cudaStreamSynchronize(c->stream));
   return CRM_OK;

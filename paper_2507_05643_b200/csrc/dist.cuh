@@ -73,6 +73,7 @@ void post_slice(crm_t* c, int peer, bool send, int y, uint32_t b, uint32_t e, bo
   if (e <= b) return;
   const size_t k = e - b;
   post(c, peer, send, c->P[y] + b, k * 16);
+  post(c, peer, send, c->L[y] + b, k * 16);
   post(c, peer, send, c->U[y] + b, k * 16);
   post(c, peer, send, c->S1[y] + b, k * 16);
   post(c, peer, send, c->S2[y] + b, k * 8);
@@ -83,6 +84,7 @@ void post_mid_slice(crm_t* c, int peer, bool send, uint32_t b, uint32_t e) {
   if (e <= b) return;
   const size_t k = e - b;
   post(c, peer, send, c->Pm + b, k * 16);
+  post(c, peer, send, c->Lm + b, k * 16);
   post(c, peer, send, c->Um + b, k * 16);
   post(c, peer, send, c->S1m + b, k * 16);
   post(c, peer, send, c->S2m + b, k * 8);

@@ -118,6 +118,7 @@ __global__ void __launch_bounds__(BODY_BS) k_body_update(const int* __restrict__
                                                          const uint32_t* __restrict__ slot_of_id,
                                                          const float4* __restrict__ macc,
                                                          const float4* __restrict__ Pmid,
+                                                         const float4* __restrict__ Lmid,
                                                          BodyState* __restrict__ bodies, double dt, float g0,
                                                          float g1, float g2) {
   __shared__ double red[6][BODY_BS];
@@ -129,8 +130,9 @@ __global__ void __launch_bounds__(BODY_BS) k_body_update(const int* __restrict__
   for (uint32_t k = mstart[bi] + threadIdx.x; k < mstart[bi + 1]; k += BODY_BS) {
     const uint32_t s = slot_of_id[moving_ids[k]];
     const float4 f = macc[s];
-    const float4 x = Pmid[s];
-    const double r[3] = {(double)x.x - pm[0], (double)x.y - pm[1], (double)x.z - pm[2]};
+    const float4 x = Pmid[s], xl = Lmid[s];
+    const double r[3] = {(double)x.x + (double)xl.x - pm[0], (double)x.y + (double)xl.y - pm[1],
+                         (double)x.z + (double)xl.z - pm[2]};
     const double fx = f.x, fy = f.y, fz = f.z;
     acc[0] += fx; acc[1] += fy; acc[2] += fz;
     acc[3] += r[1] * fz - r[2] * fy;
@@ -167,9 +169,10 @@ __global__ void __launch_bounds__(BODY_BS) k_body_update(const int* __restrict__
 // ------------------------------------------------------------------------------------
 // state <-> fp64 id-order staging (crm_get_state / crm_set_state)
 __global__ void k_get_state(long long first, long long count, const uint32_t* __restrict__ slot_of_id,
-                            const float4* __restrict__ P, const float4* __restrict__ U,
-                            const float4* __restrict__ S1, const float2* __restrict__ S2, double* __restrict__ pos,
-                            double* __restrict__ vel, double* __restrict__ rho, double* __restrict__ sig) {
+                            const float4* __restrict__ P, const float4* __restrict__ L,
+                            const float4* __restrict__ U, const float4* __restrict__ S1,
+                            const float2* __restrict__ S2, double* __restrict__ pos, double* __restrict__ vel,
+                            double* __restrict__ rho, double* __restrict__ sig) {
   const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= count) return;
   const uint32_t s = slot_of_id[first + k];
@@ -177,7 +180,10 @@ __global__ void k_get_state(long long first, long long count, const uint32_t* __
   const float4 p = P[s], u = U[s], s1 = S1[s];
   if (tag_ghost(tag_of(u.w))) return;           // ghost copy: owned by a neighbour slab
   const float2 s2 = S2[s];
-  pos[3 * k] = p.x; pos[3 * k + 1] = p.y; pos[3 * k + 2] = p.z;
+  const float4 l = L[s];
+  pos[3 * k] = (double)p.x + (double)l.x;       // compensated position hi + lo
+  pos[3 * k + 1] = (double)p.y + (double)l.y;
+  pos[3 * k + 2] = (double)p.z + (double)l.z;
   vel[3 * k] = u.x; vel[3 * k + 1] = u.y; vel[3 * k + 2] = u.z;
   rho[k] = p.w;
   sig[6 * k] = s1.x; sig[6 * k + 1] = s1.y; sig[6 * k + 2] = s1.z;
@@ -185,17 +191,21 @@ __global__ void k_get_state(long long first, long long count, const uint32_t* __
 }
 
 __global__ void k_set_state(long long first, long long count, const uint32_t* __restrict__ slot_of_id,
-                            float4* __restrict__ P, float4* __restrict__ U, float4* __restrict__ S1,
-                            float2* __restrict__ S2, const double* __restrict__ pos, const double* __restrict__ vel,
-                            const double* __restrict__ rho, const double* __restrict__ sig, int has_pos, int has_vel,
-                            int has_rho, int has_sig) {
+                            float4* __restrict__ P, float4* __restrict__ L, float4* __restrict__ U,
+                            float4* __restrict__ S1, float2* __restrict__ S2, const double* __restrict__ pos,
+                            const double* __restrict__ vel, const double* __restrict__ rho,
+                            const double* __restrict__ sig, int has_pos, int has_vel, int has_rho, int has_sig) {
   const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= count) return;
   const uint32_t s = slot_of_id[first + k];
   if (s == 0xffffffffu) return;
   float4 p = P[s], u = U[s];
   if (tag_ghost(tag_of(u.w))) return;
-  if (has_pos) { p.x = (float)pos[3 * k]; p.y = (float)pos[3 * k + 1]; p.z = (float)pos[3 * k + 2]; }
+  if (has_pos) {   // hi = fp32 rounding of x (what rules B1/B2 see), lo = the remainder
+    p.x = (float)pos[3 * k]; p.y = (float)pos[3 * k + 1]; p.z = (float)pos[3 * k + 2];
+    L[s] = make_float4((float)(pos[3 * k] - (double)p.x), (float)(pos[3 * k + 1] - (double)p.y),
+                       (float)(pos[3 * k + 2] - (double)p.z), 0.f);
+  }
   if (has_rho && !tag_is_bce(tag_of(u.w))) p.w = (float)rho[k];
   if (has_vel) { u.x = (float)vel[3 * k]; u.y = (float)vel[3 * k + 1]; u.z = (float)vel[3 * k + 2]; }
   P[s] = p;

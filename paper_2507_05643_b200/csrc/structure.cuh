@@ -32,7 +32,7 @@ __device__ __forceinline__ bool b2_pred(float xi, float yi, float zi, float xj, 
 // moving markers: x = p + R x_local at the pose of the step start (body 0 never moves)
 __global__ void k_markers_place(int nm, const uint32_t* __restrict__ moving_ids,
                                 const float4* __restrict__ xlocal, const uint32_t* __restrict__ slot_of_id,
-                                const Pose* __restrict__ pose, float4* __restrict__ P,
+                                const Pose* __restrict__ pose, float4* __restrict__ P, float4* __restrict__ L,
                                 const float4* __restrict__ U) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= nm) return;
@@ -46,6 +46,7 @@ __global__ void k_markers_place(int nm, const uint32_t* __restrict__ moving_ids,
   p.y = q.pos[1] + q.R[3] * xl.x + q.R[4] * xl.y + q.R[5] * xl.z;
   p.z = q.pos[2] + q.R[6] * xl.x + q.R[7] * xl.y + q.R[8] * xl.z;
   P[s] = p;
+  L[s] = make_float4(0.f, 0.f, 0.f, 0.f);   // placed from the pose: no compensation term
 }
 
 // hash + per-cell count; the error latch reports particles outside the grid.
@@ -180,10 +181,11 @@ __global__ void k_scatter(int n, const uint32_t* __restrict__ key, const uint32_
 // final position = cellStart[c] + #(ids in the cell smaller than mine)  (B4, history-free)
 __global__ void k_reorder(int n, const uint32_t* __restrict__ tmp_src, const uint32_t* __restrict__ tmp_id,
                           const uint32_t* __restrict__ key, const uint32_t* __restrict__ cell_start,
-                          const float4* __restrict__ P, const float4* __restrict__ U,
-                          const float4* __restrict__ S1, const float2* __restrict__ S2,
-                          float4* __restrict__ Pn, float4* __restrict__ Un, float4* __restrict__ S1n,
-                          float2* __restrict__ S2n, uint32_t* __restrict__ ids_n, uint32_t* __restrict__ cell_of,
+                          const float4* __restrict__ P, const float4* __restrict__ L,
+                          const float4* __restrict__ U, const float4* __restrict__ S1,
+                          const float2* __restrict__ S2, float4* __restrict__ Pn, float4* __restrict__ Ln,
+                          float4* __restrict__ Un, float4* __restrict__ S1n, float2* __restrict__ S2n,
+                          uint32_t* __restrict__ ids_n, uint32_t* __restrict__ cell_of,
                           uint32_t* __restrict__ slot_of_id, uint32_t M) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n) return;
@@ -196,6 +198,7 @@ __global__ void k_reorder(int n, const uint32_t* __restrict__ tmp_src, const uin
   for (uint32_t t = b; t < e; ++t) rank += (tmp_id[t] < myid) ? 1u : 0u;
   const uint32_t d = b + rank;
   Pn[d] = P[i];
+  Ln[d] = L[i];
   Un[d] = U[i];
   S1n[d] = S1[i];
   S2n[d] = S2[i];

@@ -7,6 +7,8 @@
 //   k_bce_t<1>   markers: extrapolation at y_mid with the stored lists
 //   k_rates_t<1> fluid: pair loop at y_mid with the same lists (A17) + y_{n+1} = y_n + dt f
 //                + mu(I) return map; moving-body markers: loads (A13)
+// Each kernel: stage the window -> [filter on absolute fp32 positions (B2), rebuild steps only]
+// -> convert the window to tile-relative compensated positions -> pair loops -> epilogue.
 #pragma once
 #include "common.cuh"
 #include "physics.cuh"
@@ -16,35 +18,30 @@
 namespace crmk {
 
 // ---------------------------------------------------------------------------------------
+// neighbour state at window offset `off`; positions relative to the tile origin (see rel_pos)
 template <bool STAGED>
-__device__ __forceinline__ void load_pos(const TileSmem& sm, const float4* __restrict__ P, uint32_t off, float4& p) {
-  if (STAGED) p = sm.P[off];
-  else p = P[window_to_global(sm, off)];
-}
-
-template <bool STAGED>
-__device__ __forceinline__ void load_all(const TileSmem& sm, const float4* __restrict__ P, const float4* __restrict__ U,
-                                         const float4* __restrict__ S1, const float2* __restrict__ S2, uint32_t off,
-                                         float4& p, float4& u, float4& s1, float2& s2) {
+__device__ __forceinline__ void load_all(const TileSmem& sm, const float4* __restrict__ P, const float4* __restrict__ L,
+                                         const float4* __restrict__ U, const float4* __restrict__ S1,
+                                         const float2* __restrict__ S2, uint32_t off, float4& p, float4& u, float4& s1,
+                                         float2& s2) {
   if (STAGED) {
     p = sm.P[off]; u = sm.U[off]; s1 = sm.S1[off]; s2 = sm.S2[off];
   } else {
     const uint32_t g = window_to_global(sm, off);
-    p = P[g]; u = U[g]; s1 = S1[g]; s2 = S2[g];
+    p = rel_pos(P[g], L[g], sm); u = U[g]; s1 = S1[g]; s2 = S2[g];
   }
 }
 
 // Alg. 1 filter for particle i (window offset self) over its 9 candidate runs; stores window
 // offsets (all neighbours if store_bce, else fluid ones only); returns |P(i)|.  The candidate
 // order (runs in (da, db) order, offsets ascending) fixes the list order, hence the summation
-// order of the pair loops (deterministic).
+// order of the pair loops (deterministic).  Works on the absolute fp32 positions (rule B2).
 template <bool STAGED, bool STORE_BCE>
 __device__ __forceinline__ void filter_range(const Grid& g, const TileSmem& sm, const float4* __restrict__ P,
                                              const float4* __restrict__ U, uint32_t ob, uint32_t oe, uint32_t gshift,
-                                             const float4& pi, uint32_t self, uint32_t& cnt, ListWriter& w) {
+                                             const float4& pi, uint32_t& cnt, ListWriter& w) {
   // chunks of 32 candidates: a branch-free predicate sweep builds a bitmask (and, for marker
   // lists, a mask of the fluid candidates), then the set bits are appended in ascending order
-  // two at a time (an odd last one is paired with `self`, a zero-weight entry)
   for (uint32_t base = ob; base < oe; base += 32) {
     const uint32_t nc = min(32u, oe - base);
     uint32_t m = 0, mf = 0;
@@ -67,10 +64,10 @@ __device__ __forceinline__ void filter_range(const Grid& g, const TileSmem& sm, 
   }
 }
 
-template <bool STAGED>
+template <bool STAGED, bool STORE_BCE>
 __device__ __forceinline__ uint32_t filter(const Grid& g, const TileSmem& sm, const float4* __restrict__ P,
                                            const float4* __restrict__ U, int q, int cz, uint32_t self, float4 pi,
-                                           bool store_bce, ListWriter& w) {
+                                           ListWriter& w) {
   // (measured: pruning neighbour cells by their box distance removes ~24 % of the candidates
   //  but costs more in divergence than it saves; the full 27-cell stencil is kept)
   uint32_t cnt = 0;
@@ -82,34 +79,49 @@ __device__ __forceinline__ uint32_t filter(const Grid& g, const TileSmem& sm, co
       int r;
       cand_range(sm, q, da, db, cz, ob, oe, r);
       const uint32_t gshift = sm.run_start[r] - sm.run_base[r];
-      if (store_bce) {
-        if (da == 0 && db == 0) {   // the own run holds i itself (j != i, A18)
-          filter_range<STAGED, true>(g, sm, P, U, ob, self, gshift, pi, self, cnt, w);
-          filter_range<STAGED, true>(g, sm, P, U, self + 1, oe, gshift, pi, self, cnt, w);
-        } else {
-          filter_range<STAGED, true>(g, sm, P, U, ob, oe, gshift, pi, self, cnt, w);
-        }
+      if (da == 0 && db == 0) {   // the own run holds i itself (j != i, A18)
+        filter_range<STAGED, STORE_BCE>(g, sm, P, U, ob, self, gshift, pi, cnt, w);
+        filter_range<STAGED, STORE_BCE>(g, sm, P, U, self + 1, oe, gshift, pi, cnt, w);
       } else {
-        if (da == 0 && db == 0) {
-          filter_range<STAGED, false>(g, sm, P, U, ob, self, gshift, pi, self, cnt, w);
-          filter_range<STAGED, false>(g, sm, P, U, self + 1, oe, gshift, pi, self, cnt, w);
-        } else {
-          filter_range<STAGED, false>(g, sm, P, U, ob, oe, gshift, pi, self, cnt, w);
-        }
+        filter_range<STAGED, STORE_BCE>(g, sm, P, U, ob, oe, gshift, pi, cnt, w);
       }
     }
   }
   return cnt;
 }
 
+// rebuild step: build and store the lists of the tile's particles that pass `want`
+template <bool STAGED, bool STORE_BCE, typename Want>
+__device__ __forceinline__ void build_lists(const Grid& g, const TileSmem& sm, const float4* __restrict__ P,
+                                            const float4* __restrict__ U, uint16_t* __restrict__ list,
+                                            uint32_t* __restrict__ nlist, uint32_t* __restrict__ count_all,
+                                            const uint32_t* __restrict__ cell_of, int cap, ErrLatch* err,
+                                            const uint32_t* __restrict__ ids, long long step, Want want) {
+  const uint32_t n_i = sm.col_pref[NCOL];
+  for (uint32_t t = threadIdx.x; t < n_i; t += blockDim.x) {
+    int q;
+    const uint32_t i = tile_particle(sm, t, q);
+    if (!want(tag_of(U[i].w))) continue;
+    const int r_self = (1 + q / TY) * WRY + (1 + q % TY);
+    const uint32_t self = sm.run_base[r_self] + (i - sm.run_start[r_self]);
+    const int cz = (int)(cell_of[i] % (uint32_t)g.dims[2]);
+    ListWriter w;
+    w.init(list, i, cap);
+    const uint32_t cnt = filter<STAGED, STORE_BCE>(g, sm, P, U, q, cz, self, P[i], w);
+    w.flush(self);
+    nlist[i] = (uint32_t)min(w.k, cap);
+    count_all[i] = cnt;
+    if (w.k > cap) latch_error(err, -9 /*CRM_E_CAPACITY*/, (long long)ids[i], step, (long long)w.k);
+  }
+}
+
 // ---------------------------------------------------------------------------------------
 template <int STAGE, bool STAGED>
-__device__ __forceinline__ void bce_tile(const Grid& g, const Phys& ph, TileSmem& sm, const float4* __restrict__ P,
-                                         float4* __restrict__ U, float4* __restrict__ S1, float2* __restrict__ S2,
-                                         uint16_t* __restrict__ list, uint32_t* __restrict__ nlist,
-                                         uint32_t* __restrict__ count_all, const uint32_t* __restrict__ cell_of,
-                                         const Pose* __restrict__ pose, int cap, int store_all, Debug dbg, int dbg_on,
-                                         ErrLatch* err, const uint32_t* __restrict__ ids, long long step) {
+__device__ __forceinline__ void bce_tile(const Phys& ph, TileSmem& sm, const float4* __restrict__ P,
+                                         const float4* __restrict__ L, float4* __restrict__ U, float4* __restrict__ S1,
+                                         float2* __restrict__ S2, const uint16_t* __restrict__ list,
+                                         const uint32_t* __restrict__ nlist, const Pose* __restrict__ pose, int cap,
+                                         Debug dbg, int dbg_on) {
   const uint32_t n_i = sm.col_pref[NCOL];
   for (uint32_t t = threadIdx.x; t < n_i; t += blockDim.x) {
     int q;
@@ -117,25 +129,11 @@ __device__ __forceinline__ void bce_tile(const Grid& g, const Phys& ph, TileSmem
     const float4 ui = U[i];
     const uint32_t tag = tag_of(ui.w);
     if (!tag_is_bce(tag)) continue;
-    const float4 pa = P[i];
-    uint32_t nl;
-    if (STAGE == 0 && ph.build_lists) {   // Alg. 2: rebuild at t mod ps_freq == 0, else reuse
-      const int r_self = (1 + q / TY) * WRY + (1 + q % TY);
-      const uint32_t self = sm.run_base[r_self] + (i - sm.run_start[r_self]);
-      const int cz = (int)(cell_of[i] % (uint32_t)g.dims[2]);
-      ListWriter w;
-      w.init(list, i, cap);
-      const uint32_t cnt = filter<STAGED>(g, sm, P, U, q, cz, self, pa, store_all != 0, w);
-      w.flush(self);
-      nl = (uint32_t)min(w.k, cap);
-      nlist[i] = nl;
-      count_all[i] = cnt;
-      if (w.k > cap) latch_error(err, -9 /*CRM_E_CAPACITY*/, (long long)ids[i], step, (long long)w.k);
-    } else {
-      nl = nlist[i];
-    }
+    const float4 pabs = P[i];
+    const float4 pa = rel_pos(pabs, L[i], sm);
+    const uint32_t nl = nlist[i];
     float ub[3] = {0.f, 0.f, 0.f}, ab[3] = {0.f, 0.f, 0.f};
-    if (tag_moving(tag)) body_kinematics(pose[tag_body(tag)], pa.x, pa.y, pa.z, ub, ab);
+    if (tag_moving(tag)) body_kinematics(pose[tag_body(tag)], pabs.x, pabs.y, pabs.z, ub, ab);
     const float ga[3] = {ph.g[0] - ab[0], ph.g[1] - ab[1], ph.g[2] - ab[2]};
     float SW = 0.f, su[3] = {0.f, 0.f, 0.f}, ss[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, sh = 0.f;
     const uint4* seg = reinterpret_cast<const uint4*>(list + (size_t)i * cap);
@@ -147,15 +145,16 @@ __device__ __forceinline__ void bce_tile(const Grid& g, const Phys& ph, TileSmem
         const uint32_t off = list_entry(v, e);
         float4 pf, uf, s1;
         float2 s2;
-        load_all<STAGED>(sm, P, U, S1, S2, off, pf, uf, s1, s2);
+        load_all<STAGED>(sm, P, L, U, S1, S2, off, pf, uf, s1, s2);
         const float dx = pa.x - pf.x, dy = pa.y - pf.y, dz = pa.z - pf.z;
         const float r2 = dx * dx + dy * dy + dz * dz;
         // fluid neighbours only; W = 0 beyond the support (A17)
         const bool ok = !tag_is_bce(tag_of(uf.w)) && r2 < ph.R2;
         const float r = (r2 > 0.f) ? r2 * rsqrt_approx(r2) : 0.f;
-        const float q = r * ph.hinv;
-        const float t = 2.0f - q;
-        const float Wv = q < 1.0f ? ph.wnorm * (1.0f - 1.5f * q * q + 0.75f * q * q * q) : ph.wnorm * 0.25f * t * t * t;
+        const float qq = r * ph.hinv;
+        const float tt = 2.0f - qq;
+        const float Wv = qq < 1.0f ? ph.wnorm * (1.0f - 1.5f * qq * qq + 0.75f * qq * qq * qq)
+                                   : ph.wnorm * 0.25f * tt * tt * tt;
         const float W = ok ? Wv : 0.f;
         SW += W;
         su[0] += uf.x * W; su[1] += uf.y * W; su[2] += uf.z * W;
@@ -189,12 +188,12 @@ __device__ __forceinline__ void bce_tile(const Grid& g, const Phys& ph, TileSmem
 }
 
 template <int STAGE>
-__global__ void __launch_bounds__(TILE_THREADS, 2)
+__global__ void TILE_BOUNDS
     k_bce_t(Grid g, Phys ph, const uint32_t* __restrict__ cell_start, const float4* __restrict__ P,
-            float4* __restrict__ U, float4* __restrict__ S1, float2* __restrict__ S2, uint16_t* __restrict__ list,
-            uint32_t* __restrict__ nlist, uint32_t* __restrict__ count_all, const uint32_t* __restrict__ cell_of,
-            const Pose* __restrict__ pose, int cap, int store_all, Debug dbg, int dbg_on, ErrLatch* err,
-            const uint32_t* __restrict__ ids, long long step, long long tile_base) {
+            const float4* __restrict__ L, float4* __restrict__ U, float4* __restrict__ S1, float2* __restrict__ S2,
+            uint16_t* __restrict__ list, uint32_t* __restrict__ nlist, uint32_t* __restrict__ count_all,
+            const uint32_t* __restrict__ cell_of, const Pose* __restrict__ pose, int cap, int store_all, Debug dbg,
+            int dbg_on, ErrLatch* err, const uint32_t* __restrict__ ids, long long step, long long tile_base) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
   const TileGeom G = tile_geom(g, tile_base + (long long)blockIdx.x);
@@ -214,12 +213,21 @@ __global__ void __launch_bounds__(TILE_THREADS, 2)
   tile_stage(P, U, S1, S2, sm);
   tile_stage_wait();
   __syncthreads();
-  if (sm.staged)
-    bce_tile<STAGE, true>(g, ph, sm, P, U, S1, S2, list, nlist, count_all, cell_of, pose, cap, store_all, dbg,
-                          dbg_on, err, ids, step);
-  else
-    bce_tile<STAGE, false>(g, ph, sm, P, U, S1, S2, list, nlist, count_all, cell_of, pose, cap, store_all, dbg,
-                           dbg_on, err, ids, step);
+  if (STAGE == 0 && ph.build_lists) {   // Alg. 2: rebuild at t mod ps_freq == 0, else reuse
+    auto is_marker = [](uint32_t t) { return tag_is_bce(t); };
+    if (sm.staged) {
+      if (store_all) build_lists<true, true>(g, sm, P, U, list, nlist, count_all, cell_of, cap, err, ids, step, is_marker);
+      else build_lists<true, false>(g, sm, P, U, list, nlist, count_all, cell_of, cap, err, ids, step, is_marker);
+    } else {
+      if (store_all) build_lists<false, true>(g, sm, P, U, list, nlist, count_all, cell_of, cap, err, ids, step, is_marker);
+      else build_lists<false, false>(g, sm, P, U, list, nlist, count_all, cell_of, cap, err, ids, step, is_marker);
+    }
+    __syncthreads();
+  }
+  tile_relativize(L, sm);
+  __syncthreads();
+  if (sm.staged) bce_tile<STAGE, true>(ph, sm, P, L, U, S1, S2, list, nlist, pose, cap, dbg, dbg_on);
+  else bce_tile<STAGE, false>(ph, sm, P, L, U, S1, S2, list, nlist, pose, cap, dbg, dbg_on);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -264,10 +272,10 @@ __device__ __forceinline__ void pair_terms(PairAcc& A, const Phys& ph, const flo
 
 template <bool STAGED>
 __device__ __forceinline__ void pair_loop(PairAcc& A, const Phys& ph, const TileSmem& sm, const float4* __restrict__ P,
-                                          const float4* __restrict__ U, const float4* __restrict__ S1,
-                                          const float2* __restrict__ S2, const uint16_t* __restrict__ list,
-                                          uint32_t i, int cap, uint32_t nl, const float4& pi, const float4& ui,
-                                          bool with_L, bool fluid_only) {
+                                          const float4* __restrict__ L, const float4* __restrict__ U,
+                                          const float4* __restrict__ S1, const float2* __restrict__ S2,
+                                          const uint16_t* __restrict__ list, uint32_t i, int cap, uint32_t nl,
+                                          const float4& pi, const float4& ui, bool with_L, bool fluid_only) {
   const uint4* seg = reinterpret_cast<const uint4*>(list + (size_t)i * cap);
   for (uint32_t c = 0; c < ((nl + 7) >> 3); ++c) {   // whole padded chunks of 8, branch-free
     const uint4 v = seg[c];
@@ -275,22 +283,28 @@ __device__ __forceinline__ void pair_loop(PairAcc& A, const Phys& ph, const Tile
     for (int e = 0; e < 8; ++e) {
       float4 pj, uj, s1;
       float2 s2;
-      load_all<STAGED>(sm, P, U, S1, S2, list_entry(v, e), pj, uj, s1, s2);
+#ifdef CRM_EXP_NOCONFLICT   // timing experiment only (wrong neighbours): bank-conflict-free gathers
+      const uint32_t off = (list_entry(v, e) & ~7u) | ((threadIdx.x + 8 * c + e) & 7u);
+#else
+      const uint32_t off = list_entry(v, e);
+#endif
+      load_all<STAGED>(sm, P, L, U, S1, S2, off, pj, uj, s1, s2);
       pair_terms(A, ph, pi, ui, pj, uj, s1, s2, with_L, !(fluid_only && tag_is_bce(tag_of(uj.w))));
     }
   }
 }
 
+// STAGE 0: (P,L,U,S) = y_n; writes y_mid to (YP,YL,YU,YS).  STAGE 1: (P,L,U,S) = y_mid;
+// (YP,YL,YU,YS) = y_n in, y_{n+1} out (own slot only; neighbours are read from y_mid).
 template <int STAGE, bool STAGED>
-__device__ __forceinline__ void rates_tile(const Grid& g, const Phys& ph, float dt, TileSmem& sm,
-                                           const float4* __restrict__ P, const float4* __restrict__ U,
+__device__ __forceinline__ void rates_tile(const Phys& ph, float dt, TileSmem& sm, const float4* __restrict__ P,
+                                           const float4* __restrict__ L, const float4* __restrict__ U,
                                            const float4* __restrict__ S1, const float2* __restrict__ S2,
-                                           float4* __restrict__ YP, float4* __restrict__ YU, float4* __restrict__ YS1,
-                                           float2* __restrict__ YS2, uint16_t* __restrict__ list,
-                                           uint32_t* __restrict__ nlist, uint32_t* __restrict__ count_all,
-                                           const uint32_t* __restrict__ cell_of, int cap, float4* __restrict__ macc,
-                                           Debug dbg, int dbg_on, ErrLatch* err, const uint32_t* __restrict__ ids,
-                                           long long step) {
+                                           float4* __restrict__ YP, float4* __restrict__ YL, float4* __restrict__ YU,
+                                           float4* __restrict__ YS1, float2* __restrict__ YS2,
+                                           const uint16_t* __restrict__ list, const uint32_t* __restrict__ nlist,
+                                           int cap, float4* __restrict__ macc, Debug dbg, int dbg_on, ErrLatch* err,
+                                           const uint32_t* __restrict__ ids, long long step) {
   const uint32_t n_i = sm.col_pref[NCOL];
   for (uint32_t t = threadIdx.x; t < n_i; t += blockDim.x) {
     int q;
@@ -299,32 +313,17 @@ __device__ __forceinline__ void rates_tile(const Grid& g, const Phys& ph, float 
     const uint32_t tag = tag_of(ui.w);
     const bool bce = tag_is_bce(tag);
     if (bce && !(STAGE == 1 && tag_moving(tag))) continue;
-    const float4 pi = P[i];
-    uint32_t nl;
-    if (STAGE == 0 && ph.build_lists) {   // Alg. 2: rebuild at t mod ps_freq == 0, else reuse
-      const int r_self = (1 + q / TY) * WRY + (1 + q % TY);
-      const uint32_t self = sm.run_base[r_self] + (i - sm.run_start[r_self]);
-      const int cz = (int)(cell_of[i] % (uint32_t)g.dims[2]);
-      ListWriter w;
-      w.init(list, i, cap);
-      const uint32_t cnt = filter<STAGED>(g, sm, P, U, q, cz, self, pi, true, w);
-      w.flush(self);
-      nl = (uint32_t)min(w.k, cap);
-      nlist[i] = nl;
-      count_all[i] = cnt;
-      if (w.k > cap) latch_error(err, -9 /*CRM_E_CAPACITY*/, (long long)ids[i], step, (long long)w.k);
-    } else {
-      nl = nlist[i];
-    }
+    const float4 pi = rel_pos(P[i], L[i], sm);
+    const uint32_t nl = nlist[i];
     PairAcc A;
 #pragma unroll
     for (int k = 0; k < 9; ++k) A.L[k] = 0.f;
 #pragma unroll
     for (int k = 0; k < 3; ++k) { A.Gs[k] = 0.f; A.Ms[k] = 0.f; A.Pi[k] = 0.f; }
-    const float4 si1 = S1[i];
-    const float2 si2 = S2[i];
     if (bce) {   // STAGE 1, moving-body marker: m a_s over fluid neighbours, no gravity (A13)
-      pair_loop<STAGED>(A, ph, sm, P, U, S1, S2, list, i, cap, nl, pi, ui, false, true);
+      pair_loop<STAGED>(A, ph, sm, P, L, U, S1, S2, list, i, cap, nl, pi, ui, false, true);
+      const float4 si1 = S1[i];
+      const float2 si2 = S2[i];
       const float rinv_i = 1.0f / pi.w;
       float a[3];
       a[0] = (si1.x * A.Gs[0] + si1.w * A.Gs[1] + si2.x * A.Gs[2] + A.Ms[0]) * rinv_i + A.Pi[0];
@@ -334,7 +333,12 @@ __device__ __forceinline__ void rates_tile(const Grid& g, const Phys& ph, float 
       if (dbg_on) dbg.acc[1][i] = make_float4(a[0], a[1], a[2], 0.f);
       continue;
     }
-    pair_loop<STAGED>(A, ph, sm, P, U, S1, S2, list, i, cap, nl, pi, ui, true, false);
+    pair_loop<STAGED>(A, ph, sm, P, L, U, S1, S2, list, i, cap, nl, pi, ui, true, false);
+    // own state for the epilogue, (re)loaded after the loop to keep registers free inside it
+    const float4 phi = P[i];
+    const float4 pli = L[i];
+    const float4 si1 = S1[i];
+    const float2 si2 = S2[i];
     const float rinv_i = 1.0f / pi.w;
     float a[3];
     a[0] = (si1.x * A.Gs[0] + si1.w * A.Gs[1] + si2.x * A.Gs[2] + A.Ms[0]) * rinv_i + A.Pi[0] + ph.g[0];
@@ -373,12 +377,18 @@ __device__ __forceinline__ void rates_tile(const Grid& g, const Phys& ph, float 
     }
     if (STAGE == 0) {
       const float hd = 0.5f * dt;
-      YP[i] = make_float4(pi.x + hd * ui.x, pi.y + hd * ui.y, pi.z + hd * ui.z, pi.w + hd * drho);
+      float hx = phi.x, hy = phi.y, hz = phi.z, lx = pli.x, ly = pli.y, lz = pli.z;
+      comp_add(hx, lx, hd * ui.x);   // x_mid = x_n + dt/2 u_n, compensated
+      comp_add(hy, ly, hd * ui.y);
+      comp_add(hz, lz, hd * ui.z);
+      YP[i] = make_float4(hx, hy, hz, phi.w + hd * drho);
+      YL[i] = make_float4(lx, ly, lz, 0.f);
       YU[i] = make_float4(ui.x + hd * a[0], ui.y + hd * a[1], ui.z + hd * a[2], ui.w);
       YS1[i] = make_float4(si1.x + hd * ds[0], si1.y + hd * ds[1], si1.z + hd * ds[2], si1.w + hd * ds[3]);
       YS2[i] = make_float2(si2.x + hd * ds[4], si2.y + hd * ds[5]);
     } else {
       const float4 p0 = YP[i];
+      const float4 l0 = YL[i];
       const float4 u0 = YU[i];
       const float4 s01 = YS1[i];
       const float2 s02 = YS2[i];
@@ -386,9 +396,14 @@ __device__ __forceinline__ void rates_tile(const Grid& g, const Phys& ph, float 
       float s[6] = {s01.x + dt * ds[0], s01.y + dt * ds[1], s01.z + dt * ds[2],
                     s01.w + dt * ds[3], s02.x + dt * ds[4], s02.y + dt * ds[5]};
       return_map(s, sn, ph, dt);
-      const float4 pn = make_float4(p0.x + dt * ui.x, p0.y + dt * ui.y, p0.z + dt * ui.z, p0.w + dt * drho);
+      float hx = p0.x, hy = p0.y, hz = p0.z, lx = l0.x, ly = l0.y, lz = l0.z;
+      comp_add(hx, lx, dt * ui.x);   // x_{n+1} = x_n + dt u_mid, compensated
+      comp_add(hy, ly, dt * ui.y);
+      comp_add(hz, lz, dt * ui.z);
+      const float4 pn = make_float4(hx, hy, hz, p0.w + dt * drho);
       const float4 un = make_float4(u0.x + dt * a[0], u0.y + dt * a[1], u0.z + dt * a[2], u0.w);
       YP[i] = pn;
+      YL[i] = make_float4(lx, ly, lz, 0.f);
       YU[i] = un;
       YS1[i] = make_float4(s[0], s[1], s[2], s[3]);
       YS2[i] = make_float2(s[4], s[5]);
@@ -398,15 +413,15 @@ __device__ __forceinline__ void rates_tile(const Grid& g, const Phys& ph, float 
   }
 }
 
-// STAGE 0: (P,U,S) = y_n, (YP..) = mid (out).  STAGE 1: (P,U,S) = y_mid, (YP..) = y_n in / y_{n+1} out.
 template <int STAGE>
-__global__ void __launch_bounds__(TILE_THREADS, 2)
+__global__ void TILE_BOUNDS
     k_rates_t(Grid g, Phys ph, float dt, const uint32_t* __restrict__ cell_start, const float4* __restrict__ P,
-              const float4* __restrict__ U, const float4* __restrict__ S1, const float2* __restrict__ S2,
-              float4* __restrict__ YP, float4* __restrict__ YU, float4* __restrict__ YS1, float2* __restrict__ YS2,
-              uint16_t* __restrict__ list, uint32_t* __restrict__ nlist, uint32_t* __restrict__ count_all,
-              const uint32_t* __restrict__ cell_of, int cap, float4* __restrict__ macc, Debug dbg, int dbg_on,
-              ErrLatch* err, const uint32_t* __restrict__ ids, long long step, long long tile_base) {
+              const float4* __restrict__ L, const float4* __restrict__ U, const float4* __restrict__ S1,
+              const float2* __restrict__ S2, float4* __restrict__ YP, float4* __restrict__ YL, float4* __restrict__ YU,
+              float4* __restrict__ YS1, float2* __restrict__ YS2, uint16_t* __restrict__ list,
+              uint32_t* __restrict__ nlist, uint32_t* __restrict__ count_all, const uint32_t* __restrict__ cell_of,
+              int cap, float4* __restrict__ macc, Debug dbg, int dbg_on, ErrLatch* err,
+              const uint32_t* __restrict__ ids, long long step, long long tile_base) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
   const TileGeom G = tile_geom(g, tile_base + (long long)blockIdx.x);
@@ -424,6 +439,7 @@ __global__ void __launch_bounds__(TILE_THREADS, 2)
       work = 1;
     } else if (STAGE == 0) {
       YP[i] = P[i];     // markers: x at t_n (moving ones are re-placed at t_n + dt/2 afterwards)
+      YL[i] = L[i];
       YU[i] = ui;       // tag; u and sigma are replaced by the stage-B extrapolation
     } else {
       YU[i] = ui;       // y_{n+1} of a marker: its stage-B extrapolated u and sigma
@@ -440,16 +456,25 @@ __global__ void __launch_bounds__(TILE_THREADS, 2)
   tile_stage(P, U, S1, S2, sm);
   tile_stage_wait();
   __syncthreads();
+  if (STAGE == 0 && ph.build_lists) {   // Alg. 2: rebuild at t mod ps_freq == 0, else reuse
+    auto is_fluid = [](uint32_t t) { return !tag_is_bce(t); };
+    if (sm.staged) build_lists<true, true>(g, sm, P, U, list, nlist, count_all, cell_of, cap, err, ids, step, is_fluid);
+    else build_lists<false, true>(g, sm, P, U, list, nlist, count_all, cell_of, cap, err, ids, step, is_fluid);
+    __syncthreads();
+  }
+  tile_relativize(L, sm);
+  __syncthreads();
   if (sm.staged)
-    rates_tile<STAGE, true>(g, ph, dt, sm, P, U, S1, S2, YP, YU, YS1, YS2, list, nlist, count_all, cell_of, cap, macc,
-                            dbg, dbg_on, err, ids, step);
+    rates_tile<STAGE, true>(ph, dt, sm, P, L, U, S1, S2, YP, YL, YU, YS1, YS2, list, nlist, cap, macc, dbg, dbg_on,
+                            err, ids, step);
   else
-    rates_tile<STAGE, false>(g, ph, dt, sm, P, U, S1, S2, YP, YU, YS1, YS2, list, nlist, count_all, cell_of, cap, macc,
-                             dbg, dbg_on, err, ids, step);
+    rates_tile<STAGE, false>(ph, dt, sm, P, L, U, S1, S2, YP, YL, YU, YS1, YS2, list, nlist, cap, macc, dbg, dbg_on,
+                             err, ids, step);
 }
 
 // ---------------------------------------------------------------------------------------
-// debug: hot-path lists (window offsets) -> global sorted indices, ELL k-major u32
+// debug: hot-path lists (window offsets) -> global sorted indices, ELL k-major u32; the
+// zero-weight self padding is dropped and the remaining count written to nout
 __global__ void k_decode_lists(int n, Grid g, const uint32_t* __restrict__ cell_start,
                                const uint32_t* __restrict__ cell_of, const uint16_t* __restrict__ list,
                                const uint32_t* __restrict__ nlist, int cap, uint32_t* __restrict__ out,

@@ -20,6 +20,9 @@ constexpr int TX = 2, TY = 2, TZ = 4;
 constexpr int WRX = TX + 2, WRY = TY + 2, WR = WRX * WRY;   // 16 window runs
 constexpr int NCOL = TX * TY;                               // i columns per tile
 constexpr int TILE_THREADS = 288;
+// 2 CTAs of 288 threads per SM (ptxas caps at 96 registers; measured: __maxnreg__(112) removes the
+// small spills but drops residency to 1 CTA/SM, 1.5x slower)
+#define TILE_BOUNDS __launch_bounds__(TILE_THREADS, 2)
 constexpr int WMAX = 1920;                                  // staged window capacity (particles)
 
 struct TileSmem {
@@ -34,6 +37,7 @@ struct TileSmem {
   uint32_t col_pref[NCOL + 1];  // prefix of i counts
   int zlo, zhi, staged, any;
   int X0, Y0;
+  float ox, oy, oz;             // tile origin: pair loops use positions relative to it
 };
 
 struct TileGeom {
@@ -97,6 +101,9 @@ __device__ __forceinline__ void tile_setup(const Grid& g, const TileGeom& G, con
     sm.zhi = G.zhi;
     sm.X0 = G.X0;
     sm.Y0 = G.Y0;
+    sm.ox = g.lo[0] + (float)G.X0 * g.s;
+    sm.oy = g.lo[1] + (float)G.Y0 * g.s;
+    sm.oz = g.lo[2] + (float)G.z0 * g.s;
     sm.staged = acc <= (uint32_t)WMAX;
     sm.any = 0;
   }
@@ -124,6 +131,34 @@ __device__ __forceinline__ void tile_stage(const float4* __restrict__ P, const f
 }
 
 __device__ __forceinline__ void tile_stage_wait() { __pipeline_wait_prior(0); }
+
+// Positions are stored compensated, x = hi + lo (hi: the fp32 value the structural rules B1/B2
+// use; lo: the rounding remainder kept by the integrator).  The pair loops work in coordinates
+// relative to the tile origin, (hi - o) + lo, which keeps ~1e-9 m resolution on metre-scale beds.
+__device__ __forceinline__ float4 rel_pos(const float4& hi, const float4& lo, const TileSmem& sm) {
+  return make_float4((hi.x - sm.ox) + lo.x, (hi.y - sm.oy) + lo.y, (hi.z - sm.oz) + lo.z, hi.w);
+}
+
+// convert the staged window from absolute hi to relative compensated positions (after the filter)
+__device__ __forceinline__ void tile_relativize(const float4* __restrict__ L, TileSmem& sm) {
+  if (!sm.staged) return;
+  const uint32_t W = sm.run_base[WR];
+  for (uint32_t idx = threadIdx.x; idx < W; idx += blockDim.x) {
+    int r = 0;
+#pragma unroll
+    for (int k = 1; k < WR; ++k) r += (sm.run_base[k] <= idx) ? 1 : 0;
+    const uint32_t gidx = sm.run_start[r] + (idx - sm.run_base[r]);
+    sm.P[idx] = rel_pos(sm.P[idx], L[gidx], sm);
+  }
+}
+
+// compensated update (hi, lo) += d  (Fast2Sum; |hi| >= |lo + d| for any step an SPH particle takes)
+__device__ __forceinline__ void comp_add(float& hi, float& lo, float d) {
+  const float y = lo + d;
+  const float t = hi + y;
+  lo = y - (t - hi);
+  hi = t;
+}
 
 // global index of a window offset (global mode)
 __device__ __forceinline__ uint32_t window_to_global(const TileSmem& sm, uint32_t off) {
