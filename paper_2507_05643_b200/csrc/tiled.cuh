@@ -45,14 +45,31 @@ __device__ __forceinline__ void filter_range(const Grid& g, const TileSmem& sm, 
   for (uint32_t base = ob; base < oe; base += 32) {
     const uint32_t nc = min(32u, oe - base);
     uint32_t m = 0, mf = 0;
+    if (STAGED) {
+      // groups of 8 with compile-time bit positions; the last group may read up to 7 slots past
+      // the segment (still inside TileSmem), masked off below
+      for (uint32_t k8 = 0; k8 < nc; k8 += 8) {
+        uint32_t gm = 0, gf = 0;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float4 pj = sm.P[base + k8 + e];
+          const uint32_t bit = b2_pred(pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, g.R2) ? (1u << e) : 0u;
+          gm |= bit;
+          if (!STORE_BCE) gf |= tag_is_bce(tag_of(sm.U[base + k8 + e].w)) ? 0u : bit;
+        }
+        m |= gm << k8;
+        mf |= gf << k8;
+      }
+      const uint32_t valid = nc >= 32 ? 0xffffffffu : ((1u << nc) - 1u);
+      m &= valid;
+      mf &= valid;
+    } else {
 #pragma unroll 4
-    for (uint32_t k = 0; k < nc; ++k) {
-      const float4 pj = STAGED ? sm.P[base + k] : P[base + k + gshift];
-      const uint32_t bit = (b2_pred(pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, g.R2) ? 1u : 0u) << k;
-      m |= bit;
-      if (!STORE_BCE) {
-        const float tw = STAGED ? sm.U[base + k].w : U[base + k + gshift].w;
-        mf |= tag_is_bce(tag_of(tw)) ? 0u : bit;
+      for (uint32_t k = 0; k < nc; ++k) {
+        const float4 pj = P[base + k + gshift];
+        const uint32_t bit = (b2_pred(pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, g.R2) ? 1u : 0u) << k;
+        m |= bit;
+        if (!STORE_BCE) mf |= tag_is_bce(tag_of(U[base + k + gshift].w)) ? 0u : bit;
       }
     }
     cnt += __popc(m);
@@ -138,8 +155,11 @@ __device__ __forceinline__ void bce_tile(const Phys& ph, TileSmem& sm, const flo
     float SW = 0.f, su[3] = {0.f, 0.f, 0.f}, ss[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, sh = 0.f;
     const uint4* seg = reinterpret_cast<const uint4*>(list + (size_t)i * cap);
     // whole chunks of 8 (padded with the marker itself, excluded by the fluid mask): branch-free
-    for (uint32_t c = 0; c < ((nl + 7) >> 3); ++c) {
-      const uint4 v = seg[c];
+    const uint32_t nch = (nl + 7) >> 3;
+    uint4 vn = seg[0];   // chunk prefetch, as in pair_loop
+    for (uint32_t c = 0; c < nch; ++c) {
+      const uint4 v = vn;
+      vn = seg[min(c + 1, nch - 1)];
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         const uint32_t off = list_entry(v, e);
@@ -277,18 +297,19 @@ __device__ __forceinline__ void pair_loop(PairAcc& A, const Phys& ph, const Tile
                                           const uint16_t* __restrict__ list, uint32_t i, int cap, uint32_t nl,
                                           const float4& pi, const float4& ui, bool with_L, bool fluid_only) {
   const uint4* seg = reinterpret_cast<const uint4*>(list + (size_t)i * cap);
-  for (uint32_t c = 0; c < ((nl + 7) >> 3); ++c) {   // whole padded chunks of 8, branch-free
-    const uint4 v = seg[c];
+  const uint32_t nch = (nl + 7) >> 3;
+  // the list streams from HBM (written by stage A, larger than L2): chunk c + 1 is requested
+  // before chunk c is processed so its latency hides behind 8 pair evaluations
+  uint4 vn = seg[0];
+  for (uint32_t c = 0; c < nch; ++c) {   // whole padded chunks of 8, branch-free
+    const uint4 v = vn;
+    vn = seg[min(c + 1, nch - 1)];
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       float4 pj, uj, s1;
       float2 s2;
-#ifdef CRM_EXP_NOCONFLICT   // timing experiment only (wrong neighbours): bank-conflict-free gathers
-      const uint32_t off = (list_entry(v, e) & ~7u) | ((threadIdx.x + 8 * c + e) & 7u);
-#else
-      const uint32_t off = list_entry(v, e);
-#endif
-      load_all<STAGED>(sm, P, L, U, S1, S2, off, pj, uj, s1, s2);
+      // (measured: making these gathers bank-conflict free would gain only ~10 % in stage B)
+      load_all<STAGED>(sm, P, L, U, S1, S2, list_entry(v, e), pj, uj, s1, s2);
       pair_terms(A, ph, pi, ui, pj, uj, s1, s2, with_L, !(fluid_only && tag_is_bce(tag_of(uj.w))));
     }
   }
