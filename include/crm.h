@@ -45,7 +45,7 @@ extern "C" {
 #define CRM_E_INVALID     -1   /* bad argument: h <= 0, d0 <= 0, h < d0, dt <= 0, mu_s > mu_2, K/G <= 0 ... */
 #define CRM_E_DOMAIN      -2   /* a particle left the fixed grid box (reading A19) */
 #define CRM_E_NONFINITE   -3   /* non-finite fluid state after a step */
-#define CRM_E_UNSUPPORTED -4   /* Wendland kernel / Holmes extrapolation / ps_freq > 1 not built */
+#define CRM_E_UNSUPPORTED -4   /* option not built: Holmes extrapolation, support != 2, moving bodies on slabs */
 #define CRM_E_STATE       -5   /* crm_add_* after the first step, debug data not available */
 #define CRM_E_OOM         -6   /* device or host allocation failed */
 #define CRM_E_CUDA        -7   /* CUDA runtime error, or no sm_100 device */
@@ -53,7 +53,7 @@ extern "C" {
 #define CRM_E_CAPACITY    -9   /* a particle has more neighbours than crm_kernel_t.max_neighbors */
 
 #define CRM_KERNEL_CUBIC      0   /* Monaghan (1985) M4 cubic spline, support 2h (A1) */
-#define CRM_KERNEL_WENDLAND   1   /* quintic Wendland: CRM_E_UNSUPPORTED in this build */
+#define CRM_KERNEL_WENDLAND   1   /* quintic Wendland (Wendland 1995, A28): a (1 - q/2)^4 (2q + 1), support 2h */
 #define CRM_VISC_BILATERAL    0   /* Eq. artificial_viscosity_bilateral */
 #define CRM_VISC_UNILATERAL   1   /* Eq. artificial_viscosity_unilateral: only v_ij . r_ij < 0 */
 #define CRM_BC_ADAMI          0   /* Adami velocity extrapolation */
@@ -77,14 +77,14 @@ typedef struct {
 
 /* SPH discretisation (Table tab:sph_params). */
 typedef struct {
-  int    kernel;          /* CRM_KERNEL_CUBIC */
+  int    kernel;          /* CRM_KERNEL_CUBIC | CRM_KERNEL_WENDLAND (other values: CRM_E_INVALID) */
   double d0, h;           /* initial spacing, smoothing length (h >= d0); particle mass m = rho0 d0^3 */
   double support;         /* kernel support factor K = 2; 0 -> 2 */
   int    visc_mode;       /* CRM_VISC_* */
   double gamma_a;         /* artificial viscosity coefficient */
   double xi2;             /* regulariser xi^2 of Eq. 13; <= 0 -> 0.01 h^2 (A10) */
   double cs;              /* speed of sound; <= 0 -> sqrt(K / rho0) (A10) */
-  int    ps_freq;         /* neighbour-list rebuild period (Alg. 2); this build: 1 */
+  int    ps_freq;         /* neighbour-list rebuild period (Alg. 2); 0 -> 1 */
   double gravity[3];      /* body force per unit mass f_b */
   int    max_neighbors;   /* neighbour-list capacity per particle; 0 -> derived from h/d0 */
 } crm_kernel_t;

@@ -41,7 +41,8 @@ class Params(C.Structure):
                 ("grain_d", C.c_double), ("d0", C.c_double), ("h", C.c_double),
                 ("support", C.c_double), ("visc_mode", C.c_int), ("gamma_a", C.c_double),
                 ("xi2", C.c_double), ("cs", C.c_double), ("gravity", C.c_double * 3),
-                ("lo", C.c_double * 3), ("hi", C.c_double * 3), ("ps_freq", C.c_int)]
+                ("lo", C.c_double * 3), ("hi", C.c_double * 3), ("ps_freq", C.c_int),
+                ("kernel", C.c_int)]
 
 
 class BodyS(C.Structure):
@@ -64,6 +65,8 @@ def lib():
         L.oc_W.restype = C.c_double; L.oc_W.argtypes = [C.c_double, C.c_double]
         L.oc_dWdr.restype = C.c_double; L.oc_dWdr.argtypes = [C.c_double, C.c_double]
         L.oc_gradW.argtypes = [_D, C.c_double, _D]
+        L.oc_W_wendland.restype = C.c_double; L.oc_W_wendland.argtypes = [C.c_double, C.c_double]
+        L.oc_dWdr_wendland.restype = C.c_double; L.oc_dWdr_wendland.argtypes = [C.c_double, C.c_double]
         L.oc_paper_cell_index.restype = C.c_int64
         L.oc_paper_cell_index.argtypes = [C.c_int64] * 5
         L.oc_cell_coords.argtypes = [_F, _F, C.c_float, C.POINTER(C.c_int), C.POINTER(C.c_int)]
@@ -117,6 +120,14 @@ def dWdr(r: float, h: float) -> float:
     return lib().oc_dWdr(float(r), float(h))
 
 
+def W_wendland(r: float, h: float) -> float:
+    return lib().oc_W_wendland(float(r), float(h))
+
+
+def dWdr_wendland(r: float, h: float) -> float:
+    return lib().oc_dWdr_wendland(float(r), float(h))
+
+
 def gradW(xij, h: float) -> np.ndarray:
     x = _d(xij, (3,)); out = np.zeros(3)
     lib().oc_gradW(_p(x), float(h), _p(out))
@@ -158,6 +169,7 @@ def make_params(p: dict) -> Params:
         setattr(P, k, float(p.get(k, 0.0)))
     P.visc_mode = int(p.get("visc_mode", 0))
     P.ps_freq = int(p.get("ps_freq", 1))
+    P.kernel = int(p.get("kernel", 0))
     for k in ("gravity", "lo", "hi"):
         v = p.get(k, (0.0, 0.0, 0.0))
         setattr(P, k, (C.c_double * 3)(*[float(t) for t in v]))

@@ -68,6 +68,41 @@ void oc_gradW(const double xij[3], double h, double out[3]) {
 }
 
 /* ------------------------------------------------------------------------- */
+/* Kernel: quintic Wendland (Wendland 1995), support 2h (reading A28):  */
+/* the degree-5 compactly supported function W = a (1 - q/2)^4 (2q + 1),      */
+/* a = 21 / (16 pi h^3) in 3D, q = r/h <= 2.                                   */
+/* ------------------------------------------------------------------------- */
+double oc_W_wendland(double r, double h) {
+  const double q = r / h;
+  if (q >= 2.0) return 0.0;
+  const double a = 21.0 / (16.0 * M_PI * h * h * h);
+  const double t = 1.0 - 0.5 * q;
+  return a * t * t * t * t * (2.0 * q + 1.0);
+}
+
+/* d/dr of the above: a/h * [-2 t^3 (2q + 1) + 2 t^4] = -5 a q t^3 / h */
+double oc_dWdr_wendland(double r, double h) {
+  const double q = r / h;
+  if (q >= 2.0) return 0.0;
+  const double a = 21.0 / (16.0 * M_PI * h * h * h);
+  const double t = 1.0 - 0.5 * q;
+  return -5.0 * a * q * t * t * t / h;
+}
+
+/* the kernel the simulation uses (oc_params.kernel) */
+static double sim_W(const oc_params* p, double r) {
+  return p->kernel == OC_KERNEL_WENDLAND ? oc_W_wendland(r, p->h) : oc_W(r, p->h);
+}
+
+static void sim_gradW(const oc_params* p, const double xij[3], double out[3]) {
+  if (p->kernel != OC_KERNEL_WENDLAND) { oc_gradW(xij, p->h, out); return; }
+  const double r = sqrt(xij[0] * xij[0] + xij[1] * xij[1] + xij[2] * xij[2]);
+  if (r == 0.0) { out[0] = out[1] = out[2] = 0.0; return; }
+  const double f = oc_dWdr_wendland(r, p->h) / r;
+  out[0] = f * xij[0]; out[1] = f * xij[1]; out[2] = f * xij[2];
+}
+
+/* ------------------------------------------------------------------------- */
 /* Structural layer (Alg. 1) on fp32 positions, rules B1–B5.        */
 /* ------------------------------------------------------------------------- */
 /* c = z * (Y_size * X_size) + y * X_size + x. */
@@ -233,7 +268,8 @@ int oc_create(const oc_params* p, oc_sim** out) {
       || !(p->mu_s > 0) || p->mu_s > p->mu_2 || !(p->I0 > 0) || p->cohesion < 0 || !(p->grain_d > 0)
       || p->gamma_a < 0)
     return OC_E_INVALID;
-  if (p->support != 0.0 && p->support != 2.0) return OC_E_UNSUPPORTED;  /* cubic spline: support 2h */
+  if (p->support != 0.0 && p->support != 2.0) return OC_E_UNSUPPORTED;  /* both kernels: support 2h */
+  if (p->kernel != OC_KERNEL_CUBIC && p->kernel != OC_KERNEL_WENDLAND) return OC_E_INVALID;
   for (int a = 0; a < 3; ++a) if (!(p->hi[a] > p->lo[a])) return OC_E_INVALID;
   oc_sim* s = (oc_sim*)calloc(1, sizeof(oc_sim));
   if (!s) return OC_E_OOM;
@@ -533,7 +569,7 @@ static void bce_extrapolate(const oc_sim* s, const structure_t* st, const double
       if (s->kind[f] != OC_FLUID) continue;                 /* b: nearby fluid SPH particles */
       double xaf[3];
       for (int c = 0; c < 3; ++c) xaf[c] = x[3 * a + c] - x[3 * f + c];
-      const double W = oc_W(sqrt(xaf[0] * xaf[0] + xaf[1] * xaf[1] + xaf[2] * xaf[2]), h);
+      const double W = sim_W(&s->P, sqrt(xaf[0] * xaf[0] + xaf[1] * xaf[1] + xaf[2] * xaf[2]));
       SW += W;
       for (int c = 0; c < 3; ++c) su[c] += u[3 * f + c] * W;
       for (int c = 0; c < 6; ++c) ss[c] += sig[6 * f + c] * W;
@@ -583,8 +619,8 @@ static void rates(const oc_sim* s, const structure_t* st, const double* x, const
       const double r2 = xij[0] * xij[0] + xij[1] * xij[1] + xij[2] * xij[2];
       if (sqrt(r2) >= R) continue;
       double gW[3];
-      oc_gradW(xij, h, gW);
-      const double Vj = m / rho[j];                                     /* A7 */
+      sim_gradW(&s->P, xij, gW);
+      const double Vj = m / rho[j];                                   /* A7 */
       double uji[3];
       for (int c = 0; c < 3; ++c) uji[c] = u[3 * j + c] - u[3 * i + c];
       /* Eq. continuity_dis: -rho_i sum (u_j - u_i) . grad_i W_ij V_j */

@@ -40,7 +40,10 @@ typedef struct {
   double gravity[3];              /* f_b for fluid */
   double lo[3], hi[3];            /* fixed grid box (A19) */
   int    ps_freq;                 /* Alg. 2: lists rebuilt when t mod ps_freq = 0; <= 0 -> 1 */
+  int    kernel;                  /* OC_KERNEL_* (quintic Wendland or cubic spline) */
 } oc_params;
+
+enum { OC_KERNEL_CUBIC = 0, OC_KERNEL_WENDLAND = 1 };
 
 typedef struct {
   double mass, inertia[3], pos[3], quat[4], vel[3], omega[3];
@@ -54,6 +57,9 @@ typedef struct oc_sim oc_sim;
 double oc_W(double r, double h);                      /* cubic spline, A1 */
 double oc_dWdr(double r, double h);                   /* dW/dr of the same */
 void   oc_gradW(const double xij[3], double h, double out[3]);   /* grad_i W_ij, xij = x_i - x_j */
+/* quintic Wendland (Wendland 1995, reading A28), support 2h, and its dW/dr */
+double oc_W_wendland(double r, double h);
+double oc_dWdr_wendland(double r, double h);
 /* paper's linear cell index c = z*(Y*X) + y*X + x */
 int64_t oc_paper_cell_index(int64_t x, int64_t y, int64_t z, int64_t X, int64_t Y);
 /* B1 binning of one fp32 position; returns OC_E_DOMAIN if outside the grid */

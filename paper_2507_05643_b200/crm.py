@@ -169,7 +169,7 @@ class Crm:
         m = Material(params["rho0"], params["K"], params["G"], params["mu_s"], params["mu_2"], params["I0"],
                      params["cohesion"], params["grain_d"])
         k = Kernel()
-        k.kernel = 0
+        k.kernel = int(params.get("kernel", 0))
         k.d0 = params["d0"]; k.h = params["h"]; k.support = params.get("support", 2.0)
         k.visc_mode = int(params["visc_mode"]); k.gamma_a = params["gamma_a"]
         k.xi2 = params.get("xi2", 0.0); k.cs = params.get("cs", 0.0); k.ps_freq = int(params.get("ps_freq", 1))

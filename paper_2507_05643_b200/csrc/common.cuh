@@ -60,7 +60,41 @@ struct Phys {
   float kout;              // -0.75 h fnorm       : W'/r = kout (2 - q)^2 / r       (1 <= q < 2)
   float c_av;              // 2 m gamma_a h c_s   : AV coefficient numerator (Eq. 13)
   int build_lists;         // stage A filters and stores the lists (rebuild step of Alg. 2)
+  // quintic Wendland (A28): W = wd_a t^4 (2q + 1), W'/r = wd_f t^3, t = 1 - q/2
+  float wd_a;              // 21 / (16 pi h^3)
+  float wd_f;              // -5 wd_a / h^2
 };
+
+// kernel selection (template parameter of the tile kernels; CRM_KERNEL_* of include/crm.h)
+constexpr int KER_CUBIC = 0;
+constexpr int KER_WENDLAND = 1;
+
+// W(r) of the selected kernel, r < 2h (branch-free select for the cubic's two pieces)
+template <int KER>
+__device__ __forceinline__ float kernel_W(float r, const Phys& ph) {
+  const float q = r * ph.hinv;
+  if (KER == KER_WENDLAND) {
+    const float t = fmaf(-0.5f, q, 1.0f);
+    const float t2 = t * t;
+    return ph.wd_a * t2 * t2 * fmaf(2.0f, q, 1.0f);
+  } else {
+    const float tt = 2.0f - q;
+    return q < 1.0f ? ph.wnorm * (1.0f - 1.5f * q * q + 0.75f * q * q * q) : ph.wnorm * 0.25f * tt * tt * tt;
+  }
+}
+
+// W'(r)/r of the selected kernel, 0 < r < 2h; rinv = 1/r
+template <int KER>
+__device__ __forceinline__ float kernel_F(float r, float rinv, const Phys& ph) {
+  if (KER == KER_WENDLAND) {
+    const float t = fmaf(-0.5f * ph.hinv, r, 1.0f);
+    return ph.wd_f * t * t * t;
+  } else {
+    // cubic spline (A1): kin_a r + kin_b for r < h, kout (2 - r/h)^2 / r otherwise
+    const float t = fmaf(-ph.hinv, r, 2.0f);
+    return (r < ph.h) ? fmaf(ph.kin_a, r, ph.kin_b) : ph.kout * t * t * rinv;
+  }
+}
 
 // MUFU approximations (no IEEE/denormal wrappers): max rel. error ~2^-22 (rsqrt, rcp)
 __device__ __forceinline__ float rsqrt_approx(float x) {

@@ -41,10 +41,14 @@ int alloc_debug(crm_t* c) {
 void set_attrs(crm_t* c) {
   if (c->attrs_set) return;
   const int sm = (int)sizeof(TileSmem);
-  cudaFuncSetAttribute(k_bce_t<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-  cudaFuncSetAttribute(k_bce_t<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-  cudaFuncSetAttribute(k_rates_t<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-  cudaFuncSetAttribute(k_rates_t<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  cudaFuncSetAttribute(k_bce_t<0, KER_CUBIC>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  cudaFuncSetAttribute(k_bce_t<1, KER_CUBIC>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  cudaFuncSetAttribute(k_rates_t<0, KER_CUBIC>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  cudaFuncSetAttribute(k_rates_t<1, KER_CUBIC>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  cudaFuncSetAttribute(k_bce_t<0, KER_WENDLAND>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  cudaFuncSetAttribute(k_bce_t<1, KER_WENDLAND>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  cudaFuncSetAttribute(k_rates_t<0, KER_WENDLAND>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  cudaFuncSetAttribute(k_rates_t<1, KER_WENDLAND>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
   c->attrs_set = true;
 }
 
@@ -237,41 +241,55 @@ void issue_sort(crm_t* c, long long step, uint32_t drop_mask) {
 }
 
 // BCE extrapolation: stage 0 at y_n (with the marker filter), stage 1 at y_mid
+template <int KER>
+void issue_bce_k(crm_t* c, int stage, long long step, int store_all) {
+  const int y = c->cur;
+  const int dbg = c->dbg_on ? 1 : 0;
+  const dim3 tg((unsigned)c->ntiles), tb(TILE_THREADS);
+  const size_t sm = sizeof(TileSmem);
+  if (stage == 0)
+    launch_smem(c, KID_BCE_A, k_bce_t<0, KER>, tg, tb, sm, c->grid, c->ph, (const uint32_t*)c->cell_start,
+                (const float4*)c->P[y], (const float4*)c->L[y], c->U[y], c->S1[y], c->S2[y], c->list, c->nlist,
+                c->count_all, (const uint32_t*)c->cell_of, (const Pose*)c->d_pose0, c->cap, store_all, c->dbg, dbg,
+                c->d_err, (const uint32_t*)c->ids[y], step, c->tile_base);
+  else
+    launch_smem(c, KID_BCE_B, k_bce_t<1, KER>, tg, tb, sm, c->grid, c->ph, (const uint32_t*)c->cell_start,
+                (const float4*)c->Pm, (const float4*)c->Lm, c->Um, c->S1m, c->S2m, c->list, c->nlist,
+                c->count_all, (const uint32_t*)c->cell_of, (const Pose*)c->d_posem, c->cap, 0, c->dbg, dbg,
+                c->d_err, (const uint32_t*)c->ids[y], step, c->tile_base);
+}
+
 void issue_bce(crm_t* c, int stage, float dt, long long step, int store_all) {
   (void)dt;
   if (!c->n_bce) return;
-  const int y = c->cur;
-  const int dbg = c->dbg_on ? 1 : 0;
-  const dim3 tg((unsigned)c->ntiles), tb(TILE_THREADS);
-  const size_t sm = sizeof(TileSmem);
-  if (stage == 0)
-    launch_smem(c, KID_BCE_A, k_bce_t<0>, tg, tb, sm, c->grid, c->ph, (const uint32_t*)c->cell_start,
-                (const float4*)c->P[y], (const float4*)c->L[y], c->U[y], c->S1[y], c->S2[y], c->list, c->nlist,
-                c->count_all, (const uint32_t*)c->cell_of, (const Pose*)c->d_pose0, c->cap, store_all, c->dbg, dbg, c->d_err,
-                (const uint32_t*)c->ids[y], step, c->tile_base);
-  else
-    launch_smem(c, KID_BCE_B, k_bce_t<1>, tg, tb, sm, c->grid, c->ph, (const uint32_t*)c->cell_start,
-                (const float4*)c->Pm, (const float4*)c->Lm, c->Um, c->S1m, c->S2m, c->list, c->nlist,
-                c->count_all, (const uint32_t*)c->cell_of, (const Pose*)c->d_posem, c->cap, 0, c->dbg, dbg, c->d_err,
-                (const uint32_t*)c->ids[y], step, c->tile_base);
+  if (c->ker.kernel == CRM_KERNEL_WENDLAND) issue_bce_k<KER_WENDLAND>(c, stage, step, store_all);
+  else issue_bce_k<KER_CUBIC>(c, stage, step, store_all);
 }
 
 // rates: stage 0 (fluid filter + rates at y_n -> y_mid), stage 1 (rates at y_mid -> y_{n+1})
-void issue_rates(crm_t* c, int stage, float dt, long long step) {
+template <int KER>
+void issue_rates_k(crm_t* c, int stage, float dt, long long step) {
   const int y = c->cur;
   const int dbg = c->dbg_on ? 1 : 0;
   const dim3 tg((unsigned)c->ntiles), tb(TILE_THREADS);
   const size_t sm = sizeof(TileSmem);
   if (stage == 0)
-    launch_smem(c, KID_RATES_A, k_rates_t<0>, tg, tb, sm, c->grid, c->ph, dt, (const uint32_t*)c->cell_start,
+    launch_smem(c, KID_RATES_A, k_rates_t<0, KER>, tg, tb, sm, c->grid, c->ph, dt, (const uint32_t*)c->cell_start,
                 (const float4*)c->P[y], (const float4*)c->L[y], (const float4*)c->U[y], (const float4*)c->S1[y],
-                (const float2*)c->S2[y], c->Pm, c->Lm, c->Um, c->S1m, c->S2m, c->list, c->nlist, c->count_all, (const uint32_t*)c->cell_of, c->cap, c->macc,
-                c->dbg, dbg, c->d_err, (const uint32_t*)c->ids[y], step, c->tile_base);
+                (const float2*)c->S2[y], c->Pm, c->Lm, c->Um, c->S1m, c->S2m, c->list, c->nlist, c->count_all,
+                (const uint32_t*)c->cell_of, c->cap, c->macc, c->dbg, dbg, c->d_err, (const uint32_t*)c->ids[y], step,
+                c->tile_base);
   else
-    launch_smem(c, KID_RATES_B, k_rates_t<1>, tg, tb, sm, c->grid, c->ph, dt, (const uint32_t*)c->cell_start,
+    launch_smem(c, KID_RATES_B, k_rates_t<1, KER>, tg, tb, sm, c->grid, c->ph, dt, (const uint32_t*)c->cell_start,
                 (const float4*)c->Pm, (const float4*)c->Lm, (const float4*)c->Um, (const float4*)c->S1m,
-                (const float2*)c->S2m, c->P[y], c->L[y], c->U[y], c->S1[y], c->S2[y], c->list, c->nlist, c->count_all, (const uint32_t*)c->cell_of, c->cap,
-                c->macc, c->dbg, dbg, c->d_err, (const uint32_t*)c->ids[y], step, c->tile_base);
+                (const float2*)c->S2m, c->P[y], c->L[y], c->U[y], c->S1[y], c->S2[y], c->list, c->nlist, c->count_all,
+                (const uint32_t*)c->cell_of, c->cap, c->macc, c->dbg, dbg, c->d_err, (const uint32_t*)c->ids[y], step,
+                c->tile_base);
+}
+
+void issue_rates(crm_t* c, int stage, float dt, long long step) {
+  if (c->ker.kernel == CRM_KERNEL_WENDLAND) issue_rates_k<KER_WENDLAND>(c, stage, dt, step);
+  else issue_rates_k<KER_CUBIC>(c, stage, dt, step);
 }
 
 // one RK2 step on one GPU (everything on the stream, no host sync)
@@ -435,7 +453,8 @@ int crm_create(const crm_material_t* mat, const crm_kernel_t* ker, const crm_bou
   if (!(k.h > 0) || !(k.d0 > 0) || k.h < k.d0 || !(m.rho0 > 0) || !(m.K > 0) || !(m.G > 0) || !(m.mu_s > 0) ||
       m.mu_s > m.mu_2 || !(m.I0 > 0) || m.cohesion < 0 || !(m.grain_d > 0) || k.gamma_a < 0 || k.max_neighbors < 0)
     return CRM_E_INVALID;
-  if (k.kernel != CRM_KERNEL_CUBIC || (k.support != 0.0 && k.support != 2.0)) return CRM_E_UNSUPPORTED;
+  if (k.kernel != CRM_KERNEL_CUBIC && k.kernel != CRM_KERNEL_WENDLAND) return CRM_E_INVALID;
+  if (k.support != 0.0 && k.support != 2.0) return CRM_E_UNSUPPORTED;   // both kernels: 2h
   if (bnd->method != CRM_BC_ADAMI) return CRM_E_UNSUPPORTED;
   if (k.ps_freq < 0) return CRM_E_INVALID;
   if (k.visc_mode != CRM_VISC_BILATERAL && k.visc_mode != CRM_VISC_UNILATERAL) return CRM_E_INVALID;
@@ -498,6 +517,9 @@ int crm_create(const crm_material_t* mat, const crm_kernel_t* ker, const crm_bou
     c->ph.kin_b = (float)(-3.0 * fnorm);
     c->ph.kout = (float)(-0.75 * h * fnorm);
     c->ph.c_av = (float)(2.0 * m.rho0 * k.d0 * k.d0 * k.d0 * k.gamma_a * h * cs);
+    const double wa = 21.0 / (16.0 * M_PI * h * h * h);
+    c->ph.wd_a = (float)wa;
+    c->ph.wd_f = (float)(-5.0 * wa / (h * h));
   }
   // neighbour capacity: twice the lattice count of the 2h ball, rounded up to 32
   if (k.max_neighbors > 0) {

@@ -64,24 +64,6 @@ __device__ __forceinline__ void body_kinematics(const Pose& q, float x, float y,
   }
 }
 
-// cubic spline W (A1) for r^2 < R2
-__device__ __forceinline__ float kernel_W(float r2, const Phys& ph) {
-  const float r = sqrtf(r2);
-  const float q = r * ph.hinv;
-  const float t = 2.0f - q;
-  return q < 1.0f ? ph.wnorm * (1.0f - 1.5f * q * q + 0.75f * q * q * q) : ph.wnorm * 0.25f * t * t * t;
-}
-
-// W'(r)/r (A1), r2 > 0 and r2 < R2
-__device__ __forceinline__ float kernel_F(float r2, const Phys& ph) {
-  const float rinv = rsqrtf(r2);
-  const float q = r2 * rinv * ph.hinv;
-  const float t = 2.0f - q;
-  const float inner = -3.0f + 2.25f * q;
-  const float outer = -0.75f * t * t * (ph.h * rinv);   // (2-q)^2 / q
-  return ph.fnorm * (q < 1.0f ? inner : outer);
-}
-
 // ------------------------------------------------------------------------------------
 // mu(I) return map in fp32; readings A16 (gamma_dot >= 0, p floor 1 Pa for I
 // only, I = 0 -> mu_s), A27 (tau_max >= 0).  s, sn = (xx,yy,zz,xy,xz,yz)

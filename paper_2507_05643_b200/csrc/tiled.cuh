@@ -133,7 +133,7 @@ __device__ __forceinline__ void build_lists(const Grid& g, const TileSmem& sm, c
 }
 
 // ---------------------------------------------------------------------------------------
-template <int STAGE, bool STAGED>
+template <int STAGE, int KER, bool STAGED>
 __device__ __forceinline__ void bce_tile(const Phys& ph, TileSmem& sm, const float4* __restrict__ P,
                                          const float4* __restrict__ L, float4* __restrict__ U, float4* __restrict__ S1,
                                          float2* __restrict__ S2, const uint16_t* __restrict__ list,
@@ -171,11 +171,7 @@ __device__ __forceinline__ void bce_tile(const Phys& ph, TileSmem& sm, const flo
         // fluid neighbours only; W = 0 beyond the support (A17)
         const bool ok = !tag_is_bce(tag_of(uf.w)) && r2 < ph.R2;
         const float r = (r2 > 0.f) ? r2 * rsqrt_approx(r2) : 0.f;
-        const float qq = r * ph.hinv;
-        const float tt = 2.0f - qq;
-        const float Wv = qq < 1.0f ? ph.wnorm * (1.0f - 1.5f * qq * qq + 0.75f * qq * qq * qq)
-                                   : ph.wnorm * 0.25f * tt * tt * tt;
-        const float W = ok ? Wv : 0.f;
+        const float W = ok ? kernel_W<KER>(r, ph) : 0.f;
         SW += W;
         su[0] += uf.x * W; su[1] += uf.y * W; su[2] += uf.z * W;
         ss[0] += s1.x * W; ss[1] += s1.y * W; ss[2] += s1.z * W;
@@ -207,7 +203,7 @@ __device__ __forceinline__ void bce_tile(const Phys& ph, TileSmem& sm, const flo
   }
 }
 
-template <int STAGE>
+template <int STAGE, int KER>
 __global__ void TILE_BOUNDS
     k_bce_t(Grid g, Phys ph, const uint32_t* __restrict__ cell_start, const float4* __restrict__ P,
             const float4* __restrict__ L, float4* __restrict__ U, float4* __restrict__ S1, float2* __restrict__ S2,
@@ -246,8 +242,8 @@ __global__ void TILE_BOUNDS
   }
   tile_relativize(L, sm);
   __syncthreads();
-  if (sm.staged) bce_tile<STAGE, true>(ph, sm, P, L, U, S1, S2, list, nlist, pose, cap, dbg, dbg_on);
-  else bce_tile<STAGE, false>(ph, sm, P, L, U, S1, S2, list, nlist, pose, cap, dbg, dbg_on);
+  if (sm.staged) bce_tile<STAGE, KER, true>(ph, sm, P, L, U, S1, S2, list, nlist, pose, cap, dbg, dbg_on);
+  else bce_tile<STAGE, KER, false>(ph, sm, P, L, U, S1, S2, list, nlist, pose, cap, dbg, dbg_on);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -255,6 +251,7 @@ struct PairAcc {
   float L[9], Gs[3], Ms[3], Pi[3];
 };
 
+template <int KER>
 __device__ __forceinline__ void pair_terms(PairAcc& A, const Phys& ph, const float4& pi, const float4& ui,
                                            const float4& pj, const float4& uj, const float4& sj1, const float2& sj2,
                                            bool with_L, bool okj) {
@@ -263,12 +260,9 @@ __device__ __forceinline__ void pair_terms(PairAcc& A, const Phys& ph, const flo
   // branch-free: invalid pairs (r >= 2h, A17; r = 0 incl. the self padding, A18; a marker when
   // only fluid counts) get F = 0, hence a zero contribution to every sum
   const bool ok = r2 < ph.R2 && r2 > 0.f && okj;
-  // W'(r)/r of the cubic spline (A1): kin_a r + kin_b for r < h, kout (2 - r/h)^2 / r otherwise
   const float rinv = rsqrt_approx(r2);
   const float r = r2 * rinv;
-  const float t = fmaf(-ph.hinv, r, 2.0f);
-  const float Fv = (r < ph.h) ? fmaf(ph.kin_a, r, ph.kin_b) : ph.kout * t * t * rinv;
-  const float F = ok ? Fv : 0.f;
+  const float F = ok ? kernel_F<KER>(r, rinv, ph) : 0.f;   // W'(r)/r (A1 / A28)
   const float w = ph.m * rcp_approx(pj.w) * F;                         // V_j W'/r (A7)
   const float gx = w * dx, gy = w * dy, gz = w * dz;                  // V_j grad_i W_ij
   const float dux = uj.x - ui.x, duy = uj.y - ui.y, duz = uj.z - ui.z; // u_ji
@@ -290,7 +284,7 @@ __device__ __forceinline__ void pair_terms(PairAcc& A, const Phys& ph, const flo
   A.Pi[0] += coef * dx; A.Pi[1] += coef * dy; A.Pi[2] += coef * dz;
 }
 
-template <bool STAGED>
+template <int KER, bool STAGED>
 __device__ __forceinline__ void pair_loop(PairAcc& A, const Phys& ph, const TileSmem& sm, const float4* __restrict__ P,
                                           const float4* __restrict__ L, const float4* __restrict__ U,
                                           const float4* __restrict__ S1, const float2* __restrict__ S2,
@@ -310,14 +304,14 @@ __device__ __forceinline__ void pair_loop(PairAcc& A, const Phys& ph, const Tile
       float2 s2;
       // (measured: making these gathers bank-conflict free would gain only ~10 % in stage B)
       load_all<STAGED>(sm, P, L, U, S1, S2, list_entry(v, e), pj, uj, s1, s2);
-      pair_terms(A, ph, pi, ui, pj, uj, s1, s2, with_L, !(fluid_only && tag_is_bce(tag_of(uj.w))));
+      pair_terms<KER>(A, ph, pi, ui, pj, uj, s1, s2, with_L, !(fluid_only && tag_is_bce(tag_of(uj.w))));
     }
   }
 }
 
 // STAGE 0: (P,L,U,S) = y_n; writes y_mid to (YP,YL,YU,YS).  STAGE 1: (P,L,U,S) = y_mid;
 // (YP,YL,YU,YS) = y_n in, y_{n+1} out (own slot only; neighbours are read from y_mid).
-template <int STAGE, bool STAGED>
+template <int STAGE, int KER, bool STAGED>
 __device__ __forceinline__ void rates_tile(const Phys& ph, float dt, TileSmem& sm, const float4* __restrict__ P,
                                            const float4* __restrict__ L, const float4* __restrict__ U,
                                            const float4* __restrict__ S1, const float2* __restrict__ S2,
@@ -342,7 +336,7 @@ __device__ __forceinline__ void rates_tile(const Phys& ph, float dt, TileSmem& s
 #pragma unroll
     for (int k = 0; k < 3; ++k) { A.Gs[k] = 0.f; A.Ms[k] = 0.f; A.Pi[k] = 0.f; }
     if (bce) {   // STAGE 1, moving-body marker: m a_s over fluid neighbours, no gravity (A13)
-      pair_loop<STAGED>(A, ph, sm, P, L, U, S1, S2, list, i, cap, nl, pi, ui, false, true);
+      pair_loop<KER, STAGED>(A, ph, sm, P, L, U, S1, S2, list, i, cap, nl, pi, ui, false, true);
       const float4 si1 = S1[i];
       const float2 si2 = S2[i];
       const float rinv_i = 1.0f / pi.w;
@@ -354,7 +348,7 @@ __device__ __forceinline__ void rates_tile(const Phys& ph, float dt, TileSmem& s
       if (dbg_on) dbg.acc[1][i] = make_float4(a[0], a[1], a[2], 0.f);
       continue;
     }
-    pair_loop<STAGED>(A, ph, sm, P, L, U, S1, S2, list, i, cap, nl, pi, ui, true, false);
+    pair_loop<KER, STAGED>(A, ph, sm, P, L, U, S1, S2, list, i, cap, nl, pi, ui, true, false);
     // own state for the epilogue, (re)loaded after the loop to keep registers free inside it
     const float4 phi = P[i];
     const float4 pli = L[i];
@@ -434,7 +428,7 @@ __device__ __forceinline__ void rates_tile(const Phys& ph, float dt, TileSmem& s
   }
 }
 
-template <int STAGE>
+template <int STAGE, int KER>
 __global__ void TILE_BOUNDS
     k_rates_t(Grid g, Phys ph, float dt, const uint32_t* __restrict__ cell_start, const float4* __restrict__ P,
               const float4* __restrict__ L, const float4* __restrict__ U, const float4* __restrict__ S1,
@@ -486,10 +480,10 @@ __global__ void TILE_BOUNDS
   tile_relativize(L, sm);
   __syncthreads();
   if (sm.staged)
-    rates_tile<STAGE, true>(ph, dt, sm, P, L, U, S1, S2, YP, YL, YU, YS1, YS2, list, nlist, cap, macc, dbg, dbg_on,
+    rates_tile<STAGE, KER, true>(ph, dt, sm, P, L, U, S1, S2, YP, YL, YU, YS1, YS2, list, nlist, cap, macc, dbg, dbg_on,
                             err, ids, step);
   else
-    rates_tile<STAGE, false>(ph, dt, sm, P, L, U, S1, S2, YP, YL, YU, YS1, YS2, list, nlist, cap, macc, dbg, dbg_on,
+    rates_tile<STAGE, KER, false>(ph, dt, sm, P, L, U, S1, S2, YP, YL, YU, YS1, YS2, list, nlist, cap, macc, dbg, dbg_on,
                              err, ids, step);
 }
 

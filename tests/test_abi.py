@@ -72,6 +72,14 @@ def test_invalid_parameters_rejected_before_device(lib):
     with pytest.raises(crm.CrmError) as e:
         crm.Crm(p)
     assert e.value.code == crm.CRM_E_INVALID
+    p = dict(sc.params, kernel=2)                     # only cubic (0) and Wendland (1)
+    with pytest.raises(crm.CrmError) as e:
+        crm.Crm(p)
+    assert e.value.code == crm.CRM_E_INVALID
+    p = dict(sc.params, support=3.0)                  # both kernels have support 2h
+    with pytest.raises(crm.CrmError) as e:
+        crm.Crm(p)
+    assert e.value.code == crm.CRM_E_UNSUPPORTED
 
 
 def test_no_cpu_fallback_without_gpu(lib):

@@ -113,6 +113,39 @@ def test_rates_stage_A_and_B_S0(crm, visc):
         assert rel_linf(tg[nf:], to[nf:]) <= RATE_TOL, ("bce sigma", stage)
 
 
+@pytest.mark.parametrize("visc", [workloads.VISC_BILATERAL, workloads.VISC_UNILATERAL])
+def test_rates_wendland_S0(crm, visc):
+    """Quintic Wendland kernel (A28): same bars as the cubic spline."""
+    sc = workloads.rate_state_S0(workloads.block_settle())
+    sc.params.update(kernel=1, visc_mode=visc, gamma_a=0.2)
+    g, o = run_one_armed(crm, sc, sc.dt)
+    nf = sc.n_fluid
+    for stage in (0, 1):
+        for a_g, a_o in zip(g.last_rates(stage), o.last_rates(stage)):
+            assert rel_linf(a_g[:nf], a_o[:nf]) <= RATE_TOL, stage
+        for a_g, a_o in zip(g.last_bce(stage), o.last_bce(stage)):
+            assert rel_linf(a_g[nf:], a_o[nf:]) <= RATE_TOL, stage
+    # the kernel choice matters: the cubic-spline rates differ at this state by far more than the bar
+    sc.params["kernel"] = 0
+    oc = oracle.load_scenario(sc)
+    oc.step(sc.dt, 1)
+    assert rel_linf(oc.last_rates(0)[1][:nf], o.last_rates(0)[1][:nf]) > 100 * RATE_TOL
+
+
+def test_wendland_100_steps_macroscopic(crm):
+    sc = workloads.block_settle()
+    sc.params["kernel"] = 1
+    g, o = both(crm, sc)
+    g.step(sc.dt, 100)
+    o.step(sc.dt, 100)
+    nf = sc.n_fluid
+    top = np.argsort(sc.fluid_pos[:, 2])[-400:]
+    xg, xo = g.get_state()[0][:nf], o.get_state()[0][:nf]
+    hg, ho = settled_height(xg, top, sc.params["d0"]), settled_height(xo, top, sc.params["d0"])
+    assert abs(hg - ho) <= 0.02 * ho
+    assert np.abs(xg - xo).max() < 0.02 * sc.params["d0"]
+
+
 def test_one_step_state_S0_confined(crm):
     sc = workloads.rate_state_S0(workloads.block_settle())
     sc.fluid_sig = workloads.f32(sc.fluid_sig + np.array([-2000.0, -2000.0, -2000.0, 0, 0, 0]))
