@@ -90,6 +90,14 @@ def lib():
         L.oc_last_bce.argtypes = [C.c_void_p, C.c_int, _D, _D]
         L.oc_last_error.restype = C.c_char_p; L.oc_last_error.argtypes = [C.c_void_p]
         L.oc_num_threads.restype = C.c_int
+        L.oc_activity.restype = C.c_int
+        L.oc_activity.argtypes = [_D, C.c_int, _D, _D, _D, C.c_double]
+        L.oc_manage_capacity.restype = C.c_int64
+        L.oc_manage_capacity.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_int,
+                                         C.POINTER(C.c_int)]
+        L.oc_set_active_box.argtypes = [C.c_void_p, C.c_int32, _D]
+        L.oc_set_active_delay.argtypes = [C.c_void_p, C.c_double]
+        L.oc_get_activity.argtypes = [C.c_void_p, C.POINTER(C.c_uint8)]
         _lib = L
     return _lib
 
@@ -292,6 +300,38 @@ class OracleSim:
         self._chk(self._L.oc_last_bce(self.h, stage, _p(vel), _p(sig)), "last_bce")
         return vel, sig
 
+    # ---- active domains (Alg. 3)
+    def set_active_box(self, body: int, half):
+        h = _d(half, (3,))
+        self._chk(self._L.oc_set_active_box(self.h, int(body), _p(h)), "set_active_box")
+
+    def set_active_delay(self, t_delay: float):
+        self._chk(self._L.oc_set_active_delay(self.h, float(t_delay)), "set_active_delay")
+
+    def activity(self) -> np.ndarray:
+        f = np.zeros(self.count(), np.uint8)
+        self._chk(self._L.oc_get_activity(self.h, f.ctypes.data_as(C.POINTER(C.c_uint8))), "activity")
+        return f
+
+
+def activity(x, boxes, radius: float) -> int:
+    """UpdateActivity of one point; boxes = [(pos[3], R[3x3] body->world, half[3]), ...]."""
+    nb = len(boxes)
+    bp = np.zeros(3 * nb + 1); bR = np.zeros(9 * nb + 1); bh = np.zeros(3 * nb + 1)
+    for k, (pos, R, half) in enumerate(boxes):
+        bp[3 * k:3 * k + 3] = pos
+        bR[9 * k:9 * k + 9] = np.asarray(R, float).ravel()
+        bh[3 * k:3 * k + 3] = half
+    xx = _d(x, (3,))
+    return lib().oc_activity(_p(xx), nb, _p(bp), _p(bR), _p(bh), float(radius))
+
+
+def manage_capacity(capacity: int, required: int, step: int, growth=1.2, shrink=0.75, interval=50):
+    a = C.c_int(0)
+    cap = lib().oc_manage_capacity(int(capacity), int(required), int(step), float(growth), float(shrink),
+                                   int(interval), C.byref(a))
+    return int(cap), int(a.value)
+
 
 def load_scenario(sc) -> OracleSim:
     """Build an OracleSim from a workloads.Scenario (fluid first, then walls, then bodies)."""
@@ -302,4 +342,9 @@ def load_scenario(sc) -> OracleSim:
     for b in sc.bodies:
         bid = s.add_body(b)
         s.add_bce(bid, b.markers)
+    act = getattr(sc, "active", None) or {}
+    for body, half in act.get("boxes", {}).items():
+        s.set_active_box(body, half)
+    if "t_delay" in act:
+        s.set_active_delay(act["t_delay"])
     return s

@@ -242,7 +242,11 @@ struct oc_sim {
   double* xl;                 /* marker position in its body's frame */
   int nb; body_rec bodies[OC_MAX_BODIES];
   int64_t steps_done;
+  double time;                /* t = sum of the step sizes taken (Alg. 3 compares it with t_delay) */
   void* kept;                 /* structure_t of the last rebuild (Alg. 2) */
+  int has_box[OC_MAX_BODIES]; /* active boxes (Alg. 3): half extents at each body's local origin */
+  double box_half[OC_MAX_BODIES][3];
+  double t_delay;
   double* rates[2];           /* per stage: n * 10 (drho, acc3, dsig6) */
   double* bce[2];             /* per stage: n * 9 (u3, sig6) */
   char err[256];
@@ -289,6 +293,7 @@ int oc_create(const oc_params* p, oc_sim** out) {
 }
 
 static void drop_kept(oc_sim* s);
+static uint8_t* compute_activity(const oc_sim* s);
 
 void oc_destroy(oc_sim* s) {
   if (!s) return;
@@ -385,10 +390,11 @@ typedef struct {
   uint32_t* cell_start;  /* M+1 */
   int64_t* offset;       /* by id, n+1 (CSR of neighbour ids) */
   int64_t* list;
+  uint8_t* act;          /* by id: OC_ACTIVE / OC_EXTENDED / OC_INACTIVE; NULL = all active (Alg. 3 off) */
 } structure_t;
 
 static void free_structure(structure_t* st) {
-  free(st->cell); free(st->sorted); free(st->cell_start); free(st->offset); free(st->list);
+  free(st->cell); free(st->sorted); free(st->cell_start); free(st->offset); free(st->list); free(st->act);
   memset(st, 0, sizeof(*st));
 }
 
@@ -412,8 +418,12 @@ static int cmp_i64(const void* a, const void* b) {
   return x < y ? -1 : (x > y ? 1 : 0);
 }
 
-static int build_structure(oc_sim* s, const double* x, structure_t* st, int want_list) {
+/* act (by id, may be NULL) is owned by st afterwards: Inactive particles (Alg. 3) take no part in
+ * the structure: no cell (sentinel M), sorted behind every active particle, no neighbours, nobody's
+ * neighbour ("they are not included in neighbor search"). */
+static int build_structure(oc_sim* s, const double* x, structure_t* st, int want_list, uint8_t* act) {
   memset(st, 0, sizeof(*st));
+  st->act = act;
   const int64_t n = s->n;
   const double sd = s->R;                    /* cell size = 2h */
   const float s32 = (float)sd;
@@ -434,6 +444,7 @@ static int build_structure(oc_sim* s, const double* x, structure_t* st, int want
   /* Step 1: hash every particle */
   for (int64_t i = 0; i < n; ++i) {
     int c[3];
+    if (act && act[i] == OC_INACTIVE) { st->cell[i] = (uint32_t)st->M; continue; }
     if (oc_cell_coords(&x32[3 * i], lo32, s32, st->dims, c) != OC_OK) {
       snprintf(s->err, sizeof s->err, "particle id %lld outside the grid at step %lld",
                (long long)i, (long long)s->steps_done);
@@ -446,7 +457,8 @@ static int build_structure(oc_sim* s, const double* x, structure_t* st, int want
   g_sort_cell = st->cell;
   qsort(st->sorted, (size_t)n, sizeof(int64_t), cmp_cell_id);
   /* Step 3: cellStart / cellEnd; cellEnd[c] = cellStart[c+1] (CSR, B4) */
-  for (int64_t i = 0; i < n; ++i) st->cell_start[st->cell[i] + 1]++;
+  for (int64_t i = 0; i < n; ++i)
+    if (st->cell[i] < (uint32_t)st->M) st->cell_start[st->cell[i] + 1]++;
   for (int64_t c = 0; c < st->M; ++c) st->cell_start[c + 1] += st->cell_start[c];
   if (!want_list) { free(x32); return OC_OK; }
   /* Step 4 (Alg. 1): per sorted particle, 27 cells, strict < 2h.
@@ -459,9 +471,10 @@ static int build_structure(oc_sim* s, const double* x, structure_t* st, int want
     #pragma omp parallel for schedule(dynamic, 256)
     for (int64_t si = 0; si < n; ++si) {
       const int64_t i = st->sorted[si];
+      int64_t count = 0;
+      if (st->cell[i] >= (uint32_t)st->M) { if (pass == 0) cnt[i] = 0; continue; }   /* Inactive */
       int g[3];
       oc_cell_coords(&x32[3 * i], lo32, s32, st->dims, g);      /* calcGridPos */
-      int64_t count = 0;
       for (int dx = -1; dx <= 1; ++dx)
         for (int dy = -1; dy <= 1; ++dy)
           for (int dz = -1; dz <= 1; ++dz) {
@@ -492,7 +505,7 @@ static int build_structure(oc_sim* s, const double* x, structure_t* st, int want
 int oc_structure(oc_sim* s, uint32_t* cell_by_id, int64_t* sorted_ids, uint32_t* nbr_count_by_id,
                  uint32_t* cell_start, int64_t* n_cells) {
   structure_t st;
-  int r = build_structure(s, s->x, &st, nbr_count_by_id != NULL);
+  int r = build_structure(s, s->x, &st, nbr_count_by_id != NULL, compute_activity(s));
   if (r) return r;
   if (cell_by_id) memcpy(cell_by_id, st.cell, (size_t)s->n * sizeof(uint32_t));
   if (sorted_ids) memcpy(sorted_ids, st.sorted, (size_t)s->n * sizeof(int64_t));
@@ -506,7 +519,7 @@ int oc_structure(oc_sim* s, uint32_t* cell_by_id, int64_t* sorted_ids, uint32_t*
 
 int oc_neighbors(oc_sim* s, int64_t* offsets, int64_t* list) {
   structure_t st;
-  int r = build_structure(s, s->x, &st, 1);
+  int r = build_structure(s, s->x, &st, 1, compute_activity(s));
   if (r) return r;
   memcpy(offsets, st.offset, (size_t)(s->n + 1) * sizeof(int64_t));
   if (list) {
@@ -554,6 +567,98 @@ static void marker_kinematics(const oc_sim* s, const pose_t* poses, int64_t i,
   for (int a = 0; a < 3; ++a) { ub[a] = P->vel[a] + wr[a]; ab[a] = P->acc[a] + ar[a] + wwr[a]; }
 }
 
+/* ---- active domains (Alg. 3) ----------------------------------- */
+/* UpdateActivity: "Particles residing within an active box are flagged as Active ...
+ * particles outside an active box but within a distance 2h of its boundary are flagged as
+ * Extended-Active ... All remaining particles are flagged as Inactive."  The box is an OOBB at the
+ * body's local origin; the distance to it is the Euclidean distance to the solid box
+ * (reading A29), evaluated in fp64 (rule B6). */
+int oc_activity(const double x[3], int nbox, const double* box_pos, const double* box_R,
+                const double* box_half, double radius) {
+  int ext = 0;
+  for (int b = 0; b < nbox; ++b) {
+    const double* p = &box_pos[3 * b];
+    const double* R = &box_R[9 * b];
+    const double* hb = &box_half[3 * b];
+    const double d[3] = {x[0] - p[0], x[1] - p[1], x[2] - p[2]};
+    double dist2 = 0.0;
+    int inside = 1;
+    for (int a = 0; a < 3; ++a) {
+      const double l = R[a] * d[0] + R[3 + a] * d[1] + R[6 + a] * d[2];   /* body frame: R^T d */
+      const double o = fabs(l) - hb[a];
+      if (o > 0.0) { inside = 0; dist2 += o * o; }
+    }
+    if (inside) return OC_ACTIVE;
+    if (dist2 < radius * radius) ext = 1;
+  }
+  return ext ? OC_EXTENDED : OC_INACTIVE;
+}
+
+/* ManageArrayMemory: grow to N_{a+e} G when N_{a+e} exceeds the capacity; every S_I steps,
+ * shrink to N_{a+e} when N_{a+e} / capacity < S; otherwise keep. */
+int64_t oc_manage_capacity(int64_t capacity, int64_t required, int64_t step, double growth,
+                           double shrink, int shrink_interval, int* action) {
+  int act = OC_CAP_KEEP;
+  int64_t cap = capacity;
+  if (required > capacity) {
+    act = OC_CAP_GROW;
+    cap = (int64_t)ceil((double)required * growth);
+  } else if (shrink_interval > 0 && step % shrink_interval == 0 && capacity > 0 &&
+             (double)required / (double)capacity < shrink) {
+    act = OC_CAP_SHRINK;
+    cap = required;
+  }
+  if (action) *action = act;
+  return cap;
+}
+
+int oc_set_active_box(oc_sim* s, int32_t body, const double half[3]) {
+  if (s->steps_done > 0) return OC_E_STATE;
+  if (body < 0 || body >= s->nb || !half) return OC_E_INVALID;
+  for (int a = 0; a < 3; ++a) if (!(half[a] >= 0.0)) return OC_E_INVALID;
+  s->has_box[body] = 1;
+  for (int a = 0; a < 3; ++a) s->box_half[body][a] = half[a];
+  drop_kept(s);
+  return OC_OK;
+}
+
+int oc_set_active_delay(oc_sim* s, double t_delay) {
+  s->t_delay = t_delay;
+  drop_kept(s);
+  return OC_OK;
+}
+
+/* flags of every particle at the current state and time, or NULL while Alg. 3 is off
+ * ("if t > t_delay", Alg. 3); markers of moving bodies are always Active (reading A29) */
+static uint8_t* compute_activity(const oc_sim* s) {
+  int nbox = 0;
+  double bp[3 * OC_MAX_BODIES], bR[9 * OC_MAX_BODIES], bh[3 * OC_MAX_BODIES];
+  for (int b = 0; b < s->nb; ++b) {
+    if (!s->has_box[b]) continue;
+    pose_t P;
+    body_pose(&s->bodies[b], 0.0, &P);
+    for (int a = 0; a < 3; ++a) { bp[3 * nbox + a] = P.pos[a]; bh[3 * nbox + a] = s->box_half[b][a]; }
+    for (int k = 0; k < 9; ++k) bR[9 * nbox + k] = P.R[k];
+    ++nbox;
+  }
+  if (nbox == 0 || !(s->time > s->t_delay)) return NULL;
+  uint8_t* act = (uint8_t*)malloc((size_t)(s->n ? s->n : 1));
+  if (!act) return NULL;
+  for (int64_t i = 0; i < s->n; ++i) {
+    const int moving_marker = s->kind[i] == OC_BCE && s->bodies[s->body[i]].b.motion != OC_BODY_FIXED;
+    act[i] = moving_marker ? OC_ACTIVE : (uint8_t)oc_activity(&s->x[3 * i], nbox, bp, bR, bh, s->R);
+  }
+  return act;
+}
+
+int oc_get_activity(const oc_sim* s, uint8_t* flags) {
+  const structure_t* st = (const structure_t*)s->kept;
+  for (int64_t i = 0; i < s->n; ++i) flags[i] = (st && st->act) ? st->act[i] : OC_ACTIVE;
+  return OC_OK;
+}
+
+static int inactive(const structure_t* st, int64_t i) { return st->act && st->act[i] == OC_INACTIVE; }
+
 /* ---- BCE extrapolation, Adami + stress (reading A12) ---- */
 static void bce_extrapolate(const oc_sim* s, const structure_t* st, const double* x, const double* u,
                             const double* rho, const double* sig, const double* ubody,
@@ -563,6 +668,11 @@ static void bce_extrapolate(const oc_sim* s, const structure_t* st, const double
   #pragma omp parallel for schedule(dynamic, 256)
   for (int64_t a = 0; a < s->n; ++a) {
     if (s->kind[a] != OC_BCE) continue;
+    if (inactive(st, a)) {   /* Alg. 3: "their states are not updated" */
+      for (int c = 0; c < 3; ++c) u_out[3 * a + c] = u[3 * a + c];
+      for (int c = 0; c < 6; ++c) sig_out[6 * a + c] = sig[6 * a + c];
+      continue;
+    }
     double SW = 0.0, su[3] = {0, 0, 0}, ss[6] = {0, 0, 0, 0, 0, 0}, sh = 0.0;
     for (int64_t k = st->offset[a]; k < st->offset[a + 1]; ++k) {
       const int64_t f = st->list[k];
@@ -610,6 +720,7 @@ static void rates(const oc_sim* s, const structure_t* st, const double* x, const
     for (int c = 0; c < 10; ++c) o[c] = 0.0;
     const int is_fluid = s->kind[i] == OC_FLUID;
     if (!is_fluid && (s->body[i] <= 0 || s->bodies[s->body[i]].b.motion == OC_BODY_FIXED)) continue;
+    if (inactive(st, i)) continue;                                    /* Alg. 3: no RHS */
     double L[9] = {0}, cont = 0.0, mom[3] = {0, 0, 0}, Pi[3] = {0, 0, 0};
     for (int64_t k = st->offset[i]; k < st->offset[i + 1]; ++k) {
       const int64_t j = st->list[k];
@@ -680,7 +791,8 @@ static int step_once(oc_sim* s, double dt) {
     } else {
       free_structure(kept);
     }
-    if ((rc = build_structure(s, s->x, kept, 1)) != OC_OK) {
+    /* Alg. 3 steps 1–3: flags from the active boxes at t_n, refreshed with the lists (A30) */
+    if ((rc = build_structure(s, s->x, kept, 1, compute_activity(s))) != OC_OK) {
       free(kept);
       s->kept = NULL;
       return rc;
@@ -761,7 +873,7 @@ static int step_once(oc_sim* s, double dt) {
   /* ---- y_{n+1} = y_n + dt f(t_n + dt/2, y_mid), then the return map on sigma* ---- */
   #pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < n; ++i) {
-    if (s->kind[i] != OC_FLUID) continue;
+    if (s->kind[i] != OC_FLUID || inactive(&st, i)) continue;   /* Inactive: frozen (Alg. 3) */
     const double* f = &s->rates[1][10 * i];
     double sig_star[6], sig_new[6];
     for (int c = 0; c < 3; ++c) {
@@ -816,6 +928,7 @@ static int step_once(oc_sim* s, double dt) {
       marker_kinematics(s, poses, i, &s->x[3 * i], ubb, abb);
     }
   s->steps_done++;
+  s->time += dt;
   rc = check_finite(s);
 done:
   free(xm); free(um); free(rm); free(sm); free(ub); free(ab);

@@ -98,6 +98,23 @@ int  oc_neighbors(oc_sim* s, int64_t* offsets /*n+1*/, int64_t* list /*may be NU
 int  oc_last_rates(const oc_sim* s, int stage, double* drho, double* acc, double* dsig6);
 /* extrapolated BCE velocity/stress of the last step's stage (marker rows only meaningful) */
 int  oc_last_bce(const oc_sim* s, int stage, double* vel, double* sig6);
+
+/* ---- active domains (Alg. 3; readings A29–A31) ---- */
+enum { OC_ACTIVE = 0, OC_EXTENDED = 1, OC_INACTIVE = 2 };
+enum { OC_CAP_KEEP = 0, OC_CAP_GROW = 1, OC_CAP_SHRINK = 2 };
+/* UpdateActivity for one point: Active inside the box (body frame, |x_local| <= half), Extended-Active
+ * outside every box but closer than `radius` (= 2h) to one, else Inactive (Fig. active_domain).
+ * box_pos/box_R/box_half: nbox boxes (3, 9 row-major body->world, 3 doubles each). */
+int  oc_activity(const double x[3], int nbox, const double* box_pos, const double* box_R,
+                 const double* box_half, double radius);
+/* ManageArrayMemory policy: returns the new capacity and the action taken */
+int64_t oc_manage_capacity(int64_t capacity, int64_t required, int64_t step, double growth,
+                           double shrink, int shrink_interval, int* action);
+/* an active box of half extents half[3] at the local origin of `body` (before the first step) */
+int  oc_set_active_box(oc_sim* s, int32_t body, const double half[3]);
+int  oc_set_active_delay(oc_sim* s, double t_delay);
+/* activity flags (by id) of the last list rebuild; all OC_ACTIVE while the feature is off */
+int  oc_get_activity(const oc_sim* s, uint8_t* flags);
 const char* oc_last_error(const oc_sim* s);
 int  oc_num_threads(void);
 

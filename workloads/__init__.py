@@ -126,6 +126,9 @@ class Scenario:
     dt: float
     steps: int
     meta: dict = field(default_factory=dict)
+    # active domains (Alg. 3): {"boxes": {body index: half extents}, "t_delay": s}; body 0 = walls,
+    # body k = bodies[k - 1]
+    active: dict = field(default_factory=dict)
 
     @property
     def n_fluid(self) -> int:
