@@ -177,6 +177,37 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ our arm
+def active_measure(crm, torch, local, warmup, steps):
+    """ms/step of the MGRU3 wheel bin with and without active domains (same input, same steps)."""
+    out = {"workload": "mgru3_wheel", "active_box_m": [0.6, 0.6, 0.8], "steps": steps}
+    for on in (False, True):
+        sc = workloads.mgru3_wheel(active=on)
+        g = crm.load_scenario(sc, device=local)
+        st = torch.cuda.ExternalStream(g.stream(), device=local)
+        g.step(sc.dt, warmup)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        g.step(sc.dt, steps)
+        e1.record(st)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        key = "on" if on else "off"
+        out[f"ms_per_step_{key}"] = ms
+        if on:
+            s = g.active_stats()
+            out.update(n_total=g.count(), n_active=s["active"], n_extended=s["extended"],
+                       n_inactive=s["inactive"], capacity=s["capacity"])
+        else:
+            out["n_fluid"] = sc.n_fluid
+        g.close()
+    out["speedup"] = out["ms_per_step_off"] / out["ms_per_step_on"]
+    out["note"] = ("Alg. 3 (P:876-947): UpdateActivity + compaction + ManageArrayMemory each rebuild, "
+                   "ps_freq = 1; paper Table tab:active_domains_performance: MGRU3 wheel 2.93x, "
+                   "RASSOR drum 2.11x (whole co-simulation RTF, its hardware)")
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -350,6 +381,12 @@ def main():
                "note": "Alg. 2 persistent lists (P:770-806): rebuild every 10 steps; paper: 1.28-1.36x (P:866)"}
         g10.close()
 
+    # active domains (Alg. 3) on the MGRU3 wheel bin (1M particles, the
+    # paper's 0.6 x 0.6 x 0.8 m active box around a prescribed rolling wheel), on vs off
+    nxt_active = None
+    if not args.no_next and world == 1 and rank == 0:
+        nxt_active = active_measure(crm, torch, local, args.warmup, max(10, args.steps))
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = oracle_rate(args.config, 12)
@@ -364,7 +401,7 @@ def main():
                            "l2": "inputs larger than L2 (56 B x N state >> 126 MB), no flush",
                            "parallelism": f"x-slabs x{world}, NCCL ghost planes" if world > 1 else "single GPU"},
                 "roofline": roof, "hbm_roofline": hbm, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": launches, "clocks": clocks, "next_alg2": nxt}
+                "gpu_launches": launches, "clocks": clocks, "next_alg2": nxt, "next_active": nxt_active}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()

@@ -151,6 +151,32 @@ int  crm_nccl_unique_id(void* out128);
  * nplanes < world * align. */
 int  crm_slab_partition(const int64_t* plane_counts, int nplanes, int world, int align, int* bounds);
 
+/* ---- active domains (Alg. 3; readings A29–A31) ----
+ * An "active box" is an oriented box of half extents half_extents[3] (m, body frame) at the local
+ * origin of `body`, moving with it (body 0 = the fixed container frame).  After t_delay
+ * (Alg. 3 "if t > t_delay"), at every neighbour-list rebuild (Alg. 2 period), each particle is
+ * flagged: Active inside a box, Extended-Active outside every box but closer than 2h to
+ * one, Inactive otherwise; markers of moving bodies are always Active.  Inactive particles take
+ * no part in the neighbour search, their state is frozen (crm_get_state still returns it) and the
+ * arrays indexed by the active set (neighbour lists, mid-step state) are sized by the
+ * ManageArrayMemory policy (growth G, shrink threshold S every S_I steps).  Single-GPU only
+ * (CRM_E_UNSUPPORTED with world > 1); set before the first step (CRM_E_STATE after). */
+typedef struct {
+  double t_delay;        /* s; culling starts once t > t_delay (default 0) */
+  double growth;         /* G; 0 -> 1.2 */
+  double shrink;         /* S; 0 -> 0.75 */
+  int    shrink_interval;/* S_I steps; 0 -> 50 */
+} crm_active_t;
+int  crm_set_active_box(crm_t* ctx, int32_t body, const double half_extents[3]);
+int  crm_set_active_policy(crm_t* ctx, const crm_active_t* policy);
+/* out = {N_active, N_extended, N_inactive, N_{a+e}, capacity, last action (0 keep, 1 grow,
+ * 2 shrink)} of the last rebuild. */
+int  crm_active_stats(const crm_t* ctx, int64_t out[6]);
+/* Pure host helper, the ManageArrayMemory policy: new capacity for `required` elements at step
+ * `step`; *action = 0 keep, 1 grow (to ceil(required * growth)), 2 shrink (to required). */
+int64_t crm_manage_capacity(int64_t capacity, int64_t required, int64_t step, double growth, double shrink,
+                            int shrink_interval, int* action);
+
 /* Copy state of ids [first_id, first_id + count) to host fp64 arrays (any pointer may be NULL).
  * For markers: the last extrapolated u and sigma, rho = rho0. */
 int  crm_get_state(crm_t* ctx, int64_t first_id, int64_t count, double* pos, double* vel,
@@ -196,6 +222,9 @@ int  crm_debug_neighbors(crm_t* ctx, int64_t* offsets, int64_t* list /* NULL = c
 int  crm_debug_rates(crm_t* ctx, int stage, double* drho, double* acc, double* dsig6);
 /* Extrapolated marker velocity and stress of the last armed step's stage, by id. */
 int  crm_debug_bce(crm_t* ctx, int stage, double* vel, double* sig6);
+/* Activity flags (0 Active, 1 Extended-Active, 2 Inactive) by id of the last rebuild; all 0 while
+ * active domains are off or before t_delay. */
+int  crm_debug_activity(crm_t* ctx, uint8_t* flags_by_id);
 
 #ifdef __cplusplus
 }

@@ -25,7 +25,8 @@ EXPORTS = [
     "crm_stream", "crm_launch_count", "crm_profile_enable", "crm_profile_read", "crm_profile_reset",
     "crm_kernel_name", "crm_set_graphs", "crm_debug_arm", "crm_debug_structure", "crm_debug_neighbors",
     "crm_debug_rates", "crm_debug_bce", "crm_group_step", "crm_nccl_unique_id", "crm_slab_partition",
-    "crm_pair_count",
+    "crm_pair_count", "crm_set_active_box", "crm_set_active_policy", "crm_active_stats", "crm_manage_capacity",
+    "crm_debug_activity",
 ]
 
 
@@ -48,6 +49,11 @@ class Boundary(C.Structure):
 class Dist(C.Structure):
     _fields_ = [("rank", C.c_int), ("world", C.c_int), ("device", C.c_int), ("nccl_id", C.c_void_p),
                 ("cuda_stream", C.c_void_p)]
+
+
+class ActiveT(C.Structure):
+    _fields_ = [("t_delay", C.c_double), ("growth", C.c_double), ("shrink", C.c_double),
+                ("shrink_interval", C.c_int)]
 
 
 class BodyT(C.Structure):
@@ -100,8 +106,23 @@ def load_library(path: str = LIB_PATH):
     L.crm_nccl_unique_id.argtypes = [C.c_void_p]
     L.crm_slab_partition.argtypes = [_I64, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int)]
     L.crm_pair_count.argtypes = [vp, _I64]
+    L.crm_set_active_box.argtypes = [vp, C.c_int32, _D]
+    L.crm_set_active_policy.argtypes = [vp, C.POINTER(ActiveT)]
+    L.crm_active_stats.argtypes = [vp, _I64]
+    L.crm_manage_capacity.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_int,
+                                      C.POINTER(C.c_int)]
+    L.crm_manage_capacity.restype = C.c_int64
+    L.crm_debug_activity.argtypes = [vp, C.POINTER(C.c_uint8)]
     _lib = L
     return L
+
+
+def manage_capacity(capacity: int, required: int, step: int, growth=1.2, shrink=0.75, interval=50):
+    """ManageArrayMemory policy of Alg. 3 (host function of libcrm.so): (new capacity, action)."""
+    a = C.c_int(0)
+    cap = load_library().crm_manage_capacity(int(capacity), int(required), int(step), float(growth),
+                                             float(shrink), int(interval), C.byref(a))
+    return int(cap), int(a.value)
 
 
 def nccl_unique_id() -> bytes:
@@ -316,6 +337,27 @@ class Crm:
         self._chk(self._L.crm_debug_bce(self.h, stage, _p(vel), _p(sig)), "crm_debug_bce")
         return vel, sig
 
+    # ---- active domains (Alg. 3)
+    def set_active_box(self, body: int, half):
+        h = _d(half, (3,))
+        self._chk(self._L.crm_set_active_box(self.h, int(body), _p(h)), "crm_set_active_box")
+
+    def set_active_policy(self, t_delay: float = 0.0, growth: float = 0.0, shrink: float = 0.0,
+                          interval: int = 0):
+        a = ActiveT(float(t_delay), float(growth), float(shrink), int(interval))
+        self._chk(self._L.crm_set_active_policy(self.h, C.byref(a)), "crm_set_active_policy")
+
+    def active_stats(self) -> dict:
+        out = np.zeros(6, np.int64)
+        self._chk(self._L.crm_active_stats(self.h, _p(out, _I64)), "crm_active_stats")
+        keys = ("active", "extended", "inactive", "n_ae", "capacity", "action")
+        return {k: int(v) for k, v in zip(keys, out)}
+
+    def activity(self) -> np.ndarray:
+        f = np.zeros(self.count(), np.uint8)
+        self._chk(self._L.crm_debug_activity(self.h, f.ctypes.data_as(C.POINTER(C.c_uint8))), "crm_debug_activity")
+        return f
+
 
 def load_scenario(sc, **kw) -> Crm:
     """Build a Crm from a workloads.Scenario: fluid first, then walls (body 0), then bodies."""
@@ -326,4 +368,9 @@ def load_scenario(sc, **kw) -> Crm:
     for b in sc.bodies:
         bid = s.add_body(b)
         s.add_bce(bid, b.markers)
+    act = getattr(sc, "active", None) or {}
+    for body, half in act.get("boxes", {}).items():
+        s.set_active_box(body, half)
+    if "t_delay" in act or "policy" in act:
+        s.set_active_policy(act.get("t_delay", 0.0), *act.get("policy", ()))
     return s

@@ -14,6 +14,7 @@
 #include "physics.cuh"
 #include "structure.cuh"
 #include "tiled.cuh"
+#include "active.cuh"
 
 using namespace crmk;
 
@@ -22,12 +23,12 @@ namespace {
 enum KernelId {
   KID_MARKERS = 0, KID_BIN, KID_SCAN, KID_SCAN_ADD, KID_SCATTER, KID_REORDER,
   KID_BCE_A, KID_RATES_A, KID_BCE_B, KID_RATES_B, KID_BODY, KID_POSES, KID_STATE, KID_COPY, KID_DECODE,
-  KID_SLAB, KID_COUNT
+  KID_SLAB, KID_ACTIVITY, KID_COUNT
 };
 const char* kKernelNames[KID_COUNT] = {"k_markers_place", "k_bin", "k_scan_tiles", "k_scan_add", "k_scatter",
                                        "k_reorder", "k_bce_A", "k_rates_A", "k_bce_B", "k_rates_B",
                                        "k_body_update", "k_body_poses", "k_get_set_state", "k_copy_u32",
-                                       "k_decode_lists", "k_slab_util"};
+                                       "k_decode_lists", "k_slab_util", "k_activity"};
 
 struct ProfRec {
   int kid;
@@ -125,6 +126,23 @@ struct crm {
   uint32_t s_lo = 0, s_lo1 = 0, s_hi1 = 0, s_hi = 0;   // starts of planes x_lo, x_lo+1, x_hi-1, x_hi
   uint32_t s_lom1 = 0, s_hip1 = 0;                     // starts of planes x_lo-1 and x_hi+1 (ghost ranges)
   uint32_t mig_l = 0, mig_r = 0, rcv_l = 0, rcv_r = 0, gh_l = 0, gh_r = 0, n_app = 0;
+
+  // active domains (Alg. 3): boxes per body, the active-set capacity of
+  // the arrays indexed by sorted slot (lists, mid state, marker loads) and its ManageArrayMemory policy
+  std::vector<ActiveBox> boxes;
+  ActiveBox* d_boxes = nullptr;
+  double t_delay = 0.0, growth = 1.2, shrink = 0.75;
+  int shrink_interval = 50;
+  double t_now = 0.0;                    // sum of the step sizes taken (compared with t_delay)
+  bool active_on = false;                // the last rebuild culled inactive particles
+  int64_t acap = 0;                      // capacity of the active-set arrays (slots)
+  int64_t n_ae = 0, n_act = 0, n_ext = 0, n_inact = 0;
+  int last_action = 0;                   // 0 keep, 1 grow, 2 shrink (crm_manage_capacity)
+  uint8_t *d_act = nullptr, *d_act_id = nullptr;   // flags by pre-sort slot / by id
+  unsigned long long* d_actcnt = nullptr;
+  uint32_t *d_tile_list = nullptr, *d_tile_cnt = nullptr;   // non-empty tiles (kernels launch over them)
+  long long n_tiles_act = 0;
+  bool acap_async = false;               // active-set arrays come from the stream-ordered allocator
 
   // profiling
   bool prof = false;

@@ -104,6 +104,18 @@ int commit(crm_t* c) {
   r |= dalloc(c, &c->list, n * (size_t)c->cap); r |= dalloc(c, &c->nlist, n); r |= dalloc(c, &c->count_all, n);
   r |= dalloc(c, &c->d_err, 1);
   r |= dalloc(c, &c->d_xcount, 8);
+  c->acap = (int64_t)n;
+  if (!c->boxes.empty()) {   // active domains (Alg. 3)
+    r |= dalloc(c, &c->d_boxes, c->boxes.size());
+    r |= dalloc(c, &c->d_act, n); r |= dalloc(c, &c->d_act_id, (size_t)c->n);
+    r |= dalloc(c, &c->d_actcnt, 3);
+    r |= dalloc(c, &c->d_tile_list, (size_t)num_tiles(c->grid)); r |= dalloc(c, &c->d_tile_cnt, 1);
+    if (!r) {
+      CK(cudaMemcpyAsync(c->d_boxes, c->boxes.data(), c->boxes.size() * sizeof(ActiveBox), cudaMemcpyHostToDevice,
+                         c->stream));
+      CK(cudaMemsetAsync(c->d_act_id, 0, (size_t)c->n, c->stream));
+    }
+  }
   if (r) return CRM_E_OOM;
   // tiles over the owned planes
   {
@@ -220,14 +232,33 @@ int commit(crm_t* c) {
 namespace {
 
 // sort phase on the local particles: bin, scan, scatter, reorder; particles whose tag
-// matches drop_mask leave the local set
+// matches drop_mask leave the local set.  With active domains (Alg. 3) past t_delay, UpdateActivity
+// runs first and Inactive particles go behind the active set, frozen.
 void issue_sort(crm_t* c, long long step, uint32_t drop_mask) {
   const int n = (int)c->nl;
   const int a = c->cur, b = 1 - c->cur;
+  const bool act = !c->boxes.empty() && c->t_now > c->t_delay;   // Alg. 3: "if t > t_delay"
+  c->active_on = act;
   cudaMemsetAsync(c->cell_count, 0, ((size_t)c->grid.M + 1) * 4, c->stream);
+  if (act) {
+    cudaMemsetAsync(c->d_actcnt, 0, 3 * sizeof(unsigned long long), c->stream);
+    launch(c, KID_ACTIVITY, k_activity, dim3(blocks(n, 256)), dim3(256), n, (const float4*)c->P[a],
+           (const float4*)c->L[a], (const float4*)c->U[a], (const uint32_t*)c->ids[a], (const BodyState*)c->d_bodies,
+           (const ActiveBox*)c->d_boxes, (int)c->boxes.size(), c->support * (double)c->ker.h, c->d_act, c->d_act_id,
+           c->d_actcnt);
+  }
   launch(c, KID_BIN, k_bin, dim3(blocks(n, 256)), dim3(256), n, (const float4*)c->P[a], (const float4*)c->U[a],
-         (const uint32_t*)c->ids[a], c->grid, drop_mask, c->key, c->arrival, c->cell_count, c->d_err, step);
+         (const uint32_t*)c->ids[a], c->grid, drop_mask, (const uint8_t*)(act ? c->d_act : nullptr), c->key,
+         c->arrival, c->cell_count, c->d_err, step);
   scan_u32(c, c->cell_count, c->cell_start, (long long)c->grid.M + 1, 0);
+  if (act) {   // the tiles the step's kernels run on, and the counts the host sizes arrays from
+    cudaMemsetAsync(c->d_tile_cnt, 0, 4, c->stream);
+    launch(c, KID_ACTIVITY, k_tile_list, dim3(blocks(c->ntiles, 256)), dim3(256), c->ntiles, c->tile_base, c->grid,
+           (const uint32_t*)c->cell_start, c->d_tile_list, c->d_tile_cnt);
+    cudaMemcpyAsync(c->h_pin, c->cell_start + c->grid.M, 4, cudaMemcpyDeviceToHost, c->stream);
+    cudaMemcpyAsync(c->h_pin + 1, c->d_tile_cnt, 4, cudaMemcpyDeviceToHost, c->stream);
+    cudaMemcpyAsync(c->h_pin + 8, c->d_actcnt, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream);
+  }
   launch(c, KID_SCATTER, k_scatter, dim3(blocks(n, 256)), dim3(256), n, (const uint32_t*)c->key,
          (const uint32_t*)c->arrival, (const uint32_t*)c->cell_start, (const uint32_t*)c->ids[a], c->tmp_src, c->tmp_id);
   if (c->slab)
@@ -236,27 +267,88 @@ void issue_sort(crm_t* c, long long step, uint32_t drop_mask) {
          (const uint32_t*)c->tmp_id, (const uint32_t*)c->key, (const uint32_t*)c->cell_start,
          (const float4*)c->P[a], (const float4*)c->L[a], (const float4*)c->U[a], (const float4*)c->S1[a],
          (const float2*)c->S2[a], c->P[b], c->L[b], c->U[b], c->S1[b], c->S2[b], c->ids[b], c->cell_of, c->slot_of_id,
-         c->grid.M);
+         c->grid.M, act ? 1 : 0);
   c->cur = b;
 }
 
+// the arrays indexed by sorted slot < N_{a+e}: neighbour lists, mid state, marker loads
+// (stream-ordered allocator: a resize costs no device synchronisation; the first resize returns
+// the commit-time cudaMalloc buffers)
+template <typename T>
+int aalloc(crm_t* c, T** p, size_t n) {
+  if (*p) {
+    if (c->acap_async) cudaFreeAsync(*p, c->stream);
+    else cudaFree(*p);
+  }
+  *p = nullptr;
+  return cudaMallocAsync((void**)p, n * sizeof(T), c->stream) == cudaSuccess ? 0 : 1;
+}
+
+int alloc_active_arrays(crm_t* c, int64_t cap) {
+  const size_t n = (size_t)std::max<int64_t>(cap, 1);
+  int r = 0;
+  r |= aalloc(c, &c->list, n * (size_t)c->cap); r |= aalloc(c, &c->nlist, n); r |= aalloc(c, &c->count_all, n);
+  r |= aalloc(c, &c->Pm, n); r |= aalloc(c, &c->Lm, n); r |= aalloc(c, &c->Um, n); r |= aalloc(c, &c->S1m, n);
+  r |= aalloc(c, &c->S2m, n);
+  if (c->n_moving_markers) {
+    r |= aalloc(c, &c->macc, n);
+    if (!r) cudaMemsetAsync(c->macc, 0, n * sizeof(float4), c->stream);
+  }
+  c->acap_async = true;
+  if (r) return fail(c, CRM_E_OOM, "active-set arrays");
+  c->acap = cap;
+  return CRM_OK;
+}
+
+// Alg. 3 steps 2–3 after a rebuild sort: ComputeActiveCount (read back: the host sizes the arrays)
+// and ManageArrayMemory with growth G, shrink threshold S and interval S_I
+int active_capacity(crm_t* c, long long step) {
+  unsigned long long* hc = reinterpret_cast<unsigned long long*>(c->h_pin + 8);
+  if (c->active_on) {   // the copies were queued by issue_sort right after the scan
+    CK(cudaStreamSynchronize(c->stream));
+    c->n_ae = c->h_pin[0];
+    c->n_tiles_act = c->h_pin[1];
+    c->n_act = (int64_t)hc[0]; c->n_ext = (int64_t)hc[1]; c->n_inact = (int64_t)hc[2];
+  } else {
+    c->n_ae = c->nl;
+    c->n_act = c->n_ae; c->n_ext = 0; c->n_inact = 0;
+  }
+  int action = 0;
+  const int64_t cap = manage_capacity(c->acap, c->n_ae, step, c->growth, c->shrink, c->shrink_interval, &action);
+  c->last_action = action;
+  if (cap != c->acap) return alloc_active_arrays(c, cap);
+  return CRM_OK;
+}
+
+// the rebuild sort of a single-GPU step (+ the active-set bookkeeping of Alg. 3)
+int issue_rebuild_sort(crm_t* c, long long step) {
+  issue_sort(c, step, 0);
+  if (!c->boxes.empty()) return active_capacity(c, step);
+  return CRM_OK;
+}
+
 // BCE extrapolation: stage 0 at y_n (with the marker filter), stage 1 at y_mid
+// the tile grid of a step: every tile, or (active domains) the non-empty ones listed by k_tile_list
+inline long long tile_grid(const crm_t* c) { return c->active_on ? c->n_tiles_act : c->ntiles; }
+inline const uint32_t* tile_list(const crm_t* c) { return c->active_on ? c->d_tile_list : nullptr; }
+
 template <int KER>
 void issue_bce_k(crm_t* c, int stage, long long step, int store_all) {
   const int y = c->cur;
   const int dbg = c->dbg_on ? 1 : 0;
-  const dim3 tg((unsigned)c->ntiles), tb(TILE_THREADS);
+  if (tile_grid(c) == 0) return;
+  const dim3 tg((unsigned)tile_grid(c)), tb(TILE_THREADS);
   const size_t sm = sizeof(TileSmem);
   if (stage == 0)
     launch_smem(c, KID_BCE_A, k_bce_t<0, KER>, tg, tb, sm, c->grid, c->ph, (const uint32_t*)c->cell_start,
                 (const float4*)c->P[y], (const float4*)c->L[y], c->U[y], c->S1[y], c->S2[y], c->list, c->nlist,
                 c->count_all, (const uint32_t*)c->cell_of, (const Pose*)c->d_pose0, c->cap, store_all, c->dbg, dbg,
-                c->d_err, (const uint32_t*)c->ids[y], step, c->tile_base);
+                c->d_err, (const uint32_t*)c->ids[y], step, c->tile_base, tile_list(c));
   else
     launch_smem(c, KID_BCE_B, k_bce_t<1, KER>, tg, tb, sm, c->grid, c->ph, (const uint32_t*)c->cell_start,
                 (const float4*)c->Pm, (const float4*)c->Lm, c->Um, c->S1m, c->S2m, c->list, c->nlist,
                 c->count_all, (const uint32_t*)c->cell_of, (const Pose*)c->d_posem, c->cap, 0, c->dbg, dbg,
-                c->d_err, (const uint32_t*)c->ids[y], step, c->tile_base);
+                c->d_err, (const uint32_t*)c->ids[y], step, c->tile_base, tile_list(c));
 }
 
 void issue_bce(crm_t* c, int stage, float dt, long long step, int store_all) {
@@ -271,20 +363,21 @@ template <int KER>
 void issue_rates_k(crm_t* c, int stage, float dt, long long step) {
   const int y = c->cur;
   const int dbg = c->dbg_on ? 1 : 0;
-  const dim3 tg((unsigned)c->ntiles), tb(TILE_THREADS);
+  if (tile_grid(c) == 0) return;
+  const dim3 tg((unsigned)tile_grid(c)), tb(TILE_THREADS);
   const size_t sm = sizeof(TileSmem);
   if (stage == 0)
     launch_smem(c, KID_RATES_A, k_rates_t<0, KER>, tg, tb, sm, c->grid, c->ph, dt, (const uint32_t*)c->cell_start,
                 (const float4*)c->P[y], (const float4*)c->L[y], (const float4*)c->U[y], (const float4*)c->S1[y],
                 (const float2*)c->S2[y], c->Pm, c->Lm, c->Um, c->S1m, c->S2m, c->list, c->nlist, c->count_all,
                 (const uint32_t*)c->cell_of, c->cap, c->macc, c->dbg, dbg, c->d_err, (const uint32_t*)c->ids[y], step,
-                c->tile_base);
+                c->tile_base, tile_list(c));
   else
     launch_smem(c, KID_RATES_B, k_rates_t<1, KER>, tg, tb, sm, c->grid, c->ph, dt, (const uint32_t*)c->cell_start,
                 (const float4*)c->Pm, (const float4*)c->Lm, (const float4*)c->Um, (const float4*)c->S1m,
                 (const float2*)c->S2m, c->P[y], c->L[y], c->U[y], c->S1[y], c->S2[y], c->list, c->nlist, c->count_all,
                 (const uint32_t*)c->cell_of, c->cap, c->macc, c->dbg, dbg, c->d_err, (const uint32_t*)c->ids[y], step,
-                c->tile_base);
+                c->tile_base, tile_list(c));
 }
 
 void issue_rates(crm_t* c, int stage, float dt, long long step) {
@@ -293,11 +386,14 @@ void issue_rates(crm_t* c, int stage, float dt, long long step) {
 }
 
 // one RK2 step on one GPU (everything on the stream, no host sync)
-void issue_step(crm_t* c, float dt, long long step) {
+int issue_step(crm_t* c, float dt, long long step) {
   // Alg. 2: rebuild (sort + filtered lists) when t mod ps_freq == 0; otherwise the particles keep
   // their slots and the stored lists are reused without a distance re-check (A17)
   const bool rebuild = !c->lists_valid || (step % c->ps_freq) == 0;
-  if (rebuild) issue_sort(c, step, 0);
+  if (rebuild) {
+    const int r = issue_rebuild_sort(c, step);
+    if (r) return r;
+  }
   c->ph.build_lists = rebuild ? 1 : 0;
   c->lists_valid = true;
   issue_bce(c, 0, dt, step, 0);
@@ -320,6 +416,7 @@ void issue_step(crm_t* c, float dt, long long step) {
            (const Pose*)c->d_pose0, c->P[y], c->L[y], (const float4*)c->U[y]);
   }
   if (c->dbg_on) cudaMemcpyAsync(c->dbg_ids, c->ids[y], (size_t)c->nl * 4, cudaMemcpyDeviceToDevice, c->stream);
+  return CRM_OK;
 }
 
 // One single-GPU step, replayed from a CUDA graph when possible.  The launch sequence of a step
@@ -328,10 +425,8 @@ void issue_step(crm_t* c, float dt, long long step) {
 // inside a replayed step report step -1 (the host message names the crm_step call instead).
 int run_step(crm_t* c, float dt, long long step) {
   const bool rebuild = !c->lists_valid || (step % c->ps_freq) == 0;
-  if (!c->graphs || c->prof || c->dbg_on) {
-    issue_step(c, dt, step);
-    return CRM_OK;
-  }
+  // (active domains resize arrays between steps from host-read counts: launched one by one)
+  if (!c->graphs || c->prof || c->dbg_on || !c->boxes.empty()) return issue_step(c, dt, step);
   const int p = c->cur, q = rebuild ? 1 : 0;
   if (!c->gexec[p][q] || c->gdt[p][q] != dt) {
     if (c->gexec[p][q]) cudaGraphExecDestroy(c->gexec[p][q]);
@@ -341,8 +436,9 @@ int run_step(crm_t* c, float dt, long long step) {
     c->lists_valid = !rebuild;   // make issue_step take the same branch as the key
     cudaGraph_t graph;
     CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-    issue_step(c, dt, -1);
+    const int rs = issue_step(c, dt, -1);
     CK(cudaStreamEndCapture(c->stream, &graph));
+    if (rs) return rs;
     cudaError_t e = cudaGraphInstantiate(&c->gexec[p][q], graph, 0);
     cudaGraphDestroy(graph);
     if (e != cudaSuccess) return fail(c, CRM_E_CUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(e));
@@ -583,6 +679,8 @@ void crm_destroy(crm_t* c) {
     cudaFree(c->dbg.bu[b]); cudaFree(c->dbg.bs1[b]); cudaFree(c->dbg.bs2[b]);
   }
   cudaFree(c->Pm); cudaFree(c->Lm); cudaFree(c->Um); cudaFree(c->S1m); cudaFree(c->S2m);
+  cudaFree(c->d_boxes); cudaFree(c->d_act); cudaFree(c->d_act_id); cudaFree(c->d_actcnt);
+  cudaFree(c->d_tile_list); cudaFree(c->d_tile_cnt);
   cudaFree(c->key); cudaFree(c->arrival); cudaFree(c->cell_count); cudaFree(c->cell_start);
   cudaFree(c->tmp_src); cudaFree(c->tmp_id); cudaFree(c->cell_of); cudaFree(c->slot_of_id);
   cudaFree(c->list); cudaFree(c->nlist); cudaFree(c->count_all); cudaFree(c->list32);
@@ -734,6 +832,7 @@ int crm_step(crm_t* c, double dt, int64_t nsteps) {
     const long long step = (long long)(c->steps_done + s);
     if (!c->slab) {
       if ((r = run_step(c, (float)dt, step))) return r;
+      c->t_now += dt;
       continue;
     }
     for (int k = 0; k < kSlabPhases; ++k) {
@@ -761,13 +860,14 @@ int crm_group_step(crm_t** cs, int world, double dt, int64_t nsteps) {
       for (int a = 0; a < world; ++a) {
         const long long step = (long long)(cs[a]->steps_done + s);
         if (world == 1) {
-          if (k == 0) issue_step(cs[a], (float)dt, step);
+          if (k == 0 && (r = issue_step(cs[a], (float)dt, step))) return r;
           continue;
         }
         if ((r = slab_phase(cs[a], k, (float)dt, step))) return r;
       }
       if (world > 1 && (r = loopback_flush(cs, world))) return r;
     }
+    for (int a = 0; a < world; ++a) cs[a]->t_now += dt;
   }
   for (int a = 0; a < world; ++a)
     if ((r = end_steps(cs[a], nsteps))) return r;
@@ -790,14 +890,66 @@ int crm_pair_count(crm_t* c, int64_t* fluid_pairs) {
   unsigned long long* d = nullptr;
   CK(cudaMalloc(&d, 8));
   CK(cudaMemsetAsync(d, 0, 8, c->stream));
-  const int n = (int)c->nl;
-  launch(c, KID_SLAB, k_pair_count, dim3(blocks(n, 256)), dim3(256), n, (const float4*)c->U[c->cur],
-         (const uint32_t*)c->count_all, d);
+  const int n = (int)(c->boxes.empty() ? c->nl : c->n_ae);   // slots that have lists
+  if (n > 0)
+    launch(c, KID_SLAB, k_pair_count, dim3(blocks(n, 256)), dim3(256), n, (const float4*)c->U[c->cur],
+           (const uint32_t*)c->count_all, d);
   unsigned long long h = 0;
   CK(cudaMemcpyAsync(&h, d, 8, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   cudaFree(d);
   *fluid_pairs = (int64_t)h;
+  return CRM_OK;
+}
+
+// ---- active domains (Alg. 3) -------------------------------------------------------------
+int crm_set_active_box(crm_t* c, int32_t body, const double half_extents[3]) {
+  if (!c || !half_extents) return CRM_E_INVALID;
+  if (c->committed) return fail(c, CRM_E_STATE, "active boxes are set before the first step");
+  if (body < 0 || body >= (int32_t)c->bodies.size()) return fail(c, CRM_E_INVALID, "bad body");
+  if (c->world > 1) return fail(c, CRM_E_UNSUPPORTED, "active domains are single-GPU in this build");
+  for (int a = 0; a < 3; ++a)
+    if (!(half_extents[a] >= 0.0)) return fail(c, CRM_E_INVALID, "half extents must be >= 0");
+  ActiveBox bx{};
+  for (int a = 0; a < 3; ++a) bx.half[a] = half_extents[a];
+  bx.body = body;
+  for (auto& e : c->boxes)
+    if (e.body == body) { e = bx; return CRM_OK; }
+  c->boxes.push_back(bx);
+  return CRM_OK;
+}
+
+int crm_set_active_policy(crm_t* c, const crm_active_t* p) {
+  if (!c || !p) return CRM_E_INVALID;
+  if (p->growth < 0 || (p->growth > 0 && p->growth < 1.0) || p->shrink < 0 || p->shrink > 1 || p->shrink_interval < 0)
+    return fail(c, CRM_E_INVALID, "growth >= 1, 0 <= shrink <= 1, shrink_interval >= 0");
+  c->t_delay = p->t_delay;
+  c->growth = p->growth > 0 ? p->growth : 1.2;
+  c->shrink = p->shrink > 0 ? p->shrink : 0.75;
+  c->shrink_interval = p->shrink_interval > 0 ? p->shrink_interval : 50;
+  return CRM_OK;
+}
+
+int crm_active_stats(const crm_t* c, int64_t out[6]) {
+  if (!c || !out) return CRM_E_INVALID;
+  out[0] = c->n_act; out[1] = c->n_ext; out[2] = c->n_inact;
+  out[3] = c->n_ae; out[4] = c->acap; out[5] = c->last_action;
+  return CRM_OK;
+}
+
+int64_t crm_manage_capacity(int64_t capacity, int64_t required, int64_t step, double growth, double shrink,
+                            int shrink_interval, int* action) {
+  return manage_capacity(capacity, required, step, growth, shrink, shrink_interval, action);
+}
+
+int crm_debug_activity(crm_t* c, uint8_t* flags_by_id) {
+  if (!c || !flags_by_id) return CRM_E_INVALID;
+  if (!c->committed || !c->active_on) {
+    std::memset(flags_by_id, 0, (size_t)c->n);
+    return CRM_OK;
+  }
+  CK(cudaMemcpyAsync(flags_by_id, c->d_act_id, (size_t)c->n, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
   return CRM_OK;
 }
 
@@ -896,7 +1048,7 @@ int crm_debug_structure(crm_t* c, uint32_t* cell_by_id, int64_t* sorted_ids, uin
   if (r) return r;
   if (n_cells) *n_cells = c->grid.M;
   if (!cell_by_id && !sorted_ids && !nbr_count_by_id && !cell_start) return CRM_OK;
-  issue_sort(c, c->steps_done, 0);
+  if ((r = issue_rebuild_sort(c, c->steps_done))) return r;
   c->ph.build_lists = 1;
   c->lists_valid = true;
   issue_bce(c, 0, 0.0f, c->steps_done, 0);
@@ -904,10 +1056,12 @@ int crm_debug_structure(crm_t* c, uint32_t* cell_by_id, int64_t* sorted_ids, uin
   r = read_latch(c);
   if (r) return r;
   const size_t n = (size_t)c->n;
-  std::vector<uint32_t> ids(n), cell(n), cnt(n);
+  // with active domains only the active prefix has lists; Inactive particles have no neighbours
+  const size_t nv = c->boxes.empty() ? n : (size_t)c->n_ae;
+  std::vector<uint32_t> ids(n), cell(n), cnt(n, 0u);
   CK(cudaMemcpy(ids.data(), c->ids[c->cur], n * 4, cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(cell.data(), c->cell_of, n * 4, cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(cnt.data(), c->count_all, n * 4, cudaMemcpyDeviceToHost));
+  if (nv) CK(cudaMemcpy(cnt.data(), c->count_all, nv * 4, cudaMemcpyDeviceToHost));
   for (size_t s = 0; s < n; ++s) {
     if (cell_by_id) cell_by_id[ids[s]] = cell[s];
     if (sorted_ids) sorted_ids[s] = ids[s];
@@ -923,32 +1077,34 @@ int crm_debug_neighbors(crm_t* c, int64_t* offsets, int64_t* list) {
   cudaSetDevice(c->device);
   int r = commit(c);
   if (r) return r;
-  issue_sort(c, c->steps_done, 0);
+  if ((r = issue_rebuild_sort(c, c->steps_done))) return r;
   c->ph.build_lists = 1;
   c->lists_valid = true;
   issue_bce(c, 0, 0.0f, c->steps_done, 1);
   issue_rates(c, 0, 0.0f, c->steps_done);
   const size_t n = (size_t)c->n;
+  const size_t nv = c->boxes.empty() ? n : (size_t)c->n_ae;   // slots that have lists (Alg. 3)
   if (!c->list32 && dalloc(c, &c->list32, n * (size_t)c->cap)) return CRM_E_OOM;
-  launch(c, KID_DECODE, k_decode_lists, dim3(blocks((long long)n, 256)), dim3(256), (int)n, c->grid,
-         (const uint32_t*)c->cell_start, (const uint32_t*)c->cell_of, (const uint16_t*)c->list,
-         (const uint32_t*)c->nlist, c->cap, c->list32, c->tmp_id /* decoded counts (scratch) */);
+  if (nv)
+    launch(c, KID_DECODE, k_decode_lists, dim3(blocks((long long)nv, 256)), dim3(256), (int)nv, c->grid,
+           (const uint32_t*)c->cell_start, (const uint32_t*)c->cell_of, (const uint16_t*)c->list,
+           (const uint32_t*)c->nlist, c->cap, c->list32, c->tmp_id /* decoded counts (scratch) */);
   r = read_latch(c);
   if (r) return r;
-  std::vector<uint32_t> ids(n), nl(n);
+  std::vector<uint32_t> ids(n), nl(n, 0u);
   CK(cudaMemcpy(ids.data(), c->ids[c->cur], n * 4, cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(nl.data(), c->tmp_id, n * 4, cudaMemcpyDeviceToHost));
+  if (nv) CK(cudaMemcpy(nl.data(), c->tmp_id, nv * 4, cudaMemcpyDeviceToHost));
   std::vector<uint32_t> cnt_by_id(n);
   for (size_t s = 0; s < n; ++s) cnt_by_id[ids[s]] = nl[s];
   offsets[0] = 0;
   for (size_t i = 0; i < n; ++i) offsets[i + 1] = offsets[i] + cnt_by_id[i];
   if (!list) return CRM_OK;
-  std::vector<uint32_t> L(n * (size_t)c->cap);
-  CK(cudaMemcpy(L.data(), c->list32, L.size() * 4, cudaMemcpyDeviceToHost));
-  for (size_t s = 0; s < n; ++s) {
+  std::vector<uint32_t> L(nv * (size_t)c->cap);
+  if (nv) CK(cudaMemcpy(L.data(), c->list32, L.size() * 4, cudaMemcpyDeviceToHost));
+  for (size_t s = 0; s < nv; ++s) {
     const uint32_t id = ids[s];
     int64_t* row = list + offsets[id];
-    for (uint32_t k = 0; k < nl[s]; ++k) row[k] = ids[L[(size_t)k * n + s]];
+    for (uint32_t k = 0; k < nl[s]; ++k) row[k] = ids[L[(size_t)k * nv + s]];
     std::sort(row, row + nl[s]);
   }
   return CRM_OK;

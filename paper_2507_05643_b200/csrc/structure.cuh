@@ -52,13 +52,15 @@ __global__ void k_markers_place(int nm, const uint32_t* __restrict__ moving_ids,
 // hash + per-cell count; the error latch reports particles outside the grid.
 // Particles whose tag has a bit of drop_mask (multi-GPU ghosts / emigrants) get the sentinel key
 // M: they sort behind every cell and are not kept.
+// Inactive particles of Alg. 3 (act[i] == 2, act may be NULL) get the sentinel key too; k_reorder
+// keeps them (keep_tail) behind the active set instead of dropping them.
 __global__ void k_bin(int n, const float4* __restrict__ P, const float4* __restrict__ U,
-                      const uint32_t* __restrict__ ids, Grid g, uint32_t drop_mask, uint32_t* __restrict__ key,
-                      uint32_t* __restrict__ arrival, uint32_t* __restrict__ cell_count, ErrLatch* err,
-                      long long step) {
+                      const uint32_t* __restrict__ ids, Grid g, uint32_t drop_mask, const uint8_t* __restrict__ act,
+                      uint32_t* __restrict__ key, uint32_t* __restrict__ arrival, uint32_t* __restrict__ cell_count,
+                      ErrLatch* err, long long step) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  if (drop_mask && (tag_of(U[i].w) & drop_mask)) {
+  if ((drop_mask && (tag_of(U[i].w) & drop_mask)) || (act && act[i] == 2)) {
     key[i] = g.M;
     arrival[i] = atomicAdd(&cell_count[g.M], 1u);
     return;
@@ -186,17 +188,24 @@ __global__ void k_reorder(int n, const uint32_t* __restrict__ tmp_src, const uin
                           const float2* __restrict__ S2, float4* __restrict__ Pn, float4* __restrict__ Ln,
                           float4* __restrict__ Un, float4* __restrict__ S1n, float2* __restrict__ S2n,
                           uint32_t* __restrict__ ids_n, uint32_t* __restrict__ cell_of,
-                          uint32_t* __restrict__ slot_of_id, uint32_t M) {
+                          uint32_t* __restrict__ slot_of_id, uint32_t M, int keep_tail) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n) return;
   const uint32_t i = tmp_src[s];
   const uint32_t myid = tmp_id[s];
   const uint32_t c = key[i];
-  if (c == M) return;   // dropped (ghost of the previous step or emigrant)
-  const uint32_t b = cell_start[c], e = cell_start[c + 1];
-  uint32_t rank = 0;
-  for (uint32_t t = b; t < e; ++t) rank += (tmp_id[t] < myid) ? 1u : 0u;
-  const uint32_t d = b + rank;
+  uint32_t d;
+  if (c == M) {
+    // multi-GPU: a ghost of the previous step or an emigrant, dropped; Alg. 3: an Inactive particle,
+    // kept frozen behind the active set in its scatter slot (any order: it is nobody's neighbour)
+    if (!keep_tail) return;
+    d = (uint32_t)s;
+  } else {
+    const uint32_t b = cell_start[c], e = cell_start[c + 1];
+    uint32_t rank = 0;
+    for (uint32_t t = b; t < e; ++t) rank += (tmp_id[t] < myid) ? 1u : 0u;
+    d = b + rank;
+  }
   Pn[d] = P[i];
   Ln[d] = L[i];
   Un[d] = U[i];

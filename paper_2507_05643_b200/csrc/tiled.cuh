@@ -209,10 +209,11 @@ __global__ void TILE_BOUNDS
             const float4* __restrict__ L, float4* __restrict__ U, float4* __restrict__ S1, float2* __restrict__ S2,
             uint16_t* __restrict__ list, uint32_t* __restrict__ nlist, uint32_t* __restrict__ count_all,
             const uint32_t* __restrict__ cell_of, const Pose* __restrict__ pose, int cap, int store_all, Debug dbg,
-            int dbg_on, ErrLatch* err, const uint32_t* __restrict__ ids, long long step, long long tile_base) {
+            int dbg_on, ErrLatch* err, const uint32_t* __restrict__ ids, long long step, long long tile_base,
+            const uint32_t* __restrict__ tile_list) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
-  const TileGeom G = tile_geom(g, tile_base + (long long)blockIdx.x);
+  const TileGeom G = tile_geom(g, tile_list ? (long long)tile_list[blockIdx.x] : tile_base + (long long)blockIdx.x);
   tile_setup(g, G, cell_start, sm);
   const uint32_t n_i = sm.col_pref[NCOL];
   if (n_i == 0) return;
@@ -436,10 +437,11 @@ __global__ void TILE_BOUNDS
               float4* __restrict__ YS1, float2* __restrict__ YS2, uint16_t* __restrict__ list,
               uint32_t* __restrict__ nlist, uint32_t* __restrict__ count_all, const uint32_t* __restrict__ cell_of,
               int cap, float4* __restrict__ macc, Debug dbg, int dbg_on, ErrLatch* err,
-              const uint32_t* __restrict__ ids, long long step, long long tile_base) {
+              const uint32_t* __restrict__ ids, long long step, long long tile_base,
+              const uint32_t* __restrict__ tile_list) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
-  const TileGeom G = tile_geom(g, tile_base + (long long)blockIdx.x);
+  const TileGeom G = tile_geom(g, tile_list ? (long long)tile_list[blockIdx.x] : tile_base + (long long)blockIdx.x);
   tile_setup(g, G, cell_start, sm);
   const uint32_t n_i = sm.col_pref[NCOL];
   if (n_i == 0) return;

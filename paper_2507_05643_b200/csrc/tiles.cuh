@@ -68,6 +68,32 @@ __device__ __forceinline__ TileGeom tile_geom(const Grid& g, long long t) {
   return G;
 }
 
+// Active domains (Alg. 3): the tiles holding at least one (non-Inactive) particle, appended to
+// `list` (absolute tile indices, any order: tiles are independent) with warp-aggregated atomics.
+__global__ void k_tile_list(long long ntiles, long long tile_base, Grid g, const uint32_t* __restrict__ cell_start,
+                            uint32_t* __restrict__ list, uint32_t* __restrict__ count) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  bool keep = false;
+  if (t < ntiles) {
+    const TileGeom G = tile_geom(g, tile_base + t);
+    uint32_t n = 0;
+    for (int q = 0; q < NCOL; ++q) {
+      const int cx = G.X0 + q / TY, cy = G.Y0 + q % TY;
+      if (cx < g.dims[0] && cy < g.dims[1]) {
+        const uint32_t c0 = cell_id(g, cx, cy, G.z0);
+        n += cell_start[c0 + (G.z1 - G.z0)] - cell_start[c0];
+      }
+    }
+    keep = n > 0;
+  }
+  const unsigned m = __ballot_sync(0xffffffffu, keep);
+  const int lane = threadIdx.x & 31;
+  uint32_t base = 0;
+  if (lane == 0 && m) base = atomicAdd(count, (uint32_t)__popc(m));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (keep) list[base + __popc(m & ((1u << lane) - 1u))] = (uint32_t)(tile_base + t);
+}
+
 // Fill the tile geometry in shared memory (all threads call; contains __syncthreads).
 __device__ __forceinline__ void tile_setup(const Grid& g, const TileGeom& G, const uint32_t* __restrict__ cell_start,
                                           TileSmem& sm) {

@@ -92,3 +92,38 @@ def test_no_cpu_fallback_without_gpu(lib):
     with pytest.raises(crm.CrmError) as e:
         crm.Crm(sc.params)
     assert e.value.code == crm.CRM_E_CUDA
+
+
+def test_capacity_policy_host_function(lib):
+    """ManageArrayMemory of Alg. 3 in the product (host logic, no GPU): SPEC's scripted sequence
+    1000 -> 1200 -> 1200 -> 700 @ step 50 gives Grow -> 1440, Keep, Shrink -> 700 (G = 1.2, S = 0.75,
+    S_I = 50), and the same answers as the oracle's independent implementation."""
+    import oracle
+    from paper_2507_05643_b200 import crm
+    assert crm.manage_capacity(1000, 1200, 1) == (1440, 1)
+    assert crm.manage_capacity(1440, 1200, 2) == (1440, 0)
+    assert crm.manage_capacity(1000, 700, 50) == (700, 2)
+    rng = np.random.default_rng(3)
+    for _ in range(500):
+        cap, req, step = (int(v) for v in rng.integers(1, 5000, 3))
+        assert crm.manage_capacity(cap, req, step) == oracle.manage_capacity(cap, req, step)
+
+
+@pytest.mark.gpu   # crm_create needs a device
+def test_active_box_validation(lib):
+    import workloads
+    from paper_2507_05643_b200 import crm
+    sc = workloads.block_settle(n=(4, 4, 4))
+    c = crm.Crm(sc.params)
+    with pytest.raises(crm.CrmError) as e:
+        c.set_active_box(3, (0.1, 0.1, 0.1))          # no such body
+    assert e.value.code == crm.CRM_E_INVALID
+    with pytest.raises(crm.CrmError) as e:
+        c.set_active_box(0, (0.1, -1.0, 0.1))
+    assert e.value.code == crm.CRM_E_INVALID
+    with pytest.raises(crm.CrmError) as e:
+        c.set_active_policy(0.0, 0.5, 0.75, 50)       # growth < 1
+    assert e.value.code == crm.CRM_E_INVALID
+    c.set_active_box(0, (0.1, 0.1, 0.1))
+    c.set_active_policy(0.01)
+    c.close()

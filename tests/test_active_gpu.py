@@ -1,0 +1,131 @@
+"""GPU parity of active domains (Alg. 3) against the oracle, and the properties SPEC
+lists for it: full coverage bit-identical to the feature off, frozen inactive state,
+activity flags and the active set's structure bit-exact, rates within 1e-4 on the processed set,
+the ManageArrayMemory capacity policy, fewer particles processed than N."""
+import numpy as np
+import pytest
+
+import oracle
+import workloads
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def crm():
+    from paper_2507_05643_b200 import build
+    build.build_library()
+    from paper_2507_05643_b200 import crm as m
+    m.load_library()
+    return m
+
+
+def rel_linf(a, b):
+    den = np.abs(b).max()
+    return np.abs(a - b).max() / (den if den > 0 else 1.0)
+
+
+def plough_bed(nx=28, ny=10, nz=8, v=0.5, S0=False):
+    """A bed with a prescribed 'plough' (small marker cube) moving along +x above and into it;
+    its active box (half extents 3 d0 x 3 d0 x 6 d0) travels with it."""
+    sc = workloads.block_settle(n=(nx, ny, nz), jitter=0.05, seed=4)
+    if S0:
+        sc = workloads.rate_state_S0(sc)
+    d0 = sc.params["d0"]
+    g = np.arange(3) * d0
+    cube = np.stack(np.meshgrid(g, g, g, indexing="ij"), -1).reshape(-1, 3) - d0
+    pos0 = np.array([5.3 * d0, 5.1 * d0, 7.7 * d0])
+    b = workloads.Body(mass=1.0, inertia=(1, 1, 1), pos=tuple(pos0), vel=(v, 0.0, 0.0),
+                       motion=workloads.BODY_PRESCRIBED, markers=workloads.f32(cube + pos0))
+    sc.bodies = [b]
+    sc.active = {"boxes": {1: (3.1 * d0, 3.1 * d0, 6.1 * d0)}, "t_delay": -1.0}
+    return sc
+
+
+def test_full_coverage_bit_identical(crm):
+    sc = workloads.block_settle(n=(16, 10, 8), jitter=0.05, seed=4)
+    p = sc.params
+    a = crm.load_scenario(sc)
+    sc.active = {"boxes": {0: [0.5 * (p["hi"][k] - p["lo"][k]) + 1.0 for k in range(3)]}, "t_delay": -1.0}
+    b = crm.load_scenario(sc)
+    a.step(sc.dt, 12)
+    b.step(sc.dt, 12)
+    assert np.all(b.activity() == 0)
+    for x, y in zip(a.get_state(), b.get_state()):
+        assert np.array_equal(x, y)
+
+
+def test_activity_and_structure_match_oracle(crm):
+    sc = plough_bed()
+    g = crm.load_scenario(sc)
+    o = oracle.load_scenario(sc)
+    for k in range(3):
+        if k:   # flags of the last step's rebuild on both sides
+            assert np.array_equal(g.activity(), o.activity())
+        sg, so = g.structure(), o.structure()
+        nae = int(so["cell_start"][-1])
+        assert int(sg["cell_start"][-1]) == nae and nae < g.count()   # fewer than N processed
+        assert np.array_equal(sg["cell_start"], so["cell_start"])
+        assert np.array_equal(sg["sorted_ids"][:nae], so["sorted_ids"][:nae])
+        assert np.array_equal(np.sort(sg["sorted_ids"][nae:]), so["sorted_ids"][nae:])
+        assert np.array_equal(sg["cell"], so["cell"])
+        assert np.array_equal(sg["counts"], so["counts"])
+        og, lg = g.neighbors()
+        oo, lo = o.neighbors()
+        assert np.array_equal(og, oo) and np.array_equal(lg, lo)
+        g.step(sc.dt, 10)
+        o.step(sc.dt, 10)
+    st = g.active_stats()
+    f = g.activity()
+    assert st["active"] == int((f == 0).sum()) and st["extended"] == int((f == 1).sum())
+    assert st["inactive"] == int((f == 2).sum()) and st["n_ae"] == st["active"] + st["extended"]
+
+
+def test_rates_parity_on_the_active_set(crm):
+    sc = plough_bed(S0=True)
+    sc.params["gamma_a"] = 0.2
+    g = crm.load_scenario(sc)
+    o = oracle.load_scenario(sc)
+    g.debug_arm(True)
+    g.step(sc.dt, 1)
+    o.step(sc.dt, 1)
+    nf = sc.n_fluid
+    f = o.activity()[:nf]
+    assert np.array_equal(g.activity()[:nf], f)
+    proc = f != 2
+    assert proc.sum() > 100 and (~proc).sum() > 100
+    for stage in (0, 1):
+        for a_g, a_o in zip(g.last_rates(stage), o.last_rates(stage)):
+            assert rel_linf(a_g[:nf][proc], a_o[:nf][proc]) <= 1e-4, stage
+            assert np.all(a_o[:nf][~proc] == 0)
+
+
+def test_trajectory_frozen_state_and_capacity(crm):
+    sc = plough_bed()
+    g = crm.load_scenario(sc)
+    o = oracle.load_scenario(sc)
+    x0 = g.get_state()
+    g.step(sc.dt, 1)
+    st = g.active_stats()
+    # step 0 is a multiple of S_I = 50 and N_{a+e} / N < S = 0.75: ManageArrayMemory shrinks
+    assert st["action"] == 2 and st["capacity"] == st["n_ae"] < g.count()
+    for _ in range(6):
+        g.step(sc.dt, 10)
+        s = g.active_stats()
+        assert s["capacity"] >= s["n_ae"]
+        if s["action"] == 1:            # Grow to ceil(N G)
+            assert s["capacity"] == int(np.ceil(s["n_ae"] * 1.2))
+    o.step(sc.dt, 61)
+    nf = sc.n_fluid
+    xg, ug, rg, sg = [a[:nf] for a in g.get_state()]
+    xo, uo, ro, so = [a[:nf] for a in o.get_state()]
+    assert np.abs(xg - xo).max() < 1e-2 * sc.params["d0"]
+    # particles that never left the Inactive set are bit-identical to the input
+    never = np.ones(nf, bool)
+    o2 = oracle.load_scenario(sc)
+    for _ in range(61):
+        o2.step(sc.dt, 1)
+        never &= o2.activity()[:nf] == 2
+    assert never.sum() > 100
+    for a, b in zip(g.get_state(), x0):
+        assert np.array_equal(a[:nf][never], b[:nf][never])

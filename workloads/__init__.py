@@ -271,6 +271,45 @@ def mgru3_bin(d0=1e-2, n=(500, 80, 25), dt=2.5e-4, steps=100) -> Scenario:
     return Scenario("mgru3_bin", p, f32(pos), None, None, f32(walls), [], dt, steps, meta=dict(n=n))
 
 
+def cylinder_markers(R: float, width: float, d0: float, layers: int) -> np.ndarray:
+    """BCE markers of a wheel rim: cylindrical shells r = R - k d0 (k < layers) about the body y
+    axis, spacing ~d0 along the arc and the width."""
+    out = []
+    ny = max(1, int(round(width / d0)))
+    ys = (np.arange(ny) + 0.5) * (width / ny) - 0.5 * width
+    for k in range(layers):
+        r = R - k * d0
+        nt = max(8, int(round(2 * math.pi * r / d0)))
+        th = (np.arange(nt) + 0.5) * (2 * math.pi / nt)
+        T, Y = np.meshgrid(th, ys, indexing="ij")
+        out.append(np.stack([r * np.cos(T).ravel(), Y.ravel(), r * np.sin(T).ravel()], -1))
+    return np.concatenate(out, axis=0)
+
+
+def mgru3_wheel(d0=1e-2, n=(500, 80, 25), R=0.2, width=0.2, vx=0.2, slip=0.3, sinkage=0.02,
+                active=True, dt=2.5e-4) -> Scenario:
+    """NEXT #2/#3 workload: the C4 MGRU3 soil bin with a prescribed rolling wheel (rim markers,
+    v = vx, omega_y = vx / (R (1 - slip))) and the paper's MGRU3 active box 0.6 x 0.6 x 0.8 m
+    around the wheel (P:950, P:960 'Active Box: 0.6 x 0.6 x 0.8 m', Alg. 3); fluid inside the wheel removed."""
+    sc = mgru3_bin(d0=d0, n=n, dt=dt)
+    nx, ny, nz = n
+    c = np.array([0.8, 0.5 * ny * d0, nz * d0 + R - sinkage])
+    rim = cylinder_markers(R, width, d0, bce_layers(sc.params["h"], d0))
+    rel = sc.fluid_pos - c
+    inside = (rel[:, 0] ** 2 + rel[:, 2] ** 2 < (R + 0.5 * d0) ** 2) & (np.abs(rel[:, 1]) < 0.5 * width + d0)
+    sc.fluid_pos = sc.fluid_pos[~inside]
+    hi = list(sc.params["hi"])
+    hi[2] = max(hi[2], c[2] + R + 4 * d0)          # grid box above the wheel top
+    sc.params["hi"] = tuple(hi)
+    b = Body(mass=10.0, inertia=(1.0, 1.0, 1.0), pos=tuple(c), vel=(vx, 0.0, 0.0),
+             omega=(0.0, vx / (R * (1.0 - slip)), 0.0), motion=BODY_PRESCRIBED, markers=f32(rim + c))
+    sc.bodies = [b]
+    sc.name = "mgru3_wheel"
+    if active:
+        sc.active = {"boxes": {1: (0.3, 0.3, 0.4)}, "t_delay": -1.0}
+    return sc
+
+
 def random_cloud(n: int, seed: int, box: float = 1.0) -> np.ndarray:
     """Uniform random cloud in [0, box)^3, fp32-representable."""
     rng = np.random.default_rng(seed)
