@@ -177,6 +177,10 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ our arm
+def ps_freq_of(sc) -> int:
+    return int(sc.params.get("ps_freq", 1) or 1)
+
+
 def active_measure(crm, torch, local, warmup, steps):
     """ms/step of the MGRU3 wheel bin with and without active domains (same input, same steps)."""
     out = {"workload": "mgru3_wheel", "active_box_m": [0.6, 0.6, 0.8], "steps": steps}
@@ -206,6 +210,32 @@ def active_measure(crm, torch, local, warmup, steps):
                    "ps_freq = 1; paper Table tab:active_domains_performance: MGRU3 wheel 2.93x, "
                    "RASSOR drum 2.11x (whole co-simulation RTF, its hardware)")
     return out
+
+
+def cone_measure(crm, torch, local, warmup, steps_total=1500, every=150):
+    """The cone penetration test (P:65-104) on the full C3 bed: 60 deg cone, fall from H = L;
+    ms/step and the depth-vs-time curve of the tip below the initial surface."""
+    sc = workloads.cone_drop(H_over_L=1.0)
+    g = crm.load_scenario(sc, device=local)
+    st = torch.cuda.ExternalStream(g.stream(), device=local)
+    surface = sc.meta["n"][2] * sc.params["d0"]
+    curve, ms = [], 0.0
+    for _ in range(steps_total // every):
+        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        g.step(sc.dt, every)
+        e1.record(st)
+        torch.cuda.synchronize()
+        ms += e0.elapsed_time(e1)
+        tip = g.get_body(1)["pos"][2] - 0.75 * sc.meta["cone_L"]
+        curve.append([round((len(curve) + 1) * every * sc.dt, 6), round(surface - tip, 6)])
+    g.close()
+    n = (steps_total // every) * every
+    return {"workload": sc.name, "n_fluid": sc.n_fluid, "n_bce": sc.n_bce, "steps": n,
+            "ms_per_step": ms / n, "value": sc.n_fluid / (ms / n * 1e-3), "unit": UNIT,
+            "depth_vs_time_s_m": curve,
+            "note": "free 60 deg / 19.8 mm steel cone (reading A32) entering with sqrt(2 g L); the paper "
+                    "compares this curve with experiments (P:100), which are not reproduced here"}
 
 
 def main():
@@ -262,6 +292,7 @@ def main():
     # directed fluid pairs of this rank (algorithmic work of the rates kernels)
     pairs_local = g.pair_count()
     pairs_fluid = pairs_local
+    cand_local, cand_markers = g.candidate_count()   # Alg. 1 candidate tests (filter work)
     if dist is not None:
         t = torch.tensor([pairs_local], dtype=torch.int64, device=f"cuda:{local}")
         dist.all_reduce(t)
@@ -300,10 +331,13 @@ def main():
     if dname in ("k_rates_A", "k_rates_B"):
         n_own = g.count(crm.CRM_OWNED) if world > 1 else n_fluid
         flops = pairs_local * FLOPS_PER_PAIR + min(n_own, n_fluid) * FLOPS_EPILOGUE[dname]
+        if dname == "k_rates_A" and ps_freq_of(sc) == 1:   # stage A also runs Alg. 1's filter every step
+            flops += cand_local * FLOPS_PER_CANDIDATE
         achieved = flops / per_launch_s / 1e12
         peak = fp32_peak_tflops(pk["sm_max_mhz"])
         roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                 "kernel": dname, "algorithmic_flops_per_launch": flops, "flops_per_pair": FLOPS_PER_PAIR,
+                "pairs": pairs_local, "candidates": cand_local, "flops_per_candidate": FLOPS_PER_CANDIDATE,
                 "peak_note": "148 SM x 128 FP32 lanes x 2 x sm_max_mhz (DESIGN.md §Roofline)"}
     else:
         nbytes = (n_fluid + n_bce) * KERNEL_BYTES.get(dname, 56)
@@ -384,8 +418,10 @@ def main():
     # active domains (Alg. 3) on the MGRU3 wheel bin (1M particles, the
     # paper's 0.6 x 0.6 x 0.8 m active box around a prescribed rolling wheel), on vs off
     nxt_active = None
+    nxt_cone = None
     if not args.no_next and world == 1 and rank == 0:
         nxt_active = active_measure(crm, torch, local, args.warmup, max(10, args.steps))
+        nxt_cone = cone_measure(crm, torch, local, args.warmup)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -401,7 +437,8 @@ def main():
                            "l2": "inputs larger than L2 (56 B x N state >> 126 MB), no flush",
                            "parallelism": f"x-slabs x{world}, NCCL ghost planes" if world > 1 else "single GPU"},
                 "roofline": roof, "hbm_roofline": hbm, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": launches, "clocks": clocks, "next_alg2": nxt, "next_active": nxt_active}
+                "gpu_launches": launches, "clocks": clocks, "next_alg2": nxt, "next_active": nxt_active,
+                "next_cone": nxt_cone}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()

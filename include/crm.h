@@ -45,7 +45,7 @@ extern "C" {
 #define CRM_E_INVALID     -1   /* bad argument: h <= 0, d0 <= 0, h < d0, dt <= 0, mu_s > mu_2, K/G <= 0 ... */
 #define CRM_E_DOMAIN      -2   /* a particle left the fixed grid box (reading A19) */
 #define CRM_E_NONFINITE   -3   /* non-finite fluid state after a step */
-#define CRM_E_UNSUPPORTED -4   /* option not built: Holmes extrapolation, support != 2, moving bodies on slabs */
+#define CRM_E_UNSUPPORTED -4   /* option not built: Holmes extrapolation, support != 2, active domains on slabs */
 #define CRM_E_STATE       -5   /* crm_add_* after the first step, debug data not available */
 #define CRM_E_OOM         -6   /* device or host allocation failed */
 #define CRM_E_CUDA        -7   /* CUDA runtime error, or no sm_100 device */
@@ -138,8 +138,10 @@ int  crm_step(crm_t* ctx, double dt, int64_t nsteps);
  * A context created with crm_dist_t.world > 1 owns the cell planes [x_lo, x_hi) chosen from a
  * prefix sum of per-plane particle counts of the (identical) global crm_add_* input.  Every rank
  * passes the same global arrays; the library keeps its slab.  crm_get_state then fills only the
- * rows of owned ids (other rows are NaN) and crm_count(ctx, CRM_OWNED) counts them.  Moving
- * bodies and the debug exports are single-GPU only in this build (CRM_E_UNSUPPORTED). */
+ * rows of owned ids (other rows are NaN) and crm_count(ctx, CRM_OWNED) counts them.  The
+ * debug exports and active domains are single-GPU only in this build (CRM_E_UNSUPPORTED); moving
+ * bodies work on slabs: each slab sums the loads of the markers it owns, the partial sums are
+ * exchanged and added in rank order, so every rank integrates the same body state. */
 /* Step `world` contexts of ranks 0..world-1 living in one process on one device and stream
  * (nccl_id NULL): exchanges become device copies ("loopback"); used to test the decomposition
  * on one GPU.  Owned particles follow bit-identical trajectories to a one-context run. */
@@ -206,6 +208,10 @@ int     crm_set_graphs(crm_t* ctx, int on);
  * as built by the last step (the work of the rates loops; bench.py roofline).  CRM_E_STATE before
  * the first step. */
 int     crm_pair_count(crm_t* ctx, int64_t* fluid_pairs);
+/* Alg. 1 candidates of the last structure: for every owned particle, the particles of
+ * the 27 cells around its cell minus itself, summed over fluid particles and over markers (the
+ * work of the neighbour filter; bench.py roofline).  CRM_E_STATE before the first step. */
+int     crm_candidate_count(crm_t* ctx, int64_t* fluid_candidates, int64_t* marker_candidates);
 
 /* ---- test-only exports (parity harness) ---- */
 /* Arm/disarm capture of per-step rates and BCE values (costs extra HBM writes). */

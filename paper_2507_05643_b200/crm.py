@@ -25,7 +25,7 @@ EXPORTS = [
     "crm_stream", "crm_launch_count", "crm_profile_enable", "crm_profile_read", "crm_profile_reset",
     "crm_kernel_name", "crm_set_graphs", "crm_debug_arm", "crm_debug_structure", "crm_debug_neighbors",
     "crm_debug_rates", "crm_debug_bce", "crm_group_step", "crm_nccl_unique_id", "crm_slab_partition",
-    "crm_pair_count", "crm_set_active_box", "crm_set_active_policy", "crm_active_stats", "crm_manage_capacity",
+    "crm_pair_count", "crm_candidate_count", "crm_set_active_box", "crm_set_active_policy", "crm_active_stats", "crm_manage_capacity",
     "crm_debug_activity",
 ]
 
@@ -106,6 +106,7 @@ def load_library(path: str = LIB_PATH):
     L.crm_nccl_unique_id.argtypes = [C.c_void_p]
     L.crm_slab_partition.argtypes = [_I64, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int)]
     L.crm_pair_count.argtypes = [vp, _I64]
+    L.crm_candidate_count.argtypes = [vp, _I64, _I64]
     L.crm_set_active_box.argtypes = [vp, C.c_int32, _D]
     L.crm_set_active_policy.argtypes = [vp, C.POINTER(ActiveT)]
     L.crm_active_stats.argtypes = [vp, _I64]
@@ -299,6 +300,12 @@ class Crm:
         v = C.c_int64()
         self._chk(self._L.crm_pair_count(self.h, C.byref(v)), "crm_pair_count")
         return v.value
+
+    def candidate_count(self) -> tuple[int, int]:
+        """Alg. 1 candidates (fluid, markers) of the last structure."""
+        f, b = C.c_int64(), C.c_int64()
+        self._chk(self._L.crm_candidate_count(self.h, C.byref(f), C.byref(b)), "crm_candidate_count")
+        return f.value, b.value
 
     def set_graphs(self, on: bool):
         self._chk(self._L.crm_set_graphs(self.h, 1 if on else 0), "crm_set_graphs")

@@ -94,6 +94,7 @@ struct crm {
   int* d_moving_bodies = nullptr;
   int n_moving_markers = 0, n_moving_bodies = 0;
   float4* macc = nullptr;
+  double* d_bpart = nullptr;             // partial body loads, world blocks of n_moving_bodies x 6 (rank order)
   ErrLatch* d_err = nullptr;
   ErrLatch* h_err = nullptr;
   Debug dbg{};

@@ -59,9 +59,6 @@ int commit(crm_t* c) {
   // ---- which particles are local (slab mode: the owned planes only; ghosts come with step 1)
   std::vector<uint32_t> owned;
   if (c->slab) {
-    for (size_t b = 1; b < c->bodies.size(); ++b)
-      if (c->bodies[b].motion != CRM_BODY_FIXED)
-        return fail(c, CRM_E_UNSUPPORTED, "moving bodies are not supported with world > 1 in this build");
     const int Nx = c->grid.dims[0];
     std::vector<int64_t> counts(Nx, 0);
     std::vector<int> plane(c->n);
@@ -164,7 +161,7 @@ int commit(crm_t* c) {
   if (c->n_moving_markers) {
     if (dalloc(c, &c->d_moving_ids, mids.size()) || dalloc(c, &c->d_xlocal, xl.size()) ||
         dalloc(c, &c->d_mstart, mstart.size()) || dalloc(c, &c->d_moving_bodies, mb.size()) ||
-        dalloc(c, &c->macc, n))
+        dalloc(c, &c->macc, n) || dalloc(c, &c->d_bpart, (size_t)c->world * mb.size() * 6))
       return CRM_E_OOM;
     CK(cudaMemcpyAsync(c->d_moving_ids, mids.data(), mids.size() * 4, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->d_xlocal, xl.data(), xl.size() * 16, cudaMemcpyHostToDevice, c->stream));
@@ -386,6 +383,27 @@ void issue_rates(crm_t* c, int stage, float dt, long long step) {
 }
 
 // one RK2 step on one GPU (everything on the stream, no host sync)
+// moving bodies: this rank's partial loads into its block of d_bpart (A13)
+void issue_body_partial(crm_t* c, float dt) {
+  launch(c, KID_BODY, k_body_partial, dim3(c->n_moving_bodies), dim3(BODY_BS), (const int*)c->d_moving_bodies,
+         (const uint32_t*)c->d_mstart, (const uint32_t*)c->d_moving_ids, (const uint32_t*)c->slot_of_id,
+         (const float4*)c->U[c->cur], (const float4*)c->macc, (const float4*)c->Pm, (const float4*)c->Lm,
+         (const BodyState*)c->d_bodies, (double)dt, c->d_bpart + (size_t)c->rank * c->n_moving_bodies * 6);
+}
+
+// sum of the ranks' partial loads (rank order), rigid update, poses, markers at t_{n+1}
+void issue_body_finish(crm_t* c, float dt) {
+  launch(c, KID_BODY, k_body_integrate, dim3(blocks(c->n_moving_bodies, 64)), dim3(64), c->n_moving_bodies,
+         (const int*)c->d_moving_bodies, (const double*)c->d_bpart, c->world, c->d_bodies, (double)dt, c->ph.g[0],
+         c->ph.g[1], c->ph.g[2]);
+  launch(c, KID_POSES, k_body_poses, dim3(1), dim3(64), (int)c->bodies.size(), (const BodyState*)c->d_bodies,
+         0.5 * (double)dt, c->d_pose0, c->d_posem);
+  const int y = c->cur;
+  launch(c, KID_MARKERS, k_markers_place, dim3(blocks(c->n_moving_markers, 128)), dim3(128), c->n_moving_markers,
+         (const uint32_t*)c->d_moving_ids, (const float4*)c->d_xlocal, (const uint32_t*)c->slot_of_id,
+         (const Pose*)c->d_pose0, c->P[y], c->L[y], (const float4*)c->U[y]);
+}
+
 int issue_step(crm_t* c, float dt, long long step) {
   // Alg. 2: rebuild (sort + filtered lists) when t mod ps_freq == 0; otherwise the particles keep
   // their slots and the stored lists are reused without a distance re-check (A17)
@@ -406,14 +424,8 @@ int issue_step(crm_t* c, float dt, long long step) {
   issue_bce(c, 1, dt, step, 0);
   issue_rates(c, 1, dt, step);
   if (c->n_moving_bodies) {
-    launch(c, KID_BODY, k_body_update, dim3(c->n_moving_bodies), dim3(BODY_BS), (const int*)c->d_moving_bodies,
-           (const uint32_t*)c->d_mstart, (const uint32_t*)c->d_moving_ids, (const uint32_t*)c->slot_of_id,
-           (const float4*)c->macc, (const float4*)c->Pm, (const float4*)c->Lm, c->d_bodies, (double)dt, c->ph.g[0], c->ph.g[1], c->ph.g[2]);
-    launch(c, KID_POSES, k_body_poses, dim3(1), dim3(64), (int)c->bodies.size(), (const BodyState*)c->d_bodies,
-           0.5 * (double)dt, c->d_pose0, c->d_posem);
-    launch(c, KID_MARKERS, k_markers_place, dim3(blocks(c->n_moving_markers, 128)), dim3(128), c->n_moving_markers,
-           (const uint32_t*)c->d_moving_ids, (const float4*)c->d_xlocal, (const uint32_t*)c->slot_of_id,
-           (const Pose*)c->d_pose0, c->P[y], c->L[y], (const float4*)c->U[y]);
+    issue_body_partial(c, dt);
+    issue_body_finish(c, dt);
   }
   if (c->dbg_on) cudaMemcpyAsync(c->dbg_ids, c->ids[y], (size_t)c->nl * 4, cudaMemcpyDeviceToDevice, c->stream);
   return CRM_OK;
@@ -688,7 +700,7 @@ void crm_destroy(crm_t* c) {
   for (auto p : c->scan_sums_x) cudaFree(p);
   cudaFree(c->d_bodies); cudaFree(c->d_pose0); cudaFree(c->d_posem);
   cudaFree(c->d_moving_ids); cudaFree(c->d_xlocal); cudaFree(c->d_mstart); cudaFree(c->d_moving_bodies);
-  cudaFree(c->macc); cudaFree(c->d_err); cudaFree(c->d_xcount); cudaFree(c->dbg_ids); cudaFree(c->d_stage);
+  cudaFree(c->macc); cudaFree(c->d_bpart); cudaFree(c->d_err); cudaFree(c->d_xcount); cudaFree(c->dbg_ids); cudaFree(c->d_stage);
   if (c->h_err) cudaFreeHost(c->h_err);
   if (c->h_pin) cudaFreeHost(c->h_pin);
   if (c->own_stream) cudaStreamDestroy(c->stream);
@@ -899,6 +911,25 @@ int crm_pair_count(crm_t* c, int64_t* fluid_pairs) {
   CK(cudaStreamSynchronize(c->stream));
   cudaFree(d);
   *fluid_pairs = (int64_t)h;
+  return CRM_OK;
+}
+
+int crm_candidate_count(crm_t* c, int64_t* fluid_candidates, int64_t* marker_candidates) {
+  if (!c) return CRM_E_INVALID;
+  if (!c->committed || c->steps_done == 0) return fail(c, CRM_E_STATE, "no step taken yet");
+  unsigned long long* d = nullptr;
+  CK(cudaMalloc(&d, 16));
+  CK(cudaMemsetAsync(d, 0, 16, c->stream));
+  const int n = (int)(c->boxes.empty() ? c->nl : c->n_ae);
+  if (n > 0)
+    launch(c, KID_SLAB, k_candidate_count, dim3(blocks(n, 256)), dim3(256), n, c->grid, (const float4*)c->U[c->cur],
+           (const uint32_t*)c->cell_of, (const uint32_t*)c->cell_start, d);
+  unsigned long long h[2] = {0, 0};
+  CK(cudaMemcpyAsync(h, d, 16, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  cudaFree(d);
+  if (fluid_candidates) *fluid_candidates = (int64_t)h[0];
+  if (marker_candidates) *marker_candidates = (int64_t)h[1];
   return CRM_OK;
 }
 

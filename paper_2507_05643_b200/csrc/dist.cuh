@@ -203,6 +203,8 @@ int post_counts(crm_t* c, uint32_t l0, uint32_t l1, uint32_t r0, uint32_t r1) {
 void issue_sort(crm_t* c, long long step, uint32_t drop_mask);
 void issue_bce(crm_t* c, int stage, float dt, long long step, int store_all);
 void issue_rates(crm_t* c, int stage, float dt, long long step);
+void issue_body_partial(crm_t* c, float dt);
+void issue_body_finish(crm_t* c, float dt);
 
 // ---------------------------------------------------------------------------------------
 // the phases of one slab step (each ends with posts; the transport flushes between phases)
@@ -324,6 +326,10 @@ int slab_phase(crm_t* c, int k, float dt, long long step) {
         if (c->s_hip1 > c->s_hi)
           launch(c, KID_SLAB, k_or_tag, dim3(blocks(c->s_hip1 - c->s_hi, 256)), dim3(256), c->U[y], c->s_hi, c->s_hip1, TAG_GHOST);
         issue_rates(c, 0, dt, step);
+        if (c->n_moving_markers)   // moving markers at the mid-step pose, before the y_mid halo
+          launch(c, KID_MARKERS, k_markers_place, dim3(blocks(c->n_moving_markers, 128)), dim3(128),
+                 c->n_moving_markers, (const uint32_t*)c->d_moving_ids, (const float4*)c->d_xlocal,
+                 (const uint32_t*)c->slot_of_id, (const Pose*)c->d_posem, c->Pm, c->Lm, (const float4*)c->Um);
       } else {
         issue_bce(c, 1, dt, step, 0);
       }
@@ -333,12 +339,24 @@ int slab_phase(crm_t* c, int k, float dt, long long step) {
       post_mid_slice(c, R, false, c->s_hi, c->s_hip1);
       return CRM_OK;
     }
-    case 7:
+    case 7:   // rates + full step; moving bodies: this slab's partial loads to every other slab
       issue_rates(c, 1, dt, step);
+      if (c->n_moving_bodies) {
+        issue_body_partial(c, dt);
+        const size_t blk = (size_t)c->n_moving_bodies * 6;
+        for (int p = 0; p < c->world; ++p) {
+          if (p == c->rank) continue;
+          post(c, p, true, c->d_bpart + (size_t)c->rank * blk, blk * sizeof(double));
+          post(c, p, false, c->d_bpart + (size_t)p * blk, blk * sizeof(double));
+        }
+      }
+      return CRM_OK;
+    case 8:   // moving bodies: loads summed over slabs in rank order (identical on every rank), update
+      if (c->n_moving_bodies) issue_body_finish(c, dt);
       return CRM_OK;
   }
   return CRM_OK;
 }
-constexpr int kSlabPhases = 8;
+constexpr int kSlabPhases = 9;
 
 }  // namespace

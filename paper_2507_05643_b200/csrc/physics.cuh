@@ -91,26 +91,29 @@ __device__ __forceinline__ void return_map(float s[6], const float sn[6], const 
 }
 
 // ------------------------------------------------------------------------------------
-// Loads of moving bodies (A13) from the stage-B marker accelerations, deterministic
-// fixed-order fp64 reduction, then the rigid update (semi-implicit Euler, once per step).
+// Loads of moving bodies (A13) from the stage-B marker accelerations: a deterministic
+// fixed-order fp64 reduction over this rank's markers (k_body_partial, one block per moving body),
+// then — after the slabs exchanged their partial sums (multi-GPU) — the sum over ranks in rank order
+// and the rigid update (semi-implicit Euler, once per step; k_body_integrate).
 constexpr int BODY_BS = 256;
-__global__ void __launch_bounds__(BODY_BS) k_body_update(const int* __restrict__ moving_bodies,
-                                                         const uint32_t* __restrict__ mstart,
-                                                         const uint32_t* __restrict__ moving_ids,
-                                                         const uint32_t* __restrict__ slot_of_id,
-                                                         const float4* __restrict__ macc,
-                                                         const float4* __restrict__ Pmid,
-                                                         const float4* __restrict__ Lmid,
-                                                         BodyState* __restrict__ bodies, double dt, float g0,
-                                                         float g1, float g2) {
+__global__ void __launch_bounds__(BODY_BS) k_body_partial(const int* __restrict__ moving_bodies,
+                                                          const uint32_t* __restrict__ mstart,
+                                                          const uint32_t* __restrict__ moving_ids,
+                                                          const uint32_t* __restrict__ slot_of_id,
+                                                          const float4* __restrict__ U,
+                                                          const float4* __restrict__ macc,
+                                                          const float4* __restrict__ Pmid,
+                                                          const float4* __restrict__ Lmid,
+                                                          const BodyState* __restrict__ bodies, double dt,
+                                                          double* __restrict__ partial) {
   __shared__ double red[6][BODY_BS];
   const int bi = blockIdx.x;
-  const int b = moving_bodies[bi];
-  BodyState& B = bodies[b];
+  const BodyState& B = bodies[moving_bodies[bi]];
   const double pm[3] = {B.pos[0] + 0.5 * dt * B.vel[0], B.pos[1] + 0.5 * dt * B.vel[1], B.pos[2] + 0.5 * dt * B.vel[2]};
   double acc[6] = {0, 0, 0, 0, 0, 0};
   for (uint32_t k = mstart[bi] + threadIdx.x; k < mstart[bi + 1]; k += BODY_BS) {
     const uint32_t s = slot_of_id[moving_ids[k]];
+    if (s == 0xffffffffu || tag_ghost(tag_of(U[s].w))) continue;   // owned by another slab
     const float4 f = macc[s];
     const float4 x = Pmid[s], xl = Lmid[s];
     const double r[3] = {(double)x.x + (double)xl.x - pm[0], (double)x.y + (double)xl.y - pm[1],
@@ -128,8 +131,22 @@ __global__ void __launch_bounds__(BODY_BS) k_body_update(const int* __restrict__
       for (int c = 0; c < 6; ++c) red[c][threadIdx.x] += red[c][threadIdx.x + o];
     __syncthreads();
   }
-  if (threadIdx.x != 0) return;
-  const double F[3] = {red[0][0], red[1][0], red[2][0]}, T[3] = {red[3][0], red[4][0], red[5][0]};
+  if (threadIdx.x < 6) partial[bi * 6 + threadIdx.x] = red[threadIdx.x][0];
+}
+
+// parts: world blocks of nbm x 6 partial sums (rank order); one thread per moving body
+__global__ void k_body_integrate(int nbm, const int* __restrict__ moving_bodies, const double* __restrict__ parts,
+                                 int world, BodyState* __restrict__ bodies, double dt, float g0, float g1, float g2) {
+  const int bi = blockIdx.x * blockDim.x + threadIdx.x;
+  if (bi >= nbm) return;
+  BodyState& B = bodies[moving_bodies[bi]];
+  double F[3], T[3];
+  for (int c = 0; c < 3; ++c) { F[c] = parts[bi * 6 + c]; T[c] = parts[bi * 6 + 3 + c]; }
+  for (int r = 1; r < world; ++r)
+    for (int c = 0; c < 3; ++c) {
+      F[c] += parts[(size_t)r * nbm * 6 + bi * 6 + c];
+      T[c] += parts[(size_t)r * nbm * 6 + bi * 6 + 3 + c];
+    }
   const double g[3] = {g0, g1, g2};
   for (int c = 0; c < 3; ++c) { B.force[c] = F[c]; B.torque[c] = T[c]; }
   if (B.motion == 1) {   // FREE

@@ -38,6 +38,7 @@ __global__ void k_markers_place(int nm, const uint32_t* __restrict__ moving_ids,
   if (k >= nm) return;
   const uint32_t id = moving_ids[k];
   const uint32_t s = slot_of_id[id];
+  if (s == 0xffffffffu) return;   // multi-GPU: the marker lives on another slab
   const uint32_t b = tag_body(tag_of(U[s].w));
   const float4 xl = xlocal[k];
   const Pose& q = pose[b];
@@ -162,6 +163,41 @@ __global__ void k_pair_count(int n, const float4* __restrict__ U, const uint32_t
   }
   for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
   if ((threadIdx.x & 31) == 0 && v) atomicAdd(out, v);
+}
+
+// Alg. 1 candidates: per particle, the particles of the 27 cells around its cell minus itself
+// (out[0] over owned fluid particles, out[1] over markers) — the filter's algorithmic work
+__global__ void k_candidate_count(int n, Grid g, const float4* __restrict__ U, const uint32_t* __restrict__ cell_of,
+                                  const uint32_t* __restrict__ cell_start, unsigned long long* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long vf = 0, vb = 0;
+  if (i < n) {
+    const uint32_t t = tag_of(U[i].w);
+    const uint32_t c = cell_of[i];
+    if (!tag_ghost(t) && c < g.M) {
+      const int Nz = g.dims[2], Ny = g.dims[1];
+      const int cz = (int)(c % (uint32_t)Nz), cy = (int)((c / (uint32_t)Nz) % (uint32_t)Ny);
+      const int cx = (int)(c / (uint32_t)(Ny * Nz));
+      unsigned long long k = 0;
+      for (int a = -1; a <= 1; ++a)
+        for (int b = -1; b <= 1; ++b) {
+          const int x = cx + a, y = cy + b;
+          if (x < 0 || x >= g.dims[0] || y < 0 || y >= Ny) continue;
+          const int z0 = max(cz - 1, 0), z1 = min(cz + 1, Nz - 1);
+          const uint32_t c0 = (uint32_t)x * (uint32_t)(Ny * Nz) + (uint32_t)y * (uint32_t)Nz;
+          k += cell_start[c0 + z1 + 1] - cell_start[c0 + z0];
+        }
+      (tag_is_bce(t) ? vb : vf) = k - 1;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    vf += __shfl_down_sync(0xffffffffu, vf, o);
+    vb += __shfl_down_sync(0xffffffffu, vb, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (vf) atomicAdd(&out[0], vf);
+    if (vb) atomicAdd(&out[1], vb);
+  }
 }
 
 __global__ void k_fill_u32(uint32_t* __restrict__ p, long long n, uint32_t v) {

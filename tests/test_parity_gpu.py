@@ -362,3 +362,27 @@ def test_cuda_graph_replay_bit_identical(crm):
         b.step(sc.dt, 7)
         for x, y in zip(a.get_state(), b.get_state()):
             assert np.array_equal(x, y)
+
+
+def test_work_counters_match_the_structure(crm):
+    """bench.py's roofline counts (directed fluid pairs, Alg. 1 candidates) against the oracle's
+    structure: pairs = sum of fluid neighbour counts; candidates = particles of the 27 cells around
+    each particle's cell minus itself."""
+    sc = workloads.block_settle(jitter=0.05)
+    g, o = both(crm, sc)
+    g.step(sc.dt, 1)
+    o2 = oracle.load_scenario(sc)       # the structure the GPU step built: from the initial state
+    so = o2.structure()
+    nf = sc.n_fluid
+    assert g.pair_count() == int(so["counts"][:nf].sum())
+    cs = so["cell_start"].astype(np.int64)
+    occ = np.diff(cs)
+    p = sc.params
+    dims = [int(np.ceil((p["hi"][a] - p["lo"][a]) / (2 * p["h"]))) for a in range(3)]
+    occ3 = occ.reshape(dims)
+    pad = np.pad(occ3, 1)
+    s27 = sum(pad[1 + a:1 + a + dims[0], 1 + b:1 + b + dims[1], 1 + c:1 + c + dims[2]]
+              for a in (-1, 0, 1) for b in (-1, 0, 1) for c in (-1, 0, 1)).ravel()
+    cand = s27[so["cell"]] - 1
+    f, m = g.candidate_count()
+    assert f == int(cand[:nf].sum()) and m == int(cand[nf:].sum())

@@ -271,6 +271,64 @@ def mgru3_bin(d0=1e-2, n=(500, 80, 25), dt=2.5e-4, steps=100) -> Scenario:
     return Scenario("mgru3_bin", p, f32(pos), None, None, f32(walls), [], dt, steps, meta=dict(n=n))
 
 
+def cone_markers(apex_deg: float, R: float, d0: float, layers: int) -> np.ndarray:
+    """BCE markers of a solid cone, apex at the origin pointing down (-z), axis +z, base radius R
+    at height L = R / tan(apex/2): layer k is the lateral surface moved inward by k d0 (a copy
+    shifted up the axis by k d0 / sin(apex/2)) plus the base disk at L - k d0; rings at slant
+    spacing ~d0, ~d0 along each ring (P:467 'first layer on the surface')."""
+    half = math.radians(apex_deg) / 2.0
+    L = R / math.tan(half)
+    out = [np.zeros((1, 3))]                       # the apex itself
+    for k in range(layers):
+        z0 = k * d0 / math.sin(half)               # apex of the k-th inward surface
+        slant = (L - z0) / math.cos(half)
+        for j in range(1 if k == 0 else 0, int(slant / d0) + 1):
+            s = j * d0
+            r, z = s * math.sin(half), z0 + s * math.cos(half)
+            if z > L - k * d0 + 1e-12 or r <= 0.0:
+                continue
+            nt = max(3, int(round(2 * math.pi * r / d0)))
+            th = (np.arange(nt) + 0.5 * (j % 2)) * (2 * math.pi / nt)
+            out.append(np.stack([r * np.cos(th), r * np.sin(th), np.full(nt, z)], -1))
+        zb = L - k * d0                             # base disk of layer k
+        rb = (zb - z0) * math.tan(half) - 0.5 * d0
+        for ir in range(int(rb / d0) + 1):
+            r = ir * d0
+            nt = 1 if r == 0 else int(round(2 * math.pi * r / d0))
+            th = np.arange(nt) * (2 * math.pi / nt)
+            out.append(np.stack([r * np.cos(th), r * np.sin(th), np.full(nt, zb)], -1))
+    return np.concatenate(out, axis=0)
+
+
+def cone_drop(apex_deg=60.0, diameter=19.8e-3, H_over_L=0.0, n=(100, 100, 100), d0=1e-3, dt=2e-5,
+              steel=7850.0) -> Scenario:
+    """the cone penetration test of P:65–104 on the C3 glass-bead bed: a
+    60 deg / 19.8 mm cone (30 deg / 9.2 mm for Ottawa sand) dropped with its tip at the surface and
+    the speed of a fall from H = 0, L/2 or L (v = sqrt(2 g H)).  The cone's mass is not printed:
+    a solid steel cone (reading A32).  Translation along z only (dof_mask = 4)."""
+    sc = cone_bed(d0=d0, n=n, dt=dt)
+    nx, ny, nz = n
+    R = 0.5 * diameter
+    half = math.radians(apex_deg) / 2.0
+    L = R / math.tan(half)
+    mass = steel * math.pi * R * R * L / 3.0
+    tip = np.array([0.5 * nx * d0, 0.5 * ny * d0, nz * d0 + 0.5 * d0])
+    com = tip + np.array([0.0, 0.0, 0.75 * L])    # centroid of a solid cone: 3L/4 from the apex
+    local = cone_markers(apex_deg, R, d0, bce_layers(sc.params["h"], d0))
+    I_ax = 0.3 * mass * R * R
+    I_tr = mass * (0.15 * R * R + 0.0375 * L * L)
+    v0 = math.sqrt(2 * 9.81 * H_over_L * L)
+    b = Body(mass=mass, inertia=(I_tr, I_tr, I_ax), pos=tuple(com), vel=(0.0, 0.0, -v0),
+             motion=BODY_FREE, dof_mask=4, markers=f32(local + tip))
+    hi = list(sc.params["hi"])
+    hi[2] = max(hi[2], tip[2] + L + 4 * d0)
+    sc.params["hi"] = tuple(hi)
+    sc.bodies = [b]
+    sc.name = f"cone{int(apex_deg)}_H{H_over_L:g}L"
+    sc.meta.update(cone_L=L, cone_R=R, tip0=tip.tolist(), com0=com.tolist(), mass=mass)
+    return sc
+
+
 def cylinder_markers(R: float, width: float, d0: float, layers: int) -> np.ndarray:
     """BCE markers of a wheel rim: cylindrical shells r = R - k d0 (k < layers) about the body y
     axis, spacing ~d0 along the arc and the width."""
