@@ -341,7 +341,8 @@ def load_scenario(sc) -> OracleSim:
         s.add_bce(0, sc.wall_pos)
     for b in sc.bodies:
         bid = s.add_body(b)
-        s.add_bce(bid, b.markers)
+        if b.markers.shape[0]:
+            s.add_bce(bid, b.markers)
     act = getattr(sc, "active", None) or {}
     for body, half in act.get("boxes", {}).items():
         s.set_active_box(body, half)

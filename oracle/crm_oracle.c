@@ -657,7 +657,11 @@ int oc_get_activity(const oc_sim* s, uint8_t* flags) {
   return OC_OK;
 }
 
-static int inactive(const structure_t* st, int64_t i) { return st->act && st->act[i] == OC_INACTIVE; }
+/* Alg. 3, reading A31: only Active particles are updated.  "SPH particles outside active boxes are
+ * deactivated ... their states are not updated"; the Extended-Active ones (outside the box,
+ * within 2h of it) are kept "to ensure their data is available for these calculations":
+ * they are neighbours of Active particles, but their own state (fluid y; marker u, sigma) is frozen. */
+static int frozen(const structure_t* st, int64_t i) { return st->act && st->act[i] != OC_ACTIVE; }
 
 /* ---- BCE extrapolation, Adami + stress (reading A12) ---- */
 static void bce_extrapolate(const oc_sim* s, const structure_t* st, const double* x, const double* u,
@@ -668,7 +672,7 @@ static void bce_extrapolate(const oc_sim* s, const structure_t* st, const double
   #pragma omp parallel for schedule(dynamic, 256)
   for (int64_t a = 0; a < s->n; ++a) {
     if (s->kind[a] != OC_BCE) continue;
-    if (inactive(st, a)) {   /* Alg. 3: "their states are not updated" */
+    if (frozen(st, a)) {   /* Alg. 3: "their states are not updated", A31 */
       for (int c = 0; c < 3; ++c) u_out[3 * a + c] = u[3 * a + c];
       for (int c = 0; c < 6; ++c) sig_out[6 * a + c] = sig[6 * a + c];
       continue;
@@ -720,7 +724,7 @@ static void rates(const oc_sim* s, const structure_t* st, const double* x, const
     for (int c = 0; c < 10; ++c) o[c] = 0.0;
     const int is_fluid = s->kind[i] == OC_FLUID;
     if (!is_fluid && (s->body[i] <= 0 || s->bodies[s->body[i]].b.motion == OC_BODY_FIXED)) continue;
-    if (inactive(st, i)) continue;                                    /* Alg. 3: no RHS */
+    if (frozen(st, i)) continue;                                      /* Alg. 3, A31: no RHS */
     double L[9] = {0}, cont = 0.0, mom[3] = {0, 0, 0}, Pi[3] = {0, 0, 0};
     for (int64_t k = st->offset[i]; k < st->offset[i + 1]; ++k) {
       const int64_t j = st->list[k];
@@ -836,8 +840,9 @@ static int step_once(oc_sim* s, double dt) {
   for (int64_t i = 0; i < n; ++i) {
     const double* f = &s->rates[0][10 * i];
     if (s->kind[i] == OC_FLUID) {
+      const double hx = frozen(&st, i) ? 0.0 : 0.5 * dt;   /* A31: a frozen particle stays put */
       for (int c = 0; c < 3; ++c) {
-        xm[3 * i + c] = s->x[3 * i + c] + 0.5 * dt * s->u[3 * i + c];
+        xm[3 * i + c] = s->x[3 * i + c] + hx * s->u[3 * i + c];
         um[3 * i + c] = s->u[3 * i + c] + 0.5 * dt * f[1 + c];
       }
       rm[i] = s->rho[i] + 0.5 * dt * f[0];
@@ -873,7 +878,7 @@ static int step_once(oc_sim* s, double dt) {
   /* ---- y_{n+1} = y_n + dt f(t_n + dt/2, y_mid), then the return map on sigma* ---- */
   #pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < n; ++i) {
-    if (s->kind[i] != OC_FLUID || inactive(&st, i)) continue;   /* Inactive: frozen (Alg. 3) */
+    if (s->kind[i] != OC_FLUID || frozen(&st, i)) continue;     /* Extended/Inactive: frozen (A31) */
     const double* f = &s->rates[1][10 * i];
     double sig_star[6], sig_new[6];
     for (int c = 0; c < 3; ++c) {

@@ -6,6 +6,9 @@
 // Inactive particles then get the sentinel key M in k_bin: they sort behind every cell (the active
 // set is the prefix [0, N_{a+e}) of the sorted arrays), take no part in the neighbour search and
 // are not touched by the tile kernels, so their state stays frozen until a box reaches them again.
+// Extended-Active particles carry TAG_FROZEN (reading A31): they are staged, searched and serve as
+// neighbours of Active ones ("to ensure their data is available"), but their own state —
+// fluid y, marker u and sigma — is not updated ("their states are not updated").
 #pragma once
 #include <cmath>
 #include "common.cuh"
@@ -24,7 +27,7 @@ struct ActiveBox {
 // Euclidean distance < 2h from one, else Inactive; fp64 on the compensated position hi + lo.
 // Markers of moving bodies are always Active.
 __global__ void k_activity(int n, const float4* __restrict__ P, const float4* __restrict__ L,
-                           const float4* __restrict__ U, const uint32_t* __restrict__ ids,
+                           float4* __restrict__ U, const uint32_t* __restrict__ ids,
                            const BodyState* __restrict__ bodies, const ActiveBox* __restrict__ boxes, int nbox,
                            double radius, uint8_t* __restrict__ act_slot, uint8_t* __restrict__ act_id,
                            unsigned long long* __restrict__ counts) {
@@ -67,6 +70,12 @@ __global__ void k_activity(int n, const float4* __restrict__ P, const float4* __
     }
     act_slot[i] = (uint8_t)f;
     act_id[ids[i]] = (uint8_t)f;
+    float4 u = U[i];
+    const uint32_t t2 = f == ACT_EXTENDED ? (tag | TAG_FROZEN) : (tag & ~TAG_FROZEN);
+    if (t2 != tag) {
+      u.w = __uint_as_float(t2);
+      U[i] = u;
+    }
   }
   // ComputeActiveCount: warp-aggregated
   const int lane = threadIdx.x & 31;

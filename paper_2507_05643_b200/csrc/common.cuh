@@ -22,13 +22,16 @@ __host__ __device__ __forceinline__ uint32_t make_tag(uint32_t kind, uint32_t bo
 }
 //   bit 17     : ghost copy of a neighbour slab's particle (multi-GPU)
 //   bit 18     : dropped at the next sort (migrated to a neighbour slab)
+//   bit 19     : Extended-Active particle of Alg. 3 (reading A31): a neighbour only, state frozen
 constexpr uint32_t TAG_GHOST = 1u << 17;
 constexpr uint32_t TAG_DROP = 1u << 18;
+constexpr uint32_t TAG_FROZEN = 1u << 19;
 __device__ __forceinline__ uint32_t tag_of(float w) { return __float_as_uint(w); }
 __device__ __forceinline__ bool tag_is_bce(uint32_t t) { return t & 1u; }
 __device__ __forceinline__ uint32_t tag_body(uint32_t t) { return (t >> 1) & 0x7fffu; }
 __device__ __forceinline__ bool tag_moving(uint32_t t) { return (t >> 16) & 1u; }
 __device__ __forceinline__ bool tag_ghost(uint32_t t) { return (t & TAG_GHOST) != 0u; }
+__device__ __forceinline__ bool tag_frozen(uint32_t t) { return (t & TAG_FROZEN) != 0u; }
 
 // fixed grid (reading A19); cells of size s = support*h
 struct Grid {
@@ -90,9 +93,12 @@ __device__ __forceinline__ float kernel_F(float r, float rinv, const Phys& ph) {
     const float t = fmaf(-0.5f * ph.hinv, r, 1.0f);
     return ph.wd_f * t * t * t;
   } else {
-    // cubic spline (A1): kin_a r + kin_b for r < h, kout (2 - r/h)^2 / r otherwise
+    // cubic spline (A1): kin_a r + kin_b for r < h, kout (2 - r/h)^2 / r otherwise; both pieces
+    // are evaluated and selected (no branch: the pair loops stay straight-line code)
     const float t = fmaf(-ph.hinv, r, 2.0f);
-    return (r < ph.h) ? fmaf(ph.kin_a, r, ph.kin_b) : ph.kout * t * t * rinv;
+    const float f_in = fmaf(ph.kin_a, r, ph.kin_b);
+    const float f_out = (ph.kout * rinv) * (t * t);
+    return (r < ph.h) ? f_in : f_out;
   }
 }
 

@@ -158,13 +158,16 @@ int commit(crm_t* c) {
   mstart.push_back((uint32_t)mids.size());
   c->n_moving_markers = (int)mids.size();
   c->n_moving_bodies = (int)mb.size();
-  if (c->n_moving_markers) {
-    if (dalloc(c, &c->d_moving_ids, mids.size()) || dalloc(c, &c->d_xlocal, xl.size()) ||
+  if (c->n_moving_bodies) {   // (a moving body may carry no markers: an active-box carrier)
+    mids.reserve(1); xl.reserve(1);
+    if (dalloc(c, &c->d_moving_ids, std::max<size_t>(mids.size(), 1)) || dalloc(c, &c->d_xlocal, std::max<size_t>(xl.size(), 1)) ||
         dalloc(c, &c->d_mstart, mstart.size()) || dalloc(c, &c->d_moving_bodies, mb.size()) ||
         dalloc(c, &c->macc, n) || dalloc(c, &c->d_bpart, (size_t)c->world * mb.size() * 6))
       return CRM_E_OOM;
-    CK(cudaMemcpyAsync(c->d_moving_ids, mids.data(), mids.size() * 4, cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(c->d_xlocal, xl.data(), xl.size() * 16, cudaMemcpyHostToDevice, c->stream));
+    if (!mids.empty()) {
+      CK(cudaMemcpyAsync(c->d_moving_ids, mids.data(), mids.size() * 4, cudaMemcpyHostToDevice, c->stream));
+      CK(cudaMemcpyAsync(c->d_xlocal, xl.data(), xl.size() * 16, cudaMemcpyHostToDevice, c->stream));
+    }
     CK(cudaMemcpyAsync(c->d_mstart, mstart.data(), mstart.size() * 4, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->d_moving_bodies, mb.data(), mb.size() * 4, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemsetAsync(c->macc, 0, n * sizeof(float4), c->stream));
@@ -240,7 +243,7 @@ void issue_sort(crm_t* c, long long step, uint32_t drop_mask) {
   if (act) {
     cudaMemsetAsync(c->d_actcnt, 0, 3 * sizeof(unsigned long long), c->stream);
     launch(c, KID_ACTIVITY, k_activity, dim3(blocks(n, 256)), dim3(256), n, (const float4*)c->P[a],
-           (const float4*)c->L[a], (const float4*)c->U[a], (const uint32_t*)c->ids[a], (const BodyState*)c->d_bodies,
+           (const float4*)c->L[a], c->U[a], (const uint32_t*)c->ids[a], (const BodyState*)c->d_bodies,
            (const ActiveBox*)c->d_boxes, (int)c->boxes.size(), c->support * (double)c->ker.h, c->d_act, c->d_act_id,
            c->d_actcnt);
   }
@@ -399,9 +402,10 @@ void issue_body_finish(crm_t* c, float dt) {
   launch(c, KID_POSES, k_body_poses, dim3(1), dim3(64), (int)c->bodies.size(), (const BodyState*)c->d_bodies,
          0.5 * (double)dt, c->d_pose0, c->d_posem);
   const int y = c->cur;
-  launch(c, KID_MARKERS, k_markers_place, dim3(blocks(c->n_moving_markers, 128)), dim3(128), c->n_moving_markers,
-         (const uint32_t*)c->d_moving_ids, (const float4*)c->d_xlocal, (const uint32_t*)c->slot_of_id,
-         (const Pose*)c->d_pose0, c->P[y], c->L[y], (const float4*)c->U[y]);
+  if (c->n_moving_markers)
+    launch(c, KID_MARKERS, k_markers_place, dim3(blocks(c->n_moving_markers, 128)), dim3(128), c->n_moving_markers,
+           (const uint32_t*)c->d_moving_ids, (const float4*)c->d_xlocal, (const uint32_t*)c->slot_of_id,
+           (const Pose*)c->d_pose0, c->P[y], c->L[y], (const float4*)c->U[y]);
 }
 
 int issue_step(crm_t* c, float dt, long long step) {

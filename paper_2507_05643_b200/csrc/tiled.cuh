@@ -18,17 +18,33 @@
 namespace crmk {
 
 // ---------------------------------------------------------------------------------------
-// neighbour state at window offset `off`; positions relative to the tile origin (see rel_pos)
+// neighbour state at list entry `e` (16 x window offset when staged, the offset in global mode); positions relative to the tile origin
+// (see rel_pos), .w = rho_j (the BCE window keeps densities)
 template <bool STAGED>
 __device__ __forceinline__ void load_all(const TileSmem& sm, const float4* __restrict__ P, const float4* __restrict__ L,
                                          const float4* __restrict__ U, const float4* __restrict__ S1,
-                                         const float2* __restrict__ S2, uint32_t off, float4& p, float4& u, float4& s1,
+                                         const float2* __restrict__ S2, uint32_t e, float4& p, float4& u, float4& s1,
                                          float2& s2) {
   if (STAGED) {
-    p = sm.P[off]; u = sm.U[off]; s1 = sm.S1[off]; s2 = sm.S2[off];
+    p = win_P(sm, e); u = win_U(sm, e); s1 = win_S1(sm, e); s2 = win_S2(sm, e);
   } else {
-    const uint32_t g = window_to_global(sm, off);
+    const uint32_t g = window_to_global(sm, e);
     p = rel_pos(P[g], L[g], sm); u = U[g]; s1 = S1[g]; s2 = S2[g];
+  }
+}
+
+// the same for the rates pair loops: .w = the signed volume V_j (see tile_relativize<true>)
+template <bool STAGED>
+__device__ __forceinline__ void load_rates(const TileSmem& sm, const float4* __restrict__ P, const float4* __restrict__ L,
+                                           const float4* __restrict__ U, const float4* __restrict__ S1,
+                                           const float2* __restrict__ S2, uint32_t e, float m, float4& p, float4& u,
+                                           float4& s1, float2& s2) {
+  if (STAGED) {
+    p = win_P(sm, e); u = win_U(sm, e); s1 = win_S1(sm, e); s2 = win_S2(sm, e);
+  } else {
+    const uint32_t g = window_to_global(sm, e);
+    p = rel_pos(P[g], L[g], sm); u = U[g]; s1 = S1[g]; s2 = S2[g];
+    p.w = signed_volume(p.w, u.w, m);
   }
 }
 
@@ -75,7 +91,8 @@ __device__ __forceinline__ void filter_range(const Grid& g, const TileSmem& sm, 
     cnt += __popc(m);
     uint32_t s = STORE_BCE ? m : mf;
     while (s) {   // (measured: branch-free funnel-shift appends beat paired/branchy appends)
-      w.push(base + (__ffs(s) - 1));
+      const uint32_t off = base + (__ffs(s) - 1);
+      w.push(STAGED ? off << 4 : off);   // list entry: byte offset of the staged slot (global mode: the offset)
       s &= s - 1;
     }
   }
@@ -125,7 +142,7 @@ __device__ __forceinline__ void build_lists(const Grid& g, const TileSmem& sm, c
     ListWriter w;
     w.init(list, i, cap);
     const uint32_t cnt = filter<STAGED, STORE_BCE>(g, sm, P, U, q, cz, self, P[i], w);
-    w.flush(self);
+    w.flush(STAGED ? self << 4 : self);
     nlist[i] = (uint32_t)min(w.k, cap);
     count_all[i] = cnt;
     if (w.k > cap) latch_error(err, -9 /*CRM_E_CAPACITY*/, (long long)ids[i], step, (long long)w.k);
@@ -146,6 +163,14 @@ __device__ __forceinline__ void bce_tile(const Phys& ph, TileSmem& sm, const flo
     const float4 ui = U[i];
     const uint32_t tag = tag_of(ui.w);
     if (!tag_is_bce(tag)) continue;
+    if (tag_frozen(tag)) {   // Extended-Active marker (A31): keeps its extrapolated values
+      if (dbg_on) {
+        dbg.bu[STAGE][i] = ui;
+        dbg.bs1[STAGE][i] = S1[i];
+        dbg.bs2[STAGE][i] = S2[i];
+      }
+      continue;
+    }
     const float4 pabs = P[i];
     const float4 pa = rel_pos(pabs, L[i], sm);
     const uint32_t nl = nlist[i];
@@ -241,7 +266,7 @@ __global__ void TILE_BOUNDS
     }
     __syncthreads();
   }
-  tile_relativize(L, sm);
+  tile_relativize<false>(L, sm, 0.f);
   __syncthreads();
   if (sm.staged) bce_tile<STAGE, KER, true>(ph, sm, P, L, U, S1, S2, list, nlist, pose, cap, dbg, dbg_on);
   else bce_tile<STAGE, KER, false>(ph, sm, P, L, U, S1, S2, list, nlist, pose, cap, dbg, dbg_on);
@@ -252,37 +277,40 @@ struct PairAcc {
   float L[9], Gs[3], Ms[3], Pi[3];
 };
 
+// One directed pair (i, j).  pj.w = signed V_j (+ fluid, - marker).  Branch-free: an invalid pair
+// (r >= 2h, A17; r = 0 incl. the self padding, A18; a marker when only fluid counts) gets w = 0, hence
+// a zero contribution to every sum.  Two MUFU per pair (rsqrt, one reciprocal for the AV).
 template <int KER>
 __device__ __forceinline__ void pair_terms(PairAcc& A, const Phys& ph, const float4& pi, const float4& ui,
                                            const float4& pj, const float4& uj, const float4& sj1, const float2& sj2,
-                                           bool with_L, bool okj) {
+                                           bool with_L, bool fluid_only) {
   const float dx = pi.x - pj.x, dy = pi.y - pj.y, dz = pi.z - pj.z;   // x_ij = x_i - x_j
-  const float r2 = dx * dx + dy * dy + dz * dz;
-  // branch-free: invalid pairs (r >= 2h, A17; r = 0 incl. the self padding, A18; a marker when
-  // only fluid counts) get F = 0, hence a zero contribution to every sum
-  const bool ok = r2 < ph.R2 && r2 > 0.f && okj;
+  const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+  const float Vj = fabsf(pj.w);
+  const bool ok = r2 < ph.R2 && r2 > 0.f && (!fluid_only || pj.w > 0.f);
   const float rinv = rsqrt_approx(r2);
-  const float r = r2 * rinv;
-  const float F = ok ? kernel_F<KER>(r, rinv, ph) : 0.f;   // W'(r)/r (A1 / A28)
-  const float w = ph.m * rcp_approx(pj.w) * F;                         // V_j W'/r (A7)
+  const float F = kernel_F<KER>(r2 * rinv, rinv, ph);                 // W'(r)/r (A1 / A28)
+  const float w = ok ? Vj * F : 0.f;                                   // V_j W'/r (A7)
   const float gx = w * dx, gy = w * dy, gz = w * dz;                  // V_j grad_i W_ij
   const float dux = uj.x - ui.x, duy = uj.y - ui.y, duz = uj.z - ui.z; // u_ji
   if (with_L) {   // velocity gradient L_ab += V_j u_ji,a gradW_b (F2, A4)
-    A.L[0] += dux * gx; A.L[1] += dux * gy; A.L[2] += dux * gz;
-    A.L[3] += duy * gx; A.L[4] += duy * gy; A.L[5] += duy * gz;
-    A.L[6] += duz * gx; A.L[7] += duz * gy; A.L[8] += duz * gz;
+    A.L[0] = fmaf(dux, gx, A.L[0]); A.L[1] = fmaf(dux, gy, A.L[1]); A.L[2] = fmaf(dux, gz, A.L[2]);
+    A.L[3] = fmaf(duy, gx, A.L[3]); A.L[4] = fmaf(duy, gy, A.L[4]); A.L[5] = fmaf(duy, gz, A.L[5]);
+    A.L[6] = fmaf(duz, gx, A.L[6]); A.L[7] = fmaf(duz, gy, A.L[7]); A.L[8] = fmaf(duz, gz, A.L[8]);
   }
   // F3 momentum: sum V_j (sigma_i + sigma_j) gradW = sigma_i sum V_j gradW + sum V_j sigma_j gradW
   A.Gs[0] += gx; A.Gs[1] += gy; A.Gs[2] += gz;
-  A.Ms[0] += sj1.x * gx + sj1.w * gy + sj2.x * gz;
-  A.Ms[1] += sj1.w * gx + sj1.y * gy + sj2.y * gz;
-  A.Ms[2] += sj2.x * gx + sj2.y * gy + sj1.z * gz;
-  // artificial viscosity (Eq. 13/14, sign of reading A9): v_ij . r_ij with v_ij = u_i - u_j
-  const float vr = -(dux * dx + duy * dy + duz * dz);
-  // gamma_a h c_s (m_j / rho_bar_ij) (v_ij . r_ij) / (r^2 + xi^2) W'/r, rho_bar = (rho_i + rho_j)/2
-  const float cv = ph.c_av * vr * F * rcp_approx((pi.w + pj.w) * (r2 + ph.xi2));
+  A.Ms[0] = fmaf(sj1.x, gx, fmaf(sj1.w, gy, fmaf(sj2.x, gz, A.Ms[0])));
+  A.Ms[1] = fmaf(sj1.w, gx, fmaf(sj1.y, gy, fmaf(sj2.y, gz, A.Ms[1])));
+  A.Ms[2] = fmaf(sj2.x, gx, fmaf(sj2.y, gy, fmaf(sj1.z, gz, A.Ms[2])));
+  // artificial viscosity (Eq. 13/14, sign of reading A9): v_ij . r_ij with v_ij = u_i - u_j;
+  // gamma_a h c_s (m_j / rho_bar_ij) (v_ij . r_ij) / (r^2 + xi^2) W'/r with rho_bar = (rho_i + rho_j)/2
+  // and rho_j = m / V_j:  m / rho_bar = 2 m V_j / (rho_i V_j + m)  (c_av holds 2 m gamma_a h c_s)
+  const float vr = -fmaf(duz, dz, fmaf(duy, dy, dux * dx));
+  const float den = fmaf(pi.w, Vj, ph.m) * (r2 + ph.xi2);
+  const float cv = (ph.c_av * vr) * (w * rcp_approx(den));
   const float coef = (!ph.unilateral || vr < 0.f) ? cv : 0.f;
-  A.Pi[0] += coef * dx; A.Pi[1] += coef * dy; A.Pi[2] += coef * dz;
+  A.Pi[0] = fmaf(coef, dx, A.Pi[0]); A.Pi[1] = fmaf(coef, dy, A.Pi[1]); A.Pi[2] = fmaf(coef, dz, A.Pi[2]);
 }
 
 template <int KER, bool STAGED>
@@ -304,8 +332,8 @@ __device__ __forceinline__ void pair_loop(PairAcc& A, const Phys& ph, const Tile
       float4 pj, uj, s1;
       float2 s2;
       // (measured: making these gathers bank-conflict free would gain only ~10 % in stage B)
-      load_all<STAGED>(sm, P, L, U, S1, S2, list_entry(v, e), pj, uj, s1, s2);
-      pair_terms<KER>(A, ph, pi, ui, pj, uj, s1, s2, with_L, !(fluid_only && tag_is_bce(tag_of(uj.w))));
+      load_rates<STAGED>(sm, P, L, U, S1, S2, list_entry(v, e), ph.m, pj, uj, s1, s2);
+      pair_terms<KER>(A, ph, pi, ui, pj, uj, s1, s2, with_L, fluid_only);
     }
   }
 }
@@ -329,6 +357,18 @@ __device__ __forceinline__ void rates_tile(const Phys& ph, float dt, TileSmem& s
     const uint32_t tag = tag_of(ui.w);
     const bool bce = tag_is_bce(tag);
     if (bce && !(STAGE == 1 && tag_moving(tag))) continue;
+    if (tag_frozen(tag)) {   // Extended-Active fluid (A31): a neighbour only, y_mid = y_{n+1} = y_n
+      if (STAGE == 0) {
+        YP[i] = P[i]; YL[i] = L[i]; YU[i] = ui; YS1[i] = S1[i]; YS2[i] = S2[i];
+      }
+      if (dbg_on) {
+        dbg.drho[STAGE][i] = 0.f;
+        dbg.acc[STAGE][i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        dbg.ds1[STAGE][i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        dbg.ds2[STAGE][i] = make_float2(0.f, 0.f);
+      }
+      continue;
+    }
     const float4 pi = rel_pos(P[i], L[i], sm);
     const uint32_t nl = nlist[i];
     PairAcc A;
@@ -457,7 +497,9 @@ __global__ void TILE_BOUNDS
     } else if (STAGE == 0) {
       YP[i] = P[i];     // markers: x at t_n (moving ones are re-placed at t_n + dt/2 afterwards)
       YL[i] = L[i];
-      YU[i] = ui;       // tag; u and sigma are replaced by the stage-B extrapolation
+      YU[i] = ui;       // tag; u and sigma are replaced by the stage-B extrapolation (frozen
+      YS1[i] = S1[i];   // Extended-Active markers keep these copies, A31)
+      YS2[i] = S2[i];
     } else {
       YU[i] = ui;       // y_{n+1} of a marker: its stage-B extrapolated u and sigma
       YS1[i] = S1[i];
@@ -479,7 +521,7 @@ __global__ void TILE_BOUNDS
     else build_lists<false, true>(g, sm, P, U, list, nlist, count_all, cell_of, cap, err, ids, step, is_fluid);
     __syncthreads();
   }
-  tile_relativize(L, sm);
+  tile_relativize<true>(L, sm, ph.m);
   __syncthreads();
   if (sm.staged)
     rates_tile<STAGE, KER, true>(ph, dt, sm, P, L, U, S1, S2, YP, YL, YU, YS1, YS2, list, nlist, cap, macc, dbg, dbg_on,
@@ -518,7 +560,7 @@ __global__ void k_decode_lists(int n, Grid g, const uint32_t* __restrict__ cell_
   rb[WR] = acc;
   uint32_t kk = 0;
   for (uint32_t k = 0; k < nlist[i]; ++k) {
-    const uint32_t off = list[(size_t)i * cap + k];
+    const uint32_t off = acc <= (uint32_t)WMAX ? list[(size_t)i * cap + k] >> 4 : list[(size_t)i * cap + k];
     int r = 0;
     for (int q = 1; q < WR; ++q) r += (rb[q] <= off) ? 1 : 0;
     const uint32_t j = rs[r] + (off - rb[r]);

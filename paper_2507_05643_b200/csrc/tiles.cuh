@@ -5,9 +5,10 @@
 // particle of the 27-cell neighbourhoods of the tile's particles — is WR = (TX+2)(TY+2)
 // contiguous runs.  One CTA per tile stages the window's 56-B states into shared memory once,
 // filters candidates there (Alg. 1) and runs the pair loops from shared memory.
-// Neighbour lists store 16-bit window offsets (list entry = position in the tile window), per
-// particle contiguous (cap entries, 16-B aligned chunks of 8), so they are read and written
-// with 16-B vector accesses.  Windows larger than WMAX are read from global memory instead
+// Neighbour lists store 16-bit window BYTE offsets (list entry = 16 x position in the tile window,
+// so a pair loop addresses the staged float4 arrays with no index arithmetic; global mode stores the
+// plain position, windows up to 65535 particles), per particle
+// contiguous (cap entries, 16-B aligned chunks of 8), read and written with 16-B vector accesses.  Windows larger than WMAX are read from global memory instead
 // (same list format, slower; "global mode").
 #pragma once
 #include <cuda_pipeline.h>
@@ -165,8 +166,19 @@ __device__ __forceinline__ float4 rel_pos(const float4& hi, const float4& lo, co
   return make_float4((hi.x - sm.ox) + lo.x, (hi.y - sm.oy) + lo.y, (hi.z - sm.oz) + lo.z, hi.w);
 }
 
-// convert the staged window from absolute hi to relative compensated positions (after the filter)
-__device__ __forceinline__ void tile_relativize(const float4* __restrict__ L, TileSmem& sm) {
+// signed neighbour volume carried in the .w slot of a rates window: +m/rho for fluid, -m/rho for
+// markers (A7, A8: markers are ordinary neighbours with V = m/rho0; the sign lets the marker-load
+// loop keep fluid neighbours only without reading the tag)
+__device__ __forceinline__ float signed_volume(float rho, float tagw, float m) {
+  const float V = __fdiv_rn(m, rho);
+  return tag_is_bce(tag_of(tagw)) ? -V : V;
+}
+
+// convert the staged window from absolute hi to relative compensated positions (after the filter);
+// TO_V: the rates kernels also replace rho_j by the signed volume V_j (one division per staged
+// particle instead of one reciprocal per pair)
+template <bool TO_V>
+__device__ __forceinline__ void tile_relativize(const float4* __restrict__ L, TileSmem& sm, float m) {
   if (!sm.staged) return;
   const uint32_t W = sm.run_base[WR];
   for (uint32_t idx = threadIdx.x; idx < W; idx += blockDim.x) {
@@ -174,8 +186,24 @@ __device__ __forceinline__ void tile_relativize(const float4* __restrict__ L, Ti
 #pragma unroll
     for (int k = 1; k < WR; ++k) r += (sm.run_base[k] <= idx) ? 1 : 0;
     const uint32_t gidx = sm.run_start[r] + (idx - sm.run_base[r]);
-    sm.P[idx] = rel_pos(sm.P[idx], L[gidx], sm);
+    float4 p = rel_pos(sm.P[idx], L[gidx], sm);
+    if (TO_V) p.w = signed_volume(p.w, sm.U[idx].w, m);
+    sm.P[idx] = p;
   }
+}
+
+// staged window entries by list entry (byte offset of the float4 slot)
+__device__ __forceinline__ float4 win_P(const TileSmem& sm, uint32_t e) {
+  return *reinterpret_cast<const float4*>(reinterpret_cast<const char*>(sm.P) + e);
+}
+__device__ __forceinline__ float4 win_U(const TileSmem& sm, uint32_t e) {
+  return *reinterpret_cast<const float4*>(reinterpret_cast<const char*>(sm.U) + e);
+}
+__device__ __forceinline__ float4 win_S1(const TileSmem& sm, uint32_t e) {
+  return *reinterpret_cast<const float4*>(reinterpret_cast<const char*>(sm.S1) + e);
+}
+__device__ __forceinline__ float2 win_S2(const TileSmem& sm, uint32_t e) {
+  return *reinterpret_cast<const float2*>(reinterpret_cast<const char*>(sm.S2) + (e >> 1));
 }
 
 // compensated update (hi, lo) += d  (Fast2Sum; |hi| >= |lo + d| for any step an SPH particle takes)
@@ -186,7 +214,7 @@ __device__ __forceinline__ void comp_add(float& hi, float& lo, float d) {
   hi = t;
 }
 
-// global index of a window offset (global mode)
+// global index of a window offset (global mode, where list entries are plain offsets)
 __device__ __forceinline__ uint32_t window_to_global(const TileSmem& sm, uint32_t off) {
   int r = 0;
 #pragma unroll

@@ -4,8 +4,8 @@
   Grow -> 1440, Keep, Shrink -> 700 with the paper's constants G = 1.2, S = 0.75, S_I = 50.
 * UpdateActivity: inside -> Active, face + 1.5h -> Extended-Active, face + 2.5h -> Inactive (S:485);
   the Euclidean distance to the box decides at corners (A29); the box turns with its body.
-* Full coverage is bit-identical to the feature off; an Inactive particle keeps exactly its
-  frozen state and re-enters with it (S:507); inactive particles have no neighbours and no rates;
+* Full coverage is bit-identical to the feature off; an Inactive or Extended-Active particle
+  keeps exactly its frozen state (A31) and re-enters with it (S:507); inactive particles have no neighbours and no rates;
   the active set's structure equals brute force on that subset; t_delay gates the feature (Alg. 3)."""
 import numpy as np
 import pytest
@@ -93,15 +93,17 @@ def test_inactive_particles_are_frozen_and_reenter(oracle_mod):
     assert (f1 == 0).any() and (f1 == 1).any() and (f1 == 2).any()
     x1, u1, r1, s1 = [a[:nf] for a in o.get_state()]
     ina = f1 == 2
-    # frozen: exactly the initial state
-    assert np.array_equal(x1[ina], x0[ina]) and np.array_equal(u1[ina], u0[ina])
-    assert np.array_equal(r1[ina], r0[ina]) and np.array_equal(s1[ina], s0[ina])
-    # the processed set moved (gravity acts on every active/extended particle)
-    assert np.all(u1[~ina] != u0[~ina])
-    # rates: zero on inactive particles, full RHS on Extended-Active ones (A31)
-    d, acc, ds = o.last_rates(0)
-    assert np.all(acc[:nf][ina] == 0) and np.all(d[:nf][ina] == 0)
-    assert np.all(np.abs(acc[:nf][f1 == 1]).sum(axis=1) > 0)
+    fro = f1 != 0
+    # frozen: Inactive and Extended-Active particles keep exactly the initial state (A31)
+    assert np.array_equal(x1[fro], x0[fro]) and np.array_equal(u1[fro], u0[fro])
+    assert np.array_equal(r1[fro], r0[fro]) and np.array_equal(s1[fro], s0[fro])
+    # the Active set moved (gravity acts on every one of them)
+    assert np.all(u1[~fro] != u0[~fro])
+    # rates: zero outside the Active set (A31)
+    for stage in (0, 1):
+        d, acc, ds = o.last_rates(stage)
+        assert np.all(acc[:nf][fro] == 0) and np.all(d[:nf][fro] == 0) and np.all(ds[:nf][fro] == 0)
+        assert np.all(np.abs(acc[:nf][~fro]).sum(axis=1) > 0)
     # the box travels 0.5 m/s: after enough steps a particle ahead of it re-enters
     ahead = np.nonzero(ina & (x0[:, 0] > x0[:, 0].min() + 0.5 * (x0[:, 0].max() - x0[:, 0].min())))[0]
     steps = 0
@@ -109,7 +111,7 @@ def test_inactive_particles_are_frozen_and_reenter(oracle_mod):
         o.step(sc.dt, 10)
         steps += 10
         f = o.activity()[:nf]
-        newly = ahead[f[ahead] != 2]
+        newly = ahead[f[ahead] == 0]
         if len(newly):
             break
     assert len(newly), "the moving box never reached the particles ahead of it"

@@ -345,26 +345,41 @@ def cylinder_markers(R: float, width: float, d0: float, layers: int) -> np.ndarr
 
 
 def mgru3_wheel(d0=1e-2, n=(500, 80, 25), R=0.2, width=0.2, vx=0.2, slip=0.3, sinkage=0.02,
-                active=True, dt=2.5e-4) -> Scenario:
-    """NEXT #2/#3 workload: the C4 MGRU3 soil bin with a prescribed rolling wheel (rim markers,
-    v = vx, omega_y = vx / (R (1 - slip))) and the paper's MGRU3 active box 0.6 x 0.6 x 0.8 m
-    around the wheel (P:950, P:960 'Active Box: 0.6 x 0.6 x 0.8 m', Alg. 3); fluid inside the wheel removed."""
+                active=True, dt=2.5e-4, free=False, omega=0.8, load=15.0) -> Scenario:
+    """NEXT #2/#3 workload: the C4 MGRU3 soil bin with a rolling wheel (rim markers) and the paper's
+    MGRU3 active box 0.6 x 0.6 x 0.8 m around it (P:950, P:960 'Active Box: 0.6 x 0.6 x 0.8 m',
+    Alg. 3); fluid inside the wheel removed; lithostatic (settled) initial stress.
+
+    free=False: prescribed motion, v = vx, omega_y = vx / (R (1 - slip)), fixed sinkage (throughput).
+    free=True: the paper's single-wheel rig: constant angular velocity omega, free to
+    move in x and z under a wheel load of `load` kg (the rover mass is not printed: reading A33),
+    starting at rest on the surface; the slip follows from the steady forward speed."""
     sc = mgru3_bin(d0=d0, n=n, dt=dt)
     nx, ny, nz = n
-    c = np.array([0.8, 0.5 * ny * d0, nz * d0 + R - sinkage])
+    c = np.array([0.8, 0.5 * ny * d0, nz * d0 + R - (0.0 if free else sinkage)])
     rim = cylinder_markers(R, width, d0, bce_layers(sc.params["h"], d0))
     rel = sc.fluid_pos - c
     inside = (rel[:, 0] ** 2 + rel[:, 2] ** 2 < (R + 0.5 * d0) ** 2) & (np.abs(rel[:, 1]) < 0.5 * width + d0)
     sc.fluid_pos = sc.fluid_pos[~inside]
+    # a settled terrain (the paper lets it settle for t_delay = 1 s before activating the boxes,
+    # P:950): lithostatic initial stress (reading A20)
+    K, G = sc.params["K"], sc.params["G"]
+    nu = (3 * K - 2 * G) / (2 * (3 * K + G))
+    sc.fluid_sig = f32(lithostatic_stress(sc.fluid_pos, sc.params["rho0"], 9.81, nz * d0, nu / (1 - nu)))
     hi = list(sc.params["hi"])
-    hi[2] = max(hi[2], c[2] + R + 4 * d0)          # grid box above the wheel top
+    hi[2] = max(hi[2], c[2] + 2.5 * R)            # grid box well above the wheel top (thrown soil)
     sc.params["hi"] = tuple(hi)
-    b = Body(mass=10.0, inertia=(1.0, 1.0, 1.0), pos=tuple(c), vel=(vx, 0.0, 0.0),
-             omega=(0.0, vx / (R * (1.0 - slip)), 0.0), motion=BODY_PRESCRIBED, markers=f32(rim + c))
+    if free:
+        b = Body(mass=load, inertia=(1.0, 1.0, 1.0), pos=tuple(c), vel=(0.0, 0.0, 0.0),
+                 omega=(0.0, omega, 0.0), motion=BODY_FREE, dof_mask=1 | 4, markers=f32(rim + c))
+    else:
+        b = Body(mass=10.0, inertia=(1.0, 1.0, 1.0), pos=tuple(c), vel=(vx, 0.0, 0.0),
+                 omega=(0.0, vx / (R * (1.0 - slip)), 0.0), motion=BODY_PRESCRIBED, markers=f32(rim + c))
     sc.bodies = [b]
     sc.name = "mgru3_wheel"
-    if active:
-        sc.active = {"boxes": {1: (0.3, 0.3, 0.4)}, "t_delay": -1.0}
+    if active:   # activated after a few full steps, so the frozen shell's markers carry extrapolated
+        # values of the settled terrain (the paper waits t_delay = 1 s for its terrain to settle)
+        sc.active = {"boxes": {1: (0.3, 0.3, 0.4)}, "t_delay": 2.5 * dt}
     return sc
 
 
