@@ -14,6 +14,7 @@
 #include "physics.cuh"
 #include "structure.cuh"
 #include "tiled.cuh"
+#include "filter.cuh"
 #include "active.cuh"
 
 using namespace crmk;
@@ -23,12 +24,12 @@ namespace {
 enum KernelId {
   KID_MARKERS = 0, KID_BIN, KID_SCAN, KID_SCAN_ADD, KID_SCATTER, KID_REORDER,
   KID_BCE_A, KID_RATES_A, KID_BCE_B, KID_RATES_B, KID_BODY, KID_POSES, KID_STATE, KID_COPY, KID_DECODE,
-  KID_SLAB, KID_ACTIVITY, KID_COUNT
+  KID_SLAB, KID_ACTIVITY, KID_FILTER, KID_COUNT
 };
 const char* kKernelNames[KID_COUNT] = {"k_markers_place", "k_bin", "k_scan_tiles", "k_scan_add", "k_scatter",
                                        "k_reorder", "k_bce_A", "k_rates_A", "k_bce_B", "k_rates_B",
                                        "k_body_update", "k_body_poses", "k_get_set_state", "k_copy_u32",
-                                       "k_decode_lists", "k_slab_util", "k_activity"};
+                                       "k_decode_lists", "k_slab_util", "k_activity", "k_filter"};
 
 struct ProfRec {
   int kid;

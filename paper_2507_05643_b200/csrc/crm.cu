@@ -2,7 +2,7 @@
 //
 // One crm_step(dt, n) issues, per step, on the context's stream:
 //   memset counts | k_bin | scan (k_scan_tiles, k_scan_add) | k_scatter | k_reorder |
-//   k_bce_t<0> (marker filter + extrapolation) | k_rates_t<0> (fluid filter + rates + half step) |
+//   k_filter_t (Alg. 1 lists, rebuild steps) | k_bce_t<0> (extrapolation) | k_rates_t<0> (rates + half step) |
 //   [k_markers_place(mid)] | k_bce_t<1> | k_rates_t<1> (rates + full step + return map) |
 //   [k_body_update | k_body_poses | k_markers_place]
 // and synchronises once at the end to read the device error latch.  With world > 1 the same
@@ -41,6 +41,7 @@ int alloc_debug(crm_t* c) {
 void set_attrs(crm_t* c) {
   if (c->attrs_set) return;
   const int sm = (int)sizeof(TileSmem);
+  cudaFuncSetAttribute(k_filter_t, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FilterSmem));
   cudaFuncSetAttribute(k_bce_t<0, KER_CUBIC>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
   cudaFuncSetAttribute(k_bce_t<1, KER_CUBIC>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
   cudaFuncSetAttribute(k_rates_t<0, KER_CUBIC>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
@@ -351,8 +352,20 @@ void issue_bce_k(crm_t* c, int stage, long long step, int store_all) {
                 c->d_err, (const uint32_t*)c->ids[y], step, c->tile_base, tile_list(c));
 }
 
+// Alg. 1 lists of every tile particle (rebuild steps of Alg. 2): fluid particles all neighbours,
+// markers their fluid neighbours (all of them with store_all, the debug export)
+void issue_filter(crm_t* c, long long step, int store_all) {
+  const int y = c->cur;
+  if (tile_grid(c) == 0) return;
+  launch_smem(c, KID_FILTER, k_filter_t, dim3((unsigned)tile_grid(c)), dim3(FILTER_THREADS), sizeof(FilterSmem),
+              c->grid, (const uint32_t*)c->cell_start, (const float4*)c->P[y], (const float4*)c->U[y], c->list,
+              c->nlist, c->count_all, (const uint32_t*)c->cell_of, c->cap, store_all, c->d_err,
+              (const uint32_t*)c->ids[y], step, c->tile_base, tile_list(c));
+}
+
 void issue_bce(crm_t* c, int stage, float dt, long long step, int store_all) {
   (void)dt;
+  if (stage == 0 && c->ph.build_lists) issue_filter(c, step, store_all);
   if (!c->n_bce) return;
   if (c->ker.kernel == CRM_KERNEL_WENDLAND) issue_bce_k<KER_WENDLAND>(c, stage, step, store_all);
   else issue_bce_k<KER_CUBIC>(c, stage, step, store_all);

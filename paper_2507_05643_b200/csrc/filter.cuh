@@ -1,0 +1,164 @@
+// filter.cuh — Alg. 1 neighbour lists in a kernel of their own.
+//
+//   k_filter_t  one CTA per cell tile; stages only the window's positions (16 B) and a BCE flag
+//               (1 B) per particle — a quarter of the rates kernels' 56-B window — so several CTAs
+//               share an SM and the branchy, latency-bound candidate sweep runs at high occupancy
+//               instead of inside the register- and shared-memory-limited pair kernels.  Every
+//               particle of the tile gets its list: fluid particles all neighbours, markers their
+//               fluid neighbours (Adami sums run over fluid only), or all with store_all
+//               (debug export).  count_all = |P(i)| for the structure checks.
+// Runs only at rebuild steps of Alg. 2 (t mod ps_freq == 0); the tile kernels read the lists.
+// The predicate is rule B2 on the absolute fp32 positions; the candidate order (runs in (da, db)
+// order, offsets ascending) fixes the list order and hence the summation order of the pair loops.
+#pragma once
+#include "common.cuh"
+#include "structure.cuh"
+#include "tiles.cuh"
+
+namespace crmk {
+
+struct FilterSmem : TileHead {
+  float4 P[WMAX + 8];        // absolute positions (the last 8-group may read past a segment)
+  uint8_t bce[WMAX + 8];     // 1 = BCE marker
+};
+
+// positions + flags of the window (LDGSTS for the positions)
+__device__ __forceinline__ void filter_stage(const float4* __restrict__ P, const float4* __restrict__ U,
+                                             FilterSmem& sm) {
+  if (!sm.staged) return;
+  const uint32_t W = sm.run_base[WR];
+  for (uint32_t idx = threadIdx.x; idx < W; idx += blockDim.x) {
+    int r = 0;
+#pragma unroll
+    for (int k = 1; k < WR; ++k) r += (sm.run_base[k] <= idx) ? 1 : 0;
+    const uint32_t gidx = sm.run_start[r] + (idx - sm.run_base[r]);
+    __pipeline_memcpy_async(&sm.P[idx], &P[gidx], sizeof(float4));
+    sm.bce[idx] = tag_is_bce(tag_of(U[gidx].w)) ? 1 : 0;
+  }
+  __pipeline_commit();
+}
+
+// Alg. 1 over one contiguous candidate range [ob, oe) of window offsets: chunks of 32 candidates,
+// a branch-free predicate sweep builds a bitmask (and, for marker lists, a mask of the fluid
+// candidates); the set bits are appended in ascending order.
+template <bool STAGED, bool STORE_BCE>
+__device__ __forceinline__ void filter_range(float R2, const FilterSmem& sm, const float4* __restrict__ P,
+                                             const float4* __restrict__ U, uint32_t ob, uint32_t oe, uint32_t gshift,
+                                             const float4& pi, uint32_t& cnt, ListWriter& w) {
+  for (uint32_t base = ob; base < oe; base += 32) {
+    const uint32_t nc = min(32u, oe - base);
+    uint32_t m = 0, mf = 0;
+    if (STAGED) {
+      // groups of 8 with compile-time bit positions; the last group may read up to 7 slots past
+      // the segment (inside FilterSmem), masked off below
+      for (uint32_t k8 = 0; k8 < nc; k8 += 8) {
+        uint32_t gm = 0, gf = 0;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float4 pj = sm.P[base + k8 + e];
+          const uint32_t bit = b2_pred(pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, R2) ? (1u << e) : 0u;
+          gm |= bit;
+          if (!STORE_BCE) gf |= sm.bce[base + k8 + e] ? 0u : bit;
+        }
+        m |= gm << k8;
+        mf |= gf << k8;
+      }
+      const uint32_t valid = nc >= 32 ? 0xffffffffu : ((1u << nc) - 1u);
+      m &= valid;
+      mf &= valid;
+    } else {
+#pragma unroll 4
+      for (uint32_t k = 0; k < nc; ++k) {
+        const float4 pj = P[base + k + gshift];
+        const uint32_t bit = (b2_pred(pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, R2) ? 1u : 0u) << k;
+        m |= bit;
+        if (!STORE_BCE) mf |= tag_is_bce(tag_of(U[base + k + gshift].w)) ? 0u : bit;
+      }
+    }
+    cnt += __popc(m);
+    uint32_t s = STORE_BCE ? m : mf;
+    while (s) {   // (measured: branch-free funnel-shift appends beat paired/branchy appends)
+      const uint32_t off = base + (__ffs(s) - 1);
+      w.push(STAGED ? off << 4 : off);   // list entry: byte offset of the staged slot (global mode: the offset)
+      s &= s - 1;
+    }
+  }
+}
+
+// the 9 candidate runs of particle i (window offset self, column q, cell z = cz); returns |P(i)|
+template <bool STAGED, bool STORE_BCE>
+__device__ __forceinline__ uint32_t filter_particle(float R2, const FilterSmem& sm, const float4* __restrict__ P,
+                                                    const float4* __restrict__ U, int q, int cz, uint32_t self,
+                                                    float4 pi, ListWriter& w) {
+  // (measured: pruning neighbour cells by their box distance removes ~24 % of the candidates
+  //  but costs more in divergence than it saves; the full 27-cell stencil is kept)
+  uint32_t cnt = 0;
+#pragma unroll 1
+  for (int da = -1; da <= 1; ++da) {
+#pragma unroll 1
+    for (int db = -1; db <= 1; ++db) {
+      uint32_t ob, oe;
+      int r;
+      cand_range(sm, q, da, db, cz, ob, oe, r);
+      const uint32_t gshift = sm.run_start[r] - sm.run_base[r];
+      if (da == 0 && db == 0) {   // the own run holds i itself (j != i, A18)
+        filter_range<STAGED, STORE_BCE>(R2, sm, P, U, ob, self, gshift, pi, cnt, w);
+        filter_range<STAGED, STORE_BCE>(R2, sm, P, U, self + 1, oe, gshift, pi, cnt, w);
+      } else {
+        filter_range<STAGED, STORE_BCE>(R2, sm, P, U, ob, oe, gshift, pi, cnt, w);
+      }
+    }
+  }
+  return cnt;
+}
+
+template <bool STAGED>
+__device__ __forceinline__ void filter_tile(const Grid& g, const FilterSmem& sm, const float4* __restrict__ P,
+                                            const float4* __restrict__ U, uint16_t* __restrict__ list,
+                                            uint32_t* __restrict__ nlist, uint32_t* __restrict__ count_all,
+                                            const uint32_t* __restrict__ cell_of, int cap, int store_all,
+                                            ErrLatch* err, const uint32_t* __restrict__ ids, long long step) {
+  const uint32_t n_i = sm.col_pref[NCOL];
+  for (uint32_t t = threadIdx.x; t < n_i; t += blockDim.x) {
+    int q;
+    const uint32_t i = tile_particle(sm, t, q);
+    const int r_self = (1 + q / TY) * WRY + (1 + q % TY);
+    const uint32_t self = sm.run_base[r_self] + (i - sm.run_start[r_self]);
+    const int cz = (int)(cell_of[i] % (uint32_t)g.dims[2]);
+    const float4 pi = STAGED ? sm.P[self] : P[i];
+    const bool fluid_only = !store_all && tag_is_bce(tag_of(U[i].w));
+    ListWriter w;
+    w.init(list, i, cap);
+    const uint32_t cnt = fluid_only ? filter_particle<STAGED, false>(g.R2, sm, P, U, q, cz, self, pi, w)
+                                    : filter_particle<STAGED, true>(g.R2, sm, P, U, q, cz, self, pi, w);
+    w.flush(STAGED ? self << 4 : self);
+    nlist[i] = (uint32_t)min(w.k, cap);
+    count_all[i] = cnt;
+    if (w.k > cap) latch_error(err, -9 /*CRM_E_CAPACITY*/, (long long)ids[i], step, (long long)w.k);
+  }
+}
+
+constexpr int FILTER_THREADS = 288;
+__global__ void __launch_bounds__(FILTER_THREADS, 4)
+    k_filter_t(Grid g, const uint32_t* __restrict__ cell_start, const float4* __restrict__ P,
+               const float4* __restrict__ U, uint16_t* __restrict__ list, uint32_t* __restrict__ nlist,
+               uint32_t* __restrict__ count_all, const uint32_t* __restrict__ cell_of, int cap, int store_all,
+               ErrLatch* err, const uint32_t* __restrict__ ids, long long step, long long tile_base,
+               const uint32_t* __restrict__ tile_list) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  FilterSmem& sm = *reinterpret_cast<FilterSmem*>(smem_raw);
+  const TileGeom G = tile_geom(g, tile_list ? (long long)tile_list[blockIdx.x] : tile_base + (long long)blockIdx.x);
+  tile_setup(g, G, cell_start, sm);
+  if (sm.col_pref[NCOL] == 0) return;
+  if (sm.run_base[WR] > 65535u) {   // 16-bit list entries
+    if (threadIdx.x == 0) latch_error(err, -9, -1, step, (long long)sm.run_base[WR]);
+    return;
+  }
+  filter_stage(P, U, sm);
+  tile_stage_wait();
+  __syncthreads();
+  if (sm.staged) filter_tile<true>(g, sm, P, U, list, nlist, count_all, cell_of, cap, store_all, err, ids, step);
+  else filter_tile<false>(g, sm, P, U, list, nlist, count_all, cell_of, cap, store_all, err, ids, step);
+}
+
+}  // namespace crmk

@@ -1,14 +1,13 @@
 // tiled.cuh — the hot kernels: one CTA per cell tile, window staged in shared memory.
 //
-//   k_bce_t<0>   markers: Alg. 1 filter over the window (fluid neighbours stored, all counted),
-//                Adami extrapolation at y_n                       -> U, S of markers
-//   k_rates_t<0> fluid: Alg. 1 filter (all neighbours stored) + pair loop at y_n
-//                + y_mid = y_n + dt/2 f; markers copied to the mid state
+//   k_bce_t<0>   markers: Adami extrapolation at y_n           -> U, S of markers
+//   k_rates_t<0> fluid: pair loop at y_n + y_mid = y_n + dt/2 f; markers
+//                copied to the mid state
 //   k_bce_t<1>   markers: extrapolation at y_mid with the stored lists
 //   k_rates_t<1> fluid: pair loop at y_mid with the same lists (A17) + y_{n+1} = y_n + dt f
 //                + mu(I) return map; moving-body markers: loads (A13)
-// Each kernel: stage the window -> [filter on absolute fp32 positions (B2), rebuild steps only]
-// -> convert the window to tile-relative compensated positions -> pair loops -> epilogue.
+// Each kernel: stage the window -> convert it to tile-relative compensated positions -> pair
+// loops over the Alg. 1 lists of k_filter_t (filter.cuh) -> epilogue.
 #pragma once
 #include "common.cuh"
 #include "physics.cuh"
@@ -45,107 +44,6 @@ __device__ __forceinline__ void load_rates(const TileSmem& sm, const float4* __r
     const uint32_t g = window_to_global(sm, e);
     p = rel_pos(P[g], L[g], sm); u = U[g]; s1 = S1[g]; s2 = S2[g];
     p.w = signed_volume(p.w, u.w, m);
-  }
-}
-
-// Alg. 1 filter for particle i (window offset self) over its 9 candidate runs; stores window
-// offsets (all neighbours if store_bce, else fluid ones only); returns |P(i)|.  The candidate
-// order (runs in (da, db) order, offsets ascending) fixes the list order, hence the summation
-// order of the pair loops (deterministic).  Works on the absolute fp32 positions (rule B2).
-template <bool STAGED, bool STORE_BCE>
-__device__ __forceinline__ void filter_range(const Grid& g, const TileSmem& sm, const float4* __restrict__ P,
-                                             const float4* __restrict__ U, uint32_t ob, uint32_t oe, uint32_t gshift,
-                                             const float4& pi, uint32_t& cnt, ListWriter& w) {
-  // chunks of 32 candidates: a branch-free predicate sweep builds a bitmask (and, for marker
-  // lists, a mask of the fluid candidates), then the set bits are appended in ascending order
-  for (uint32_t base = ob; base < oe; base += 32) {
-    const uint32_t nc = min(32u, oe - base);
-    uint32_t m = 0, mf = 0;
-    if (STAGED) {
-      // groups of 8 with compile-time bit positions; the last group may read up to 7 slots past
-      // the segment (still inside TileSmem), masked off below
-      for (uint32_t k8 = 0; k8 < nc; k8 += 8) {
-        uint32_t gm = 0, gf = 0;
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const float4 pj = sm.P[base + k8 + e];
-          const uint32_t bit = b2_pred(pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, g.R2) ? (1u << e) : 0u;
-          gm |= bit;
-          if (!STORE_BCE) gf |= tag_is_bce(tag_of(sm.U[base + k8 + e].w)) ? 0u : bit;
-        }
-        m |= gm << k8;
-        mf |= gf << k8;
-      }
-      const uint32_t valid = nc >= 32 ? 0xffffffffu : ((1u << nc) - 1u);
-      m &= valid;
-      mf &= valid;
-    } else {
-#pragma unroll 4
-      for (uint32_t k = 0; k < nc; ++k) {
-        const float4 pj = P[base + k + gshift];
-        const uint32_t bit = (b2_pred(pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, g.R2) ? 1u : 0u) << k;
-        m |= bit;
-        if (!STORE_BCE) mf |= tag_is_bce(tag_of(U[base + k + gshift].w)) ? 0u : bit;
-      }
-    }
-    cnt += __popc(m);
-    uint32_t s = STORE_BCE ? m : mf;
-    while (s) {   // (measured: branch-free funnel-shift appends beat paired/branchy appends)
-      const uint32_t off = base + (__ffs(s) - 1);
-      w.push(STAGED ? off << 4 : off);   // list entry: byte offset of the staged slot (global mode: the offset)
-      s &= s - 1;
-    }
-  }
-}
-
-template <bool STAGED, bool STORE_BCE>
-__device__ __forceinline__ uint32_t filter(const Grid& g, const TileSmem& sm, const float4* __restrict__ P,
-                                           const float4* __restrict__ U, int q, int cz, uint32_t self, float4 pi,
-                                           ListWriter& w) {
-  // (measured: pruning neighbour cells by their box distance removes ~24 % of the candidates
-  //  but costs more in divergence than it saves; the full 27-cell stencil is kept)
-  uint32_t cnt = 0;
-#pragma unroll 1
-  for (int da = -1; da <= 1; ++da) {
-#pragma unroll 1
-    for (int db = -1; db <= 1; ++db) {
-      uint32_t ob, oe;
-      int r;
-      cand_range(sm, q, da, db, cz, ob, oe, r);
-      const uint32_t gshift = sm.run_start[r] - sm.run_base[r];
-      if (da == 0 && db == 0) {   // the own run holds i itself (j != i, A18)
-        filter_range<STAGED, STORE_BCE>(g, sm, P, U, ob, self, gshift, pi, cnt, w);
-        filter_range<STAGED, STORE_BCE>(g, sm, P, U, self + 1, oe, gshift, pi, cnt, w);
-      } else {
-        filter_range<STAGED, STORE_BCE>(g, sm, P, U, ob, oe, gshift, pi, cnt, w);
-      }
-    }
-  }
-  return cnt;
-}
-
-// rebuild step: build and store the lists of the tile's particles that pass `want`
-template <bool STAGED, bool STORE_BCE, typename Want>
-__device__ __forceinline__ void build_lists(const Grid& g, const TileSmem& sm, const float4* __restrict__ P,
-                                            const float4* __restrict__ U, uint16_t* __restrict__ list,
-                                            uint32_t* __restrict__ nlist, uint32_t* __restrict__ count_all,
-                                            const uint32_t* __restrict__ cell_of, int cap, ErrLatch* err,
-                                            const uint32_t* __restrict__ ids, long long step, Want want) {
-  const uint32_t n_i = sm.col_pref[NCOL];
-  for (uint32_t t = threadIdx.x; t < n_i; t += blockDim.x) {
-    int q;
-    const uint32_t i = tile_particle(sm, t, q);
-    if (!want(tag_of(U[i].w))) continue;
-    const int r_self = (1 + q / TY) * WRY + (1 + q % TY);
-    const uint32_t self = sm.run_base[r_self] + (i - sm.run_start[r_self]);
-    const int cz = (int)(cell_of[i] % (uint32_t)g.dims[2]);
-    ListWriter w;
-    w.init(list, i, cap);
-    const uint32_t cnt = filter<STAGED, STORE_BCE>(g, sm, P, U, q, cz, self, P[i], w);
-    w.flush(STAGED ? self << 4 : self);
-    nlist[i] = (uint32_t)min(w.k, cap);
-    count_all[i] = cnt;
-    if (w.k > cap) latch_error(err, -9 /*CRM_E_CAPACITY*/, (long long)ids[i], step, (long long)w.k);
   }
 }
 
@@ -255,17 +153,6 @@ __global__ void TILE_BOUNDS
   tile_stage(P, U, S1, S2, sm);
   tile_stage_wait();
   __syncthreads();
-  if (STAGE == 0 && ph.build_lists) {   // Alg. 2: rebuild at t mod ps_freq == 0, else reuse
-    auto is_marker = [](uint32_t t) { return tag_is_bce(t); };
-    if (sm.staged) {
-      if (store_all) build_lists<true, true>(g, sm, P, U, list, nlist, count_all, cell_of, cap, err, ids, step, is_marker);
-      else build_lists<true, false>(g, sm, P, U, list, nlist, count_all, cell_of, cap, err, ids, step, is_marker);
-    } else {
-      if (store_all) build_lists<false, true>(g, sm, P, U, list, nlist, count_all, cell_of, cap, err, ids, step, is_marker);
-      else build_lists<false, false>(g, sm, P, U, list, nlist, count_all, cell_of, cap, err, ids, step, is_marker);
-    }
-    __syncthreads();
-  }
   tile_relativize<false>(L, sm, 0.f);
   __syncthreads();
   if (sm.staged) bce_tile<STAGE, KER, true>(ph, sm, P, L, U, S1, S2, list, nlist, pose, cap, dbg, dbg_on);
@@ -515,12 +402,6 @@ __global__ void TILE_BOUNDS
   tile_stage(P, U, S1, S2, sm);
   tile_stage_wait();
   __syncthreads();
-  if (STAGE == 0 && ph.build_lists) {   // Alg. 2: rebuild at t mod ps_freq == 0, else reuse
-    auto is_fluid = [](uint32_t t) { return !tag_is_bce(t); };
-    if (sm.staged) build_lists<true, true>(g, sm, P, U, list, nlist, count_all, cell_of, cap, err, ids, step, is_fluid);
-    else build_lists<false, true>(g, sm, P, U, list, nlist, count_all, cell_of, cap, err, ids, step, is_fluid);
-    __syncthreads();
-  }
   tile_relativize<true>(L, sm, ph.m);
   __syncthreads();
   if (sm.staged)

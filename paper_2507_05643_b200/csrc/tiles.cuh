@@ -26,11 +26,8 @@ constexpr int TILE_THREADS = 288;
 #define TILE_BOUNDS __launch_bounds__(TILE_THREADS, 2)
 constexpr int WMAX = 1920;                                  // staged window capacity (particles)
 
-struct TileSmem {
-  float4 P[WMAX];
-  float4 U[WMAX];
-  float4 S1[WMAX];
-  float2 S2[WMAX];
+// tile geometry shared by every tile kernel (the window arrays follow in the derived structs)
+struct TileHead {
   uint32_t run_start[WR];       // first global index of each window run
   uint32_t run_base[WR + 1];    // window offset of each run (prefix of lengths)
   uint32_t wcs[WR][TZ + 3];     // cellStart of the run's cells zlo..zhi, plus the end
@@ -39,6 +36,14 @@ struct TileSmem {
   int zlo, zhi, staged, any;
   int X0, Y0;
   float ox, oy, oz;             // tile origin: pair loops use positions relative to it
+};
+
+// the rates / BCE kernels stage the whole 56-B state of the window
+struct TileSmem : TileHead {
+  float4 P[WMAX];
+  float4 U[WMAX];
+  float4 S1[WMAX];
+  float2 S2[WMAX];
 };
 
 struct TileGeom {
@@ -97,7 +102,7 @@ __global__ void k_tile_list(long long ntiles, long long tile_base, Grid g, const
 
 // Fill the tile geometry in shared memory (all threads call; contains __syncthreads).
 __device__ __forceinline__ void tile_setup(const Grid& g, const TileGeom& G, const uint32_t* __restrict__ cell_start,
-                                          TileSmem& sm) {
+                                          TileHead& sm) {
   const int nzw = G.zhi - G.zlo + 1;
   if (threadIdx.x < WR) {
     const int r = threadIdx.x;
@@ -162,7 +167,7 @@ __device__ __forceinline__ void tile_stage_wait() { __pipeline_wait_prior(0); }
 // Positions are stored compensated, x = hi + lo (hi: the fp32 value the structural rules B1/B2
 // use; lo: the rounding remainder kept by the integrator).  The pair loops work in coordinates
 // relative to the tile origin, (hi - o) + lo, which keeps ~1e-9 m resolution on metre-scale beds.
-__device__ __forceinline__ float4 rel_pos(const float4& hi, const float4& lo, const TileSmem& sm) {
+__device__ __forceinline__ float4 rel_pos(const float4& hi, const float4& lo, const TileHead& sm) {
   return make_float4((hi.x - sm.ox) + lo.x, (hi.y - sm.oy) + lo.y, (hi.z - sm.oz) + lo.z, hi.w);
 }
 
@@ -215,7 +220,7 @@ __device__ __forceinline__ void comp_add(float& hi, float& lo, float d) {
 }
 
 // global index of a window offset (global mode, where list entries are plain offsets)
-__device__ __forceinline__ uint32_t window_to_global(const TileSmem& sm, uint32_t off) {
+__device__ __forceinline__ uint32_t window_to_global(const TileHead& sm, uint32_t off) {
   int r = 0;
 #pragma unroll
   for (int k = 1; k < WR; ++k) r += (sm.run_base[k] <= off) ? 1 : 0;
@@ -223,7 +228,7 @@ __device__ __forceinline__ uint32_t window_to_global(const TileSmem& sm, uint32_
 }
 
 // tile-local slot t -> (global i, column q)
-__device__ __forceinline__ uint32_t tile_particle(const TileSmem& sm, uint32_t t, int& q) {
+__device__ __forceinline__ uint32_t tile_particle(const TileHead& sm, uint32_t t, int& q) {
   q = 0;
 #pragma unroll
   for (int k = 1; k < NCOL; ++k) q += (sm.col_pref[k] <= t) ? 1 : 0;
@@ -231,7 +236,7 @@ __device__ __forceinline__ uint32_t tile_particle(const TileSmem& sm, uint32_t t
 }
 
 // candidate window-offset range of run (da, db) for a particle of column q at cell z = cz
-__device__ __forceinline__ void cand_range(const TileSmem& sm, int q, int da, int db, int cz, uint32_t& ob,
+__device__ __forceinline__ void cand_range(const TileHead& sm, int q, int da, int db, int cz, uint32_t& ob,
                                            uint32_t& oe, int& r) {
   r = (1 + q / TY + da) * WRY + (1 + q % TY + db);
   const int klo = max(cz - 1, sm.zlo) - sm.zlo;
