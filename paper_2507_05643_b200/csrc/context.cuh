@@ -143,6 +143,8 @@ struct crm {
   uint8_t *d_act = nullptr, *d_act_id = nullptr;   // flags by pre-sort slot / by id
   unsigned long long* d_actcnt = nullptr;
   uint32_t *d_tile_list = nullptr, *d_tile_cnt = nullptr;   // non-empty tiles (kernels launch over them)
+  uint32_t *d_mtiles = nullptr, *d_mtile_cnt = nullptr;    // tiles holding markers (k_filter_t -> k_bce_t)
+  int num_sms = 148;
   long long n_tiles_act = 0;
   bool acap_async = false;               // active-set arrays come from the stream-ordered allocator
 

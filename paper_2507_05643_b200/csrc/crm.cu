@@ -101,6 +101,7 @@ int commit(crm_t* c) {
   r |= dalloc(c, &c->slot_of_id, (size_t)c->n);
   r |= dalloc(c, &c->list, n * (size_t)c->cap); r |= dalloc(c, &c->nlist, n); r |= dalloc(c, &c->count_all, n);
   r |= dalloc(c, &c->d_err, 1);
+  r |= dalloc(c, &c->d_mtiles, (size_t)std::max<long long>(num_tiles(c->grid), 1)); r |= dalloc(c, &c->d_mtile_cnt, 1);
   r |= dalloc(c, &c->d_xcount, 8);
   c->acap = (int64_t)n;
   if (!c->boxes.empty()) {   // active domains (Alg. 3)
@@ -334,41 +335,43 @@ inline long long tile_grid(const crm_t* c) { return c->active_on ? c->n_tiles_ac
 inline const uint32_t* tile_list(const crm_t* c) { return c->active_on ? c->d_tile_list : nullptr; }
 
 template <int KER>
-void issue_bce_k(crm_t* c, int stage, long long step, int store_all) {
-  const int y = c->cur;
+void issue_bce_k(crm_t* c, int stage, long long step) {
   const int dbg = c->dbg_on ? 1 : 0;
   if (tile_grid(c) == 0) return;
-  const dim3 tg((unsigned)tile_grid(c)), tb(TILE_THREADS);
+  // persistent: two resident CTAs per SM walk the marker tiles listed by k_filter_t
+  const dim3 tg((unsigned)std::min<long long>(tile_grid(c), 2LL * c->num_sms)), tb(TILE_THREADS);
   const size_t sm = sizeof(TileSmem);
+  const int y = c->cur;
   if (stage == 0)
     launch_smem(c, KID_BCE_A, k_bce_t<0, KER>, tg, tb, sm, c->grid, c->ph, (const uint32_t*)c->cell_start,
-                (const float4*)c->P[y], (const float4*)c->L[y], c->U[y], c->S1[y], c->S2[y], c->list, c->nlist,
-                c->count_all, (const uint32_t*)c->cell_of, (const Pose*)c->d_pose0, c->cap, store_all, c->dbg, dbg,
-                c->d_err, (const uint32_t*)c->ids[y], step, c->tile_base, tile_list(c));
+                (const float4*)c->P[y], (const float4*)c->L[y], c->U[y], c->S1[y], c->S2[y], (const uint16_t*)c->list,
+                (const uint32_t*)c->nlist, (const Pose*)c->d_pose0, c->cap, c->dbg, dbg, c->d_err, step,
+                (const uint32_t*)c->d_mtiles, (const uint32_t*)c->d_mtile_cnt);
   else
     launch_smem(c, KID_BCE_B, k_bce_t<1, KER>, tg, tb, sm, c->grid, c->ph, (const uint32_t*)c->cell_start,
-                (const float4*)c->Pm, (const float4*)c->Lm, c->Um, c->S1m, c->S2m, c->list, c->nlist,
-                c->count_all, (const uint32_t*)c->cell_of, (const Pose*)c->d_posem, c->cap, 0, c->dbg, dbg,
-                c->d_err, (const uint32_t*)c->ids[y], step, c->tile_base, tile_list(c));
+                (const float4*)c->Pm, (const float4*)c->Lm, c->Um, c->S1m, c->S2m, (const uint16_t*)c->list,
+                (const uint32_t*)c->nlist, (const Pose*)c->d_posem, c->cap, c->dbg, dbg, c->d_err, step,
+                (const uint32_t*)c->d_mtiles, (const uint32_t*)c->d_mtile_cnt);
 }
 
 // Alg. 1 lists of every tile particle (rebuild steps of Alg. 2): fluid particles all neighbours,
 // markers their fluid neighbours (all of them with store_all, the debug export)
 void issue_filter(crm_t* c, long long step, int store_all) {
   const int y = c->cur;
+  cudaMemsetAsync(c->d_mtile_cnt, 0, 4, c->stream);
   if (tile_grid(c) == 0) return;
   launch_smem(c, KID_FILTER, k_filter_t, dim3((unsigned)tile_grid(c)), dim3(FILTER_THREADS), sizeof(FilterSmem),
               c->grid, (const uint32_t*)c->cell_start, (const float4*)c->P[y], (const float4*)c->U[y], c->list,
               c->nlist, c->count_all, (const uint32_t*)c->cell_of, c->cap, store_all, c->d_err,
-              (const uint32_t*)c->ids[y], step, c->tile_base, tile_list(c));
+              (const uint32_t*)c->ids[y], step, c->tile_base, tile_list(c), c->d_mtiles, c->d_mtile_cnt);
 }
 
 void issue_bce(crm_t* c, int stage, float dt, long long step, int store_all) {
   (void)dt;
   if (stage == 0 && c->ph.build_lists) issue_filter(c, step, store_all);
   if (!c->n_bce) return;
-  if (c->ker.kernel == CRM_KERNEL_WENDLAND) issue_bce_k<KER_WENDLAND>(c, stage, step, store_all);
-  else issue_bce_k<KER_CUBIC>(c, stage, step, store_all);
+  if (c->ker.kernel == CRM_KERNEL_WENDLAND) issue_bce_k<KER_WENDLAND>(c, stage, step);
+  else issue_bce_k<KER_CUBIC>(c, stage, step);
 }
 
 // rates: stage 0 (fluid filter + rates at y_n -> y_mid), stage 1 (rates at y_mid -> y_{n+1})
@@ -676,6 +679,7 @@ int crm_create(const crm_material_t* mat, const crm_kernel_t* ker, const crm_bou
     delete c;
     return CRM_E_CUDA;
   }
+  c->num_sms = prop.multiProcessorCount;
   if (dist && dist->cuda_stream) {
     c->stream = (cudaStream_t)dist->cuda_stream;
   } else {
@@ -709,7 +713,7 @@ void crm_destroy(crm_t* c) {
   }
   cudaFree(c->Pm); cudaFree(c->Lm); cudaFree(c->Um); cudaFree(c->S1m); cudaFree(c->S2m);
   cudaFree(c->d_boxes); cudaFree(c->d_act); cudaFree(c->d_act_id); cudaFree(c->d_actcnt);
-  cudaFree(c->d_tile_list); cudaFree(c->d_tile_cnt);
+  cudaFree(c->d_tile_list); cudaFree(c->d_tile_cnt); cudaFree(c->d_mtiles); cudaFree(c->d_mtile_cnt);
   cudaFree(c->key); cudaFree(c->arrival); cudaFree(c->cell_count); cudaFree(c->cell_start);
   cudaFree(c->tmp_src); cudaFree(c->tmp_id); cudaFree(c->cell_of); cudaFree(c->slot_of_id);
   cudaFree(c->list); cudaFree(c->nlist); cudaFree(c->count_all); cudaFree(c->list32);

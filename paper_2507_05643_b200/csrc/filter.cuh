@@ -6,7 +6,8 @@
 //               instead of inside the register- and shared-memory-limited pair kernels.  Every
 //               particle of the tile gets its list: fluid particles all neighbours, markers their
 //               fluid neighbours (Adami sums run over fluid only), or all with store_all
-//               (debug export).  count_all = |P(i)| for the structure checks.
+//               (debug export).  count_all = |P(i)| for the structure checks.  The tiles that hold
+//               markers are appended to `mtiles` for the BCE kernels.
 // Runs only at rebuild steps of Alg. 2 (t mod ps_freq == 0); the tile kernels read the lists.
 // The predicate is rule B2 on the absolute fp32 positions; the candidate order (runs in (da, db)
 // order, offsets ascending) fixes the list order and hence the summation order of the pair loops.
@@ -113,12 +114,13 @@ __device__ __forceinline__ uint32_t filter_particle(float R2, const FilterSmem& 
 }
 
 template <bool STAGED>
-__device__ __forceinline__ void filter_tile(const Grid& g, const FilterSmem& sm, const float4* __restrict__ P,
+__device__ __forceinline__ int filter_tile(const Grid& g, const FilterSmem& sm, const float4* __restrict__ P,
                                             const float4* __restrict__ U, uint16_t* __restrict__ list,
                                             uint32_t* __restrict__ nlist, uint32_t* __restrict__ count_all,
                                             const uint32_t* __restrict__ cell_of, int cap, int store_all,
                                             ErrLatch* err, const uint32_t* __restrict__ ids, long long step) {
   const uint32_t n_i = sm.col_pref[NCOL];
+  int has_marker = 0;
   for (uint32_t t = threadIdx.x; t < n_i; t += blockDim.x) {
     int q;
     const uint32_t i = tile_particle(sm, t, q);
@@ -126,7 +128,9 @@ __device__ __forceinline__ void filter_tile(const Grid& g, const FilterSmem& sm,
     const uint32_t self = sm.run_base[r_self] + (i - sm.run_start[r_self]);
     const int cz = (int)(cell_of[i] % (uint32_t)g.dims[2]);
     const float4 pi = STAGED ? sm.P[self] : P[i];
-    const bool fluid_only = !store_all && tag_is_bce(tag_of(U[i].w));
+    const bool bce = tag_is_bce(tag_of(U[i].w));
+    has_marker |= bce ? 1 : 0;
+    const bool fluid_only = !store_all && bce;
     ListWriter w;
     w.init(list, i, cap);
     const uint32_t cnt = fluid_only ? filter_particle<STAGED, false>(g.R2, sm, P, U, q, cz, self, pi, w)
@@ -136,6 +140,7 @@ __device__ __forceinline__ void filter_tile(const Grid& g, const FilterSmem& sm,
     count_all[i] = cnt;
     if (w.k > cap) latch_error(err, -9 /*CRM_E_CAPACITY*/, (long long)ids[i], step, (long long)w.k);
   }
+  return has_marker;
 }
 
 constexpr int FILTER_THREADS = 288;
@@ -144,10 +149,11 @@ __global__ void __launch_bounds__(FILTER_THREADS, 4)
                const float4* __restrict__ U, uint16_t* __restrict__ list, uint32_t* __restrict__ nlist,
                uint32_t* __restrict__ count_all, const uint32_t* __restrict__ cell_of, int cap, int store_all,
                ErrLatch* err, const uint32_t* __restrict__ ids, long long step, long long tile_base,
-               const uint32_t* __restrict__ tile_list) {
+               const uint32_t* __restrict__ tile_list, uint32_t* __restrict__ mtiles, uint32_t* __restrict__ mcount) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   FilterSmem& sm = *reinterpret_cast<FilterSmem*>(smem_raw);
-  const TileGeom G = tile_geom(g, tile_list ? (long long)tile_list[blockIdx.x] : tile_base + (long long)blockIdx.x);
+  const long long tile = tile_list ? (long long)tile_list[blockIdx.x] : tile_base + (long long)blockIdx.x;
+  const TileGeom G = tile_geom(g, tile);
   tile_setup(g, G, cell_start, sm);
   if (sm.col_pref[NCOL] == 0) return;
   if (sm.run_base[WR] > 65535u) {   // 16-bit list entries
@@ -157,8 +163,10 @@ __global__ void __launch_bounds__(FILTER_THREADS, 4)
   filter_stage(P, U, sm);
   tile_stage_wait();
   __syncthreads();
-  if (sm.staged) filter_tile<true>(g, sm, P, U, list, nlist, count_all, cell_of, cap, store_all, err, ids, step);
-  else filter_tile<false>(g, sm, P, U, list, nlist, count_all, cell_of, cap, store_all, err, ids, step);
+  const int has = sm.staged ? filter_tile<true>(g, sm, P, U, list, nlist, count_all, cell_of, cap, store_all, err, ids, step)
+                            : filter_tile<false>(g, sm, P, U, list, nlist, count_all, cell_of, cap, store_all, err, ids, step);
+  // the tiles holding markers: the BCE kernels run over these only (any order: tiles are independent)
+  if (__syncthreads_or(has) && threadIdx.x == 0) mtiles[atomicAdd(mcount, 1u)] = (uint32_t)tile;
 }
 
 }  // namespace crmk

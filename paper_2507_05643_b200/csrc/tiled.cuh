@@ -126,37 +126,36 @@ __device__ __forceinline__ void bce_tile(const Phys& ph, TileSmem& sm, const flo
   }
 }
 
+// Persistent over the tiles that hold markers (listed by k_filter_t at the last rebuild): a tile
+// of fluid only has nothing to extrapolate, and a CTA per tile of the whole grid would cost more
+// in setup than the markers' work.
 template <int STAGE, int KER>
 __global__ void TILE_BOUNDS
     k_bce_t(Grid g, Phys ph, const uint32_t* __restrict__ cell_start, const float4* __restrict__ P,
             const float4* __restrict__ L, float4* __restrict__ U, float4* __restrict__ S1, float2* __restrict__ S2,
-            uint16_t* __restrict__ list, uint32_t* __restrict__ nlist, uint32_t* __restrict__ count_all,
-            const uint32_t* __restrict__ cell_of, const Pose* __restrict__ pose, int cap, int store_all, Debug dbg,
-            int dbg_on, ErrLatch* err, const uint32_t* __restrict__ ids, long long step, long long tile_base,
-            const uint32_t* __restrict__ tile_list) {
+            const uint16_t* __restrict__ list, const uint32_t* __restrict__ nlist, const Pose* __restrict__ pose,
+            int cap, Debug dbg, int dbg_on, ErrLatch* err, long long step, const uint32_t* __restrict__ mtiles,
+            const uint32_t* __restrict__ mcount) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
-  const TileGeom G = tile_geom(g, tile_list ? (long long)tile_list[blockIdx.x] : tile_base + (long long)blockIdx.x);
-  tile_setup(g, G, cell_start, sm);
-  const uint32_t n_i = sm.col_pref[NCOL];
-  if (n_i == 0) return;
-  int has = 0;
-  for (uint32_t t = threadIdx.x; t < n_i; t += blockDim.x) {
-    int q;
-    has |= tag_is_bce(tag_of(U[tile_particle(sm, t, q)].w)) ? 1 : 0;
+  const uint32_t ntile = *mcount;
+  for (uint32_t k = blockIdx.x; k < ntile; k += gridDim.x) {
+    __syncthreads();   // the previous tile's window is no longer read
+    const TileGeom G = tile_geom(g, (long long)mtiles[k]);
+    tile_setup(g, G, cell_start, sm);
+    if (sm.col_pref[NCOL] == 0) continue;
+    if (sm.run_base[WR] > 65535u) {
+      if (threadIdx.x == 0) latch_error(err, -9, -1, step, (long long)sm.run_base[WR]);
+      continue;
+    }
+    tile_stage(P, U, S1, S2, sm);
+    tile_stage_wait();
+    __syncthreads();
+    tile_relativize<false>(L, sm, 0.f);
+    __syncthreads();
+    if (sm.staged) bce_tile<STAGE, KER, true>(ph, sm, P, L, U, S1, S2, list, nlist, pose, cap, dbg, dbg_on);
+    else bce_tile<STAGE, KER, false>(ph, sm, P, L, U, S1, S2, list, nlist, pose, cap, dbg, dbg_on);
   }
-  if (!__syncthreads_or(has)) return;
-  if (sm.run_base[WR] > 65535u) {
-    if (threadIdx.x == 0) latch_error(err, -9, -1, step, (long long)sm.run_base[WR]);
-    return;
-  }
-  tile_stage(P, U, S1, S2, sm);
-  tile_stage_wait();
-  __syncthreads();
-  tile_relativize<false>(L, sm, 0.f);
-  __syncthreads();
-  if (sm.staged) bce_tile<STAGE, KER, true>(ph, sm, P, L, U, S1, S2, list, nlist, pose, cap, dbg, dbg_on);
-  else bce_tile<STAGE, KER, false>(ph, sm, P, L, U, S1, S2, list, nlist, pose, cap, dbg, dbg_on);
 }
 
 // ---------------------------------------------------------------------------------------
