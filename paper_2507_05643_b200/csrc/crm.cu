@@ -331,6 +331,7 @@ int issue_rebuild_sort(crm_t* c, long long step) {
 
 // BCE extrapolation: stage 0 at y_n (with the marker filter), stage 1 at y_mid
 // the tile grid of a step: every tile, or (active domains) the non-empty ones listed by k_tile_list
+inline ListShape list_shape(const crm_t* c) { return ListShape{c->cap, (uint32_t)c->acap}; }
 inline long long tile_grid(const crm_t* c) { return c->active_on ? c->n_tiles_act : c->ntiles; }
 inline const uint32_t* tile_list(const crm_t* c) { return c->active_on ? c->d_tile_list : nullptr; }
 
@@ -345,12 +346,12 @@ void issue_bce_k(crm_t* c, int stage, long long step) {
   if (stage == 0)
     launch_smem(c, KID_BCE_A, k_bce_t<0, KER>, tg, tb, sm, c->grid, c->ph, (const uint32_t*)c->cell_start,
                 (const float4*)c->P[y], (const float4*)c->L[y], c->U[y], c->S1[y], c->S2[y], (const uint16_t*)c->list,
-                (const uint32_t*)c->nlist, (const Pose*)c->d_pose0, c->cap, c->dbg, dbg, c->d_err, step,
+                (const uint32_t*)c->nlist, (const Pose*)c->d_pose0, list_shape(c), c->dbg, dbg, c->d_err, step,
                 (const uint32_t*)c->d_mtiles, (const uint32_t*)c->d_mtile_cnt);
   else
     launch_smem(c, KID_BCE_B, k_bce_t<1, KER>, tg, tb, sm, c->grid, c->ph, (const uint32_t*)c->cell_start,
                 (const float4*)c->Pm, (const float4*)c->Lm, c->Um, c->S1m, c->S2m, (const uint16_t*)c->list,
-                (const uint32_t*)c->nlist, (const Pose*)c->d_posem, c->cap, c->dbg, dbg, c->d_err, step,
+                (const uint32_t*)c->nlist, (const Pose*)c->d_posem, list_shape(c), c->dbg, dbg, c->d_err, step,
                 (const uint32_t*)c->d_mtiles, (const uint32_t*)c->d_mtile_cnt);
 }
 
@@ -362,7 +363,7 @@ void issue_filter(crm_t* c, long long step, int store_all) {
   if (tile_grid(c) == 0) return;
   launch_smem(c, KID_FILTER, k_filter_t, dim3((unsigned)tile_grid(c)), dim3(FILTER_THREADS), sizeof(FilterSmem),
               c->grid, (const uint32_t*)c->cell_start, (const float4*)c->P[y], (const float4*)c->U[y], c->list,
-              c->nlist, c->count_all, (const uint32_t*)c->cell_of, c->cap, store_all, c->d_err,
+              c->nlist, c->count_all, (const uint32_t*)c->cell_of, list_shape(c), store_all, c->d_err,
               (const uint32_t*)c->ids[y], step, c->tile_base, tile_list(c), c->d_mtiles, c->d_mtile_cnt);
 }
 
@@ -386,13 +387,13 @@ void issue_rates_k(crm_t* c, int stage, float dt, long long step) {
     launch_smem(c, KID_RATES_A, k_rates_t<0, KER>, tg, tb, sm, c->grid, c->ph, dt, (const uint32_t*)c->cell_start,
                 (const float4*)c->P[y], (const float4*)c->L[y], (const float4*)c->U[y], (const float4*)c->S1[y],
                 (const float2*)c->S2[y], c->Pm, c->Lm, c->Um, c->S1m, c->S2m, c->list, c->nlist, c->count_all,
-                (const uint32_t*)c->cell_of, c->cap, c->macc, c->dbg, dbg, c->d_err, (const uint32_t*)c->ids[y], step,
+                (const uint32_t*)c->cell_of, list_shape(c), c->macc, c->dbg, dbg, c->d_err, (const uint32_t*)c->ids[y], step,
                 c->tile_base, tile_list(c));
   else
     launch_smem(c, KID_RATES_B, k_rates_t<1, KER>, tg, tb, sm, c->grid, c->ph, dt, (const uint32_t*)c->cell_start,
                 (const float4*)c->Pm, (const float4*)c->Lm, (const float4*)c->Um, (const float4*)c->S1m,
                 (const float2*)c->S2m, c->P[y], c->L[y], c->U[y], c->S1[y], c->S2[y], c->list, c->nlist, c->count_all,
-                (const uint32_t*)c->cell_of, c->cap, c->macc, c->dbg, dbg, c->d_err, (const uint32_t*)c->ids[y], step,
+                (const uint32_t*)c->cell_of, list_shape(c), c->macc, c->dbg, dbg, c->d_err, (const uint32_t*)c->ids[y], step,
                 c->tile_base, tile_list(c));
 }
 
@@ -1140,7 +1141,7 @@ int crm_debug_neighbors(crm_t* c, int64_t* offsets, int64_t* list) {
   if (nv)
     launch(c, KID_DECODE, k_decode_lists, dim3(blocks((long long)nv, 256)), dim3(256), (int)nv, c->grid,
            (const uint32_t*)c->cell_start, (const uint32_t*)c->cell_of, (const uint16_t*)c->list,
-           (const uint32_t*)c->nlist, c->cap, c->list32, c->tmp_id /* decoded counts (scratch) */);
+           (const uint32_t*)c->nlist, list_shape(c), c->list32, c->tmp_id /* decoded counts (scratch) */);
   r = read_latch(c);
   if (r) return r;
   std::vector<uint32_t> ids(n), nl(n, 0u);

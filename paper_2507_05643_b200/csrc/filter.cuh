@@ -117,7 +117,7 @@ template <bool STAGED>
 __device__ __forceinline__ int filter_tile(const Grid& g, const FilterSmem& sm, const float4* __restrict__ P,
                                             const float4* __restrict__ U, uint16_t* __restrict__ list,
                                             uint32_t* __restrict__ nlist, uint32_t* __restrict__ count_all,
-                                            const uint32_t* __restrict__ cell_of, int cap, int store_all,
+                                            const uint32_t* __restrict__ cell_of, ListShape ls, int store_all,
                                             ErrLatch* err, const uint32_t* __restrict__ ids, long long step) {
   const uint32_t n_i = sm.col_pref[NCOL];
   int has_marker = 0;
@@ -132,13 +132,13 @@ __device__ __forceinline__ int filter_tile(const Grid& g, const FilterSmem& sm, 
     has_marker |= bce ? 1 : 0;
     const bool fluid_only = !store_all && bce;
     ListWriter w;
-    w.init(list, i, cap);
+    w.init(list, i, ls);
     const uint32_t cnt = fluid_only ? filter_particle<STAGED, false>(g.R2, sm, P, U, q, cz, self, pi, w)
                                     : filter_particle<STAGED, true>(g.R2, sm, P, U, q, cz, self, pi, w);
     w.flush(STAGED ? self << 4 : self);
-    nlist[i] = (uint32_t)min(w.k, cap);
+    nlist[i] = (uint32_t)min(w.k, ls.cap);
     count_all[i] = cnt;
-    if (w.k > cap) latch_error(err, -9 /*CRM_E_CAPACITY*/, (long long)ids[i], step, (long long)w.k);
+    if (w.k > ls.cap) latch_error(err, -9 /*CRM_E_CAPACITY*/, (long long)ids[i], step, (long long)w.k);
   }
   return has_marker;
 }
@@ -147,7 +147,7 @@ constexpr int FILTER_THREADS = 288;
 __global__ void __launch_bounds__(FILTER_THREADS, 4)
     k_filter_t(Grid g, const uint32_t* __restrict__ cell_start, const float4* __restrict__ P,
                const float4* __restrict__ U, uint16_t* __restrict__ list, uint32_t* __restrict__ nlist,
-               uint32_t* __restrict__ count_all, const uint32_t* __restrict__ cell_of, int cap, int store_all,
+               uint32_t* __restrict__ count_all, const uint32_t* __restrict__ cell_of, ListShape ls, int store_all,
                ErrLatch* err, const uint32_t* __restrict__ ids, long long step, long long tile_base,
                const uint32_t* __restrict__ tile_list, uint32_t* __restrict__ mtiles, uint32_t* __restrict__ mcount) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -163,8 +163,8 @@ __global__ void __launch_bounds__(FILTER_THREADS, 4)
   filter_stage(P, U, sm);
   tile_stage_wait();
   __syncthreads();
-  const int has = sm.staged ? filter_tile<true>(g, sm, P, U, list, nlist, count_all, cell_of, cap, store_all, err, ids, step)
-                            : filter_tile<false>(g, sm, P, U, list, nlist, count_all, cell_of, cap, store_all, err, ids, step);
+  const int has = sm.staged ? filter_tile<true>(g, sm, P, U, list, nlist, count_all, cell_of, ls, store_all, err, ids, step)
+                            : filter_tile<false>(g, sm, P, U, list, nlist, count_all, cell_of, ls, store_all, err, ids, step);
   // the tiles holding markers: the BCE kernels run over these only (any order: tiles are independent)
   if (__syncthreads_or(has) && threadIdx.x == 0) mtiles[atomicAdd(mcount, 1u)] = (uint32_t)tile;
 }

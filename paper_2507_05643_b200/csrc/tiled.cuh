@@ -52,7 +52,7 @@ template <int STAGE, int KER, bool STAGED>
 __device__ __forceinline__ void bce_tile(const Phys& ph, TileSmem& sm, const float4* __restrict__ P,
                                          const float4* __restrict__ L, float4* __restrict__ U, float4* __restrict__ S1,
                                          float2* __restrict__ S2, const uint16_t* __restrict__ list,
-                                         const uint32_t* __restrict__ nlist, const Pose* __restrict__ pose, int cap,
+                                         const uint32_t* __restrict__ nlist, const Pose* __restrict__ pose, ListShape ls,
                                          Debug dbg, int dbg_on) {
   const uint32_t n_i = sm.col_pref[NCOL];
   for (uint32_t t = threadIdx.x; t < n_i; t += blockDim.x) {
@@ -76,13 +76,14 @@ __device__ __forceinline__ void bce_tile(const Phys& ph, TileSmem& sm, const flo
     if (tag_moving(tag)) body_kinematics(pose[tag_body(tag)], pabs.x, pabs.y, pabs.z, ub, ab);
     const float ga[3] = {ph.g[0] - ab[0], ph.g[1] - ab[1], ph.g[2] - ab[2]};
     float SW = 0.f, su[3] = {0.f, 0.f, 0.f}, ss[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, sh = 0.f;
-    const uint4* seg = reinterpret_cast<const uint4*>(list + (size_t)i * cap);
+    const uint4* seg = reinterpret_cast<const uint4*>(list) + i;
     // whole chunks of 8 (padded with the marker itself, excluded by the fluid mask): branch-free
     const uint32_t nch = (nl + 7) >> 3;
     uint4 vn = seg[0];   // chunk prefetch, as in pair_loop
+    const size_t ls_stride = ls.stride;
     for (uint32_t c = 0; c < nch; ++c) {
       const uint4 v = vn;
-      vn = seg[min(c + 1, nch - 1)];
+      vn = seg[(size_t)min(c + 1, nch - 1) * ls_stride];
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         const uint32_t off = list_entry(v, e);
@@ -134,7 +135,7 @@ __global__ void TILE_BOUNDS
     k_bce_t(Grid g, Phys ph, const uint32_t* __restrict__ cell_start, const float4* __restrict__ P,
             const float4* __restrict__ L, float4* __restrict__ U, float4* __restrict__ S1, float2* __restrict__ S2,
             const uint16_t* __restrict__ list, const uint32_t* __restrict__ nlist, const Pose* __restrict__ pose,
-            int cap, Debug dbg, int dbg_on, ErrLatch* err, long long step, const uint32_t* __restrict__ mtiles,
+            ListShape ls, Debug dbg, int dbg_on, ErrLatch* err, long long step, const uint32_t* __restrict__ mtiles,
             const uint32_t* __restrict__ mcount) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
@@ -153,8 +154,8 @@ __global__ void TILE_BOUNDS
     __syncthreads();
     tile_relativize<false>(L, sm, 0.f);
     __syncthreads();
-    if (sm.staged) bce_tile<STAGE, KER, true>(ph, sm, P, L, U, S1, S2, list, nlist, pose, cap, dbg, dbg_on);
-    else bce_tile<STAGE, KER, false>(ph, sm, P, L, U, S1, S2, list, nlist, pose, cap, dbg, dbg_on);
+    if (sm.staged) bce_tile<STAGE, KER, true>(ph, sm, P, L, U, S1, S2, list, nlist, pose, ls, dbg, dbg_on);
+    else bce_tile<STAGE, KER, false>(ph, sm, P, L, U, S1, S2, list, nlist, pose, ls, dbg, dbg_on);
   }
 }
 
@@ -203,16 +204,17 @@ template <int KER, bool STAGED>
 __device__ __forceinline__ void pair_loop(PairAcc& A, const Phys& ph, const TileSmem& sm, const float4* __restrict__ P,
                                           const float4* __restrict__ L, const float4* __restrict__ U,
                                           const float4* __restrict__ S1, const float2* __restrict__ S2,
-                                          const uint16_t* __restrict__ list, uint32_t i, int cap, uint32_t nl,
+                                          const uint16_t* __restrict__ list, uint32_t i, ListShape ls, uint32_t nl,
                                           const float4& pi, const float4& ui, bool with_L, bool fluid_only) {
-  const uint4* seg = reinterpret_cast<const uint4*>(list + (size_t)i * cap);
+  const uint4* seg = reinterpret_cast<const uint4*>(list) + i;
+  const size_t ls_stride = ls.stride;
   const uint32_t nch = (nl + 7) >> 3;
   // the list streams from HBM (written by stage A, larger than L2): chunk c + 1 is requested
   // before chunk c is processed so its latency hides behind 8 pair evaluations
   uint4 vn = seg[0];
   for (uint32_t c = 0; c < nch; ++c) {   // whole padded chunks of 8, branch-free
     const uint4 v = vn;
-    vn = seg[min(c + 1, nch - 1)];
+    vn = seg[(size_t)min(c + 1, nch - 1) * ls_stride];
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       float4 pj, uj, s1;
@@ -233,7 +235,7 @@ __device__ __forceinline__ void rates_tile(const Phys& ph, float dt, TileSmem& s
                                            float4* __restrict__ YP, float4* __restrict__ YL, float4* __restrict__ YU,
                                            float4* __restrict__ YS1, float2* __restrict__ YS2,
                                            const uint16_t* __restrict__ list, const uint32_t* __restrict__ nlist,
-                                           int cap, float4* __restrict__ macc, Debug dbg, int dbg_on, ErrLatch* err,
+                                           ListShape ls, float4* __restrict__ macc, Debug dbg, int dbg_on, ErrLatch* err,
                                            const uint32_t* __restrict__ ids, long long step) {
   const uint32_t n_i = sm.col_pref[NCOL];
   for (uint32_t t = threadIdx.x; t < n_i; t += blockDim.x) {
@@ -263,7 +265,7 @@ __device__ __forceinline__ void rates_tile(const Phys& ph, float dt, TileSmem& s
 #pragma unroll
     for (int k = 0; k < 3; ++k) { A.Gs[k] = 0.f; A.Ms[k] = 0.f; A.Pi[k] = 0.f; }
     if (bce) {   // STAGE 1, moving-body marker: m a_s over fluid neighbours, no gravity (A13)
-      pair_loop<KER, STAGED>(A, ph, sm, P, L, U, S1, S2, list, i, cap, nl, pi, ui, false, true);
+      pair_loop<KER, STAGED>(A, ph, sm, P, L, U, S1, S2, list, i, ls, nl, pi, ui, false, true);
       const float4 si1 = S1[i];
       const float2 si2 = S2[i];
       const float rinv_i = 1.0f / pi.w;
@@ -275,7 +277,7 @@ __device__ __forceinline__ void rates_tile(const Phys& ph, float dt, TileSmem& s
       if (dbg_on) dbg.acc[1][i] = make_float4(a[0], a[1], a[2], 0.f);
       continue;
     }
-    pair_loop<KER, STAGED>(A, ph, sm, P, L, U, S1, S2, list, i, cap, nl, pi, ui, true, false);
+    pair_loop<KER, STAGED>(A, ph, sm, P, L, U, S1, S2, list, i, ls, nl, pi, ui, true, false);
     // own state for the epilogue, (re)loaded after the loop to keep registers free inside it
     const float4 phi = P[i];
     const float4 pli = L[i];
@@ -362,7 +364,7 @@ __global__ void TILE_BOUNDS
               const float2* __restrict__ S2, float4* __restrict__ YP, float4* __restrict__ YL, float4* __restrict__ YU,
               float4* __restrict__ YS1, float2* __restrict__ YS2, uint16_t* __restrict__ list,
               uint32_t* __restrict__ nlist, uint32_t* __restrict__ count_all, const uint32_t* __restrict__ cell_of,
-              int cap, float4* __restrict__ macc, Debug dbg, int dbg_on, ErrLatch* err,
+              ListShape ls, float4* __restrict__ macc, Debug dbg, int dbg_on, ErrLatch* err,
               const uint32_t* __restrict__ ids, long long step, long long tile_base,
               const uint32_t* __restrict__ tile_list) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -404,10 +406,10 @@ __global__ void TILE_BOUNDS
   tile_relativize<true>(L, sm, ph.m);
   __syncthreads();
   if (sm.staged)
-    rates_tile<STAGE, KER, true>(ph, dt, sm, P, L, U, S1, S2, YP, YL, YU, YS1, YS2, list, nlist, cap, macc, dbg, dbg_on,
+    rates_tile<STAGE, KER, true>(ph, dt, sm, P, L, U, S1, S2, YP, YL, YU, YS1, YS2, list, nlist, ls, macc, dbg, dbg_on,
                             err, ids, step);
   else
-    rates_tile<STAGE, KER, false>(ph, dt, sm, P, L, U, S1, S2, YP, YL, YU, YS1, YS2, list, nlist, cap, macc, dbg, dbg_on,
+    rates_tile<STAGE, KER, false>(ph, dt, sm, P, L, U, S1, S2, YP, YL, YU, YS1, YS2, list, nlist, ls, macc, dbg, dbg_on,
                              err, ids, step);
 }
 
@@ -416,7 +418,7 @@ __global__ void TILE_BOUNDS
 // zero-weight self padding is dropped and the remaining count written to nout
 __global__ void k_decode_lists(int n, Grid g, const uint32_t* __restrict__ cell_start,
                                const uint32_t* __restrict__ cell_of, const uint16_t* __restrict__ list,
-                               const uint32_t* __restrict__ nlist, int cap, uint32_t* __restrict__ out,
+                               const uint32_t* __restrict__ nlist, ListShape ls, uint32_t* __restrict__ out,
                                uint32_t* __restrict__ nout) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -440,7 +442,8 @@ __global__ void k_decode_lists(int n, Grid g, const uint32_t* __restrict__ cell_
   rb[WR] = acc;
   uint32_t kk = 0;
   for (uint32_t k = 0; k < nlist[i]; ++k) {
-    const uint32_t off = acc <= (uint32_t)WMAX ? list[(size_t)i * cap + k] >> 4 : list[(size_t)i * cap + k];
+    const uint32_t e = list[((size_t)(k >> 3) * ls.stride + (size_t)i) * 8 + (k & 7)];
+    const uint32_t off = acc <= (uint32_t)WMAX ? e >> 4 : e;
     int r = 0;
     for (int q = 1; q < WR; ++q) r += (rb[q] <= off) ? 1 : 0;
     const uint32_t j = rs[r] + (off - rb[r]);

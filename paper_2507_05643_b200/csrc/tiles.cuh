@@ -247,17 +247,28 @@ __device__ __forceinline__ void cand_range(const TileHead& sm, int q, int da, in
 }
 
 // 16-bit list writer: entries are collected in a 128-bit funnel-shift register buffer and
-// written 8 at a time with one 16-B store into the particle's contiguous segment; the last
+// written 8 at a time with one 16-B store (chunk-major layout, see ListShape); the last
 // chunk is padded with `fill` (the particle's own window offset: a zero-weight entry), so the
 // pair loops read whole 16-B chunks and run without per-entry branches.
+// list layout: chunk-major ELL of 16-B chunks (8 entries): chunk c of particle (slot) i at uint4
+// index c * stride + i, so the 32 lanes of a warp (consecutive slots) read one chunk each with a
+// single coalesced 512-B access; cap entries (cap % 8 == 0) per particle, stride = rows allocated
+struct ListShape {
+  int cap;
+  uint32_t stride;
+};
+
 struct ListWriter {
-  uint4* dst;        // per-particle segment (cap entries, cap % 8 == 0)
+  uint4* dst;        // chunk 0 of the particle (chunk c at dst[c * stride])
+  size_t stride;
   uint32_t b0, b1, b2, b3;
   int nb;            // entries in the buffer
   int k;             // entries found (may exceed cap: overflow is reported by the caller)
   int cap;
-  __device__ __forceinline__ void init(uint16_t* list, size_t i, int cap_) {
-    dst = reinterpret_cast<uint4*>(list + i * (size_t)cap_);
+  __device__ __forceinline__ void init(uint16_t* list, size_t i, ListShape ls) {
+    dst = reinterpret_cast<uint4*>(list) + i;
+    stride = ls.stride;
+    const int cap_ = ls.cap;
     b0 = b1 = b2 = b3 = 0u;
     nb = 0;
     k = 0;
@@ -274,7 +285,7 @@ struct ListWriter {
     ++nb;
     ++k;
     if (nb == 8) {
-      dst[(k - 8) >> 3] = make_uint4(b0, b1, b2, b3);
+      dst[(size_t)((k - 8) >> 3) * stride] = make_uint4(b0, b1, b2, b3);
       nb = 0;
     }
   }
@@ -296,7 +307,7 @@ struct ListWriter {
     nb += 2;
     k += 2;
     if (nb == 8) {
-      dst[(k - 8) >> 3] = make_uint4(b0, b1, b2, b3);
+      dst[(size_t)((k - 8) >> 3) * stride] = make_uint4(b0, b1, b2, b3);
       nb = 0;
     }
   }
@@ -314,7 +325,7 @@ struct ListWriter {
       b3 = __funnelshift_r(b3, fill, 16);
     }
     const int kk = min(k, cap);
-    dst[(kk - 1) >> 3] = make_uint4(b0, b1, b2, b3);
+    dst[(size_t)((kk - 1) >> 3) * stride] = make_uint4(b0, b1, b2, b3);
     nb = 0;
   }
 };
