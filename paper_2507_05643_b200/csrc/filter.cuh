@@ -143,8 +143,8 @@ __device__ __forceinline__ int filter_tile(const Grid& g, const FilterSmem& sm, 
   return has_marker;
 }
 
-constexpr int FILTER_THREADS = 288;
-__global__ void __launch_bounds__(FILTER_THREADS, 4)
+constexpr int FILTER_THREADS = 160;
+__global__ void __launch_bounds__(FILTER_THREADS, 6)
     k_filter_t(Grid g, const uint32_t* __restrict__ cell_start, const float4* __restrict__ P,
                const float4* __restrict__ U, uint16_t* __restrict__ list, uint32_t* __restrict__ nlist,
                uint32_t* __restrict__ count_all, const uint32_t* __restrict__ cell_of, ListShape ls, int store_all,
