@@ -164,6 +164,14 @@ struct PairAcc {
   float L[9], Gs[3], Ms[3], Pi[3];
 };
 
+// own state of a thread's first particle, requested before the window staging so that its
+// latency overlaps the staging and the relativize pass instead of following them
+struct Prefetch {
+  uint32_t i, nl;
+  float4 u, p, l;
+  uint4 c0;
+};
+
 // One directed pair (i, j).  pj.w = signed V_j (+ fluid, - marker).  Branch-free: an invalid pair
 // (r >= 2h, A17; r = 0 incl. the self padding, A18; a marker when only fluid counts) gets w = 0, hence
 // a zero contribution to every sum.  Two MUFU per pair (rsqrt, one reciprocal for the AV).
@@ -205,13 +213,15 @@ __device__ __forceinline__ void pair_loop(PairAcc& A, const Phys& ph, const Tile
                                           const float4* __restrict__ L, const float4* __restrict__ U,
                                           const float4* __restrict__ S1, const float2* __restrict__ S2,
                                           const uint16_t* __restrict__ list, uint32_t i, ListShape ls, uint32_t nl,
-                                          const float4& pi, const float4& ui, bool with_L, bool fluid_only) {
+                                          uint4 first, const float4& pi, const float4& ui, bool with_L,
+                                          bool fluid_only) {
   const uint4* seg = reinterpret_cast<const uint4*>(list) + i;
   const size_t ls_stride = ls.stride;
   const uint32_t nch = (nl + 7) >> 3;
-  // the list streams from HBM (written by stage A, larger than L2): chunk c + 1 is requested
-  // before chunk c is processed so its latency hides behind 8 pair evaluations
-  uint4 vn = seg[0];
+  // the list streams from HBM (written by the filter, larger than L2): chunk c + 1 is requested
+  // before chunk c is processed so its latency hides behind 8 pair evaluations; chunk 0 comes
+  // from the caller (requested before the window staging)
+  uint4 vn = first;
   for (uint32_t c = 0; c < nch; ++c) {   // whole padded chunks of 8, branch-free
     const uint4 v = vn;
     vn = seg[(size_t)min(c + 1, nch - 1) * ls_stride];
@@ -236,12 +246,13 @@ __device__ __forceinline__ void rates_tile(const Phys& ph, float dt, TileSmem& s
                                            float4* __restrict__ YS1, float2* __restrict__ YS2,
                                            const uint16_t* __restrict__ list, const uint32_t* __restrict__ nlist,
                                            ListShape ls, float4* __restrict__ macc, Debug dbg, int dbg_on, ErrLatch* err,
-                                           const uint32_t* __restrict__ ids, long long step) {
+                                           const uint32_t* __restrict__ ids, long long step, const Prefetch& pre) {
   const uint32_t n_i = sm.col_pref[NCOL];
   for (uint32_t t = threadIdx.x; t < n_i; t += blockDim.x) {
+    const bool first = t == threadIdx.x;   // the thread's first particle was prefetched
     int q;
-    const uint32_t i = tile_particle(sm, t, q);
-    const float4 ui = U[i];
+    const uint32_t i = first ? pre.i : tile_particle(sm, t, q);
+    const float4 ui = first ? pre.u : U[i];
     const uint32_t tag = tag_of(ui.w);
     const bool bce = tag_is_bce(tag);
     if (bce && !(STAGE == 1 && tag_moving(tag))) continue;
@@ -257,15 +268,16 @@ __device__ __forceinline__ void rates_tile(const Phys& ph, float dt, TileSmem& s
       }
       continue;
     }
-    const float4 pi = rel_pos(P[i], L[i], sm);
-    const uint32_t nl = nlist[i];
+    const float4 pi = first ? rel_pos(pre.p, pre.l, sm) : rel_pos(P[i], L[i], sm);
+    const uint32_t nl = first ? pre.nl : nlist[i];
+    const uint4 c0 = first ? pre.c0 : reinterpret_cast<const uint4*>(list)[i];
     PairAcc A;
 #pragma unroll
     for (int k = 0; k < 9; ++k) A.L[k] = 0.f;
 #pragma unroll
     for (int k = 0; k < 3; ++k) { A.Gs[k] = 0.f; A.Ms[k] = 0.f; A.Pi[k] = 0.f; }
     if (bce) {   // STAGE 1, moving-body marker: m a_s over fluid neighbours, no gravity (A13)
-      pair_loop<KER, STAGED>(A, ph, sm, P, L, U, S1, S2, list, i, ls, nl, pi, ui, false, true);
+      pair_loop<KER, STAGED>(A, ph, sm, P, L, U, S1, S2, list, i, ls, nl, c0, pi, ui, false, true);
       const float4 si1 = S1[i];
       const float2 si2 = S2[i];
       const float rinv_i = 1.0f / pi.w;
@@ -277,7 +289,7 @@ __device__ __forceinline__ void rates_tile(const Phys& ph, float dt, TileSmem& s
       if (dbg_on) dbg.acc[1][i] = make_float4(a[0], a[1], a[2], 0.f);
       continue;
     }
-    pair_loop<KER, STAGED>(A, ph, sm, P, L, U, S1, S2, list, i, ls, nl, pi, ui, true, false);
+    pair_loop<KER, STAGED>(A, ph, sm, P, L, U, S1, S2, list, i, ls, nl, c0, pi, ui, true, false);
     // own state for the epilogue, (re)loaded after the loop to keep registers free inside it
     const float4 phi = P[i];
     const float4 pli = L[i];
@@ -400,6 +412,16 @@ __global__ void TILE_BOUNDS
     if (threadIdx.x == 0) latch_error(err, -9, -1, step, (long long)sm.run_base[WR]);
     return;
   }
+  Prefetch pre;
+  if (threadIdx.x < n_i) {
+    int q;
+    pre.i = tile_particle(sm, threadIdx.x, q);
+    pre.u = U[pre.i];
+    pre.p = P[pre.i];
+    pre.l = L[pre.i];
+    pre.nl = nlist[pre.i];
+    pre.c0 = reinterpret_cast<const uint4*>(list)[pre.i];
+  }
   tile_stage(P, U, S1, S2, sm);
   tile_stage_wait();
   __syncthreads();
@@ -407,10 +429,10 @@ __global__ void TILE_BOUNDS
   __syncthreads();
   if (sm.staged)
     rates_tile<STAGE, KER, true>(ph, dt, sm, P, L, U, S1, S2, YP, YL, YU, YS1, YS2, list, nlist, ls, macc, dbg, dbg_on,
-                            err, ids, step);
+                            err, ids, step, pre);
   else
     rates_tile<STAGE, KER, false>(ph, dt, sm, P, L, U, S1, S2, YP, YL, YU, YS1, YS2, list, nlist, ls, macc, dbg, dbg_on,
-                             err, ids, step);
+                             err, ids, step, pre);
 }
 
 // ---------------------------------------------------------------------------------------
