@@ -259,74 +259,40 @@ struct ListShape {
 };
 
 struct ListWriter {
-  uint4* dst;        // chunk 0 of the particle (chunk c at dst[c * stride])
-  size_t stride;
-  uint32_t b0, b1, b2, b3;
-  int nb;            // entries in the buffer
+  uint2* dst;        // half h of chunk c of the particle at dst[c * stride2 + h] (8-B units)
+  size_t stride2;
+  uint32_t b0, b1;   // the last 4 entries (16 bits each, oldest in the low half of b0)
   int k;             // entries found (may exceed cap: overflow is reported by the caller)
   int cap;
   __device__ __forceinline__ void init(uint16_t* list, size_t i, ListShape ls) {
-    dst = reinterpret_cast<uint4*>(list) + i;
-    stride = ls.stride;
-    const int cap_ = ls.cap;
-    b0 = b1 = b2 = b3 = 0u;
-    nb = 0;
+    dst = reinterpret_cast<uint2*>(list) + 2 * i;
+    stride2 = 2 * (size_t)ls.stride;
+    b0 = b1 = 0u;
     k = 0;
-    cap = cap_;
-    pend = 0u;
-    hp = false;
+    cap = ls.cap;
+  }
+  // (measured: 4-entry buffer + 8-B stores with the capacity test only at the store beat the
+  //  16-B funnel buffer with a per-entry capacity branch, and one 2-B store per entry)
+  __device__ __forceinline__ void store(int kk) {   // entries kk - 4 .. kk - 1 are in (b0, b1)
+    const int p = kk - 4;
+    if (kk <= cap) dst[(size_t)(p >> 3) * stride2 + ((p >> 2) & 1)] = make_uint2(b0, b1);
   }
   __device__ __forceinline__ void push(uint32_t off) {
-    if (k >= cap) { ++k; return; }
     b0 = __funnelshift_r(b0, b1, 16);
-    b1 = __funnelshift_r(b1, b2, 16);
-    b2 = __funnelshift_r(b2, b3, 16);
-    b3 = __funnelshift_r(b3, off, 16);
-    ++nb;
+    b1 = __funnelshift_r(b1, off, 16);
     ++k;
-    if (nb == 8) {
-      dst[(size_t)((k - 8) >> 3) * stride] = make_uint4(b0, b1, b2, b3);
-      nb = 0;
-    }
+    if ((k & 3) == 0) store(k);
   }
-  // one entry; entries are paired into words (the first of a pair waits in `pend`)
-  uint32_t pend;
-  bool hp = false;
-  __device__ __forceinline__ void push_half(uint32_t e) {
-    if (hp) push2(pend | (e << 16));
-    else pend = e;
-    hp = !hp;
-  }
-  // two entries packed in one word (entry e1 in the low half); keeps nb even
-  __device__ __forceinline__ void push2(uint32_t word) {
-    if (k >= cap) { k += 2; return; }
-    b0 = b1;
-    b1 = b2;
-    b2 = b3;
-    b3 = word;
-    nb += 2;
-    k += 2;
-    if (nb == 8) {
-      dst[(size_t)((k - 8) >> 3) * stride] = make_uint4(b0, b1, b2, b3);
-      nb = 0;
-    }
-  }
+  // pad the last chunk of 8 with `fill` (a zero-weight entry); k keeps the unpadded count
   __device__ __forceinline__ void flush(uint32_t fill) {
-    if (hp) {
-      push2(pend | (fill << 16));
-      hp = false;
-    }
-    if (nb == 0) return;
-    const int pad = 8 - nb;
-    for (int p = 0; p < pad; ++p) {
+    if (k >= cap) return;   // cap % 8 == 0: the stored part ends on a chunk boundary
+    int kk = k;
+    while (kk & 7) {
       b0 = __funnelshift_r(b0, b1, 16);
-      b1 = __funnelshift_r(b1, b2, 16);
-      b2 = __funnelshift_r(b2, b3, 16);
-      b3 = __funnelshift_r(b3, fill, 16);
+      b1 = __funnelshift_r(b1, fill, 16);
+      ++kk;
+      if ((kk & 3) == 0) store(kk);
     }
-    const int kk = min(k, cap);
-    dst[(size_t)((kk - 1) >> 3) * stride] = make_uint4(b0, b1, b2, b3);
-    nb = 0;
   }
 };
 
