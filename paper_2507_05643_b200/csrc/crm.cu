@@ -386,14 +386,14 @@ void issue_rates_k(crm_t* c, int stage, float dt, long long step) {
   if (stage == 0)
     launch_smem(c, KID_RATES_A, k_rates_t<0, KER>, tg, tb, sm, c->grid, c->ph, dt, (const uint32_t*)c->cell_start,
                 (const float4*)c->P[y], (const float4*)c->L[y], (const float4*)c->U[y], (const float4*)c->S1[y],
-                (const float2*)c->S2[y], c->Pm, c->Lm, c->Um, c->S1m, c->S2m, c->list, c->nlist, c->count_all,
-                (const uint32_t*)c->cell_of, list_shape(c), c->macc, c->dbg, dbg, c->d_err, (const uint32_t*)c->ids[y], step,
+                (const float2*)c->S2[y], c->Pm, c->Lm, c->Um, c->S1m, c->S2m, (const uint16_t*)c->list,
+                (const uint32_t*)c->nlist, list_shape(c), c->macc, c->dbg, dbg, c->d_err, (const uint32_t*)c->ids[y], step,
                 c->tile_base, tile_list(c));
   else
     launch_smem(c, KID_RATES_B, k_rates_t<1, KER>, tg, tb, sm, c->grid, c->ph, dt, (const uint32_t*)c->cell_start,
                 (const float4*)c->Pm, (const float4*)c->Lm, (const float4*)c->Um, (const float4*)c->S1m,
-                (const float2*)c->S2m, c->P[y], c->L[y], c->U[y], c->S1[y], c->S2[y], c->list, c->nlist, c->count_all,
-                (const uint32_t*)c->cell_of, list_shape(c), c->macc, c->dbg, dbg, c->d_err, (const uint32_t*)c->ids[y], step,
+                (const float2*)c->S2m, c->P[y], c->L[y], c->U[y], c->S1[y], c->S2[y], (const uint16_t*)c->list,
+                (const uint32_t*)c->nlist, list_shape(c), c->macc, c->dbg, dbg, c->d_err, (const uint32_t*)c->ids[y], step,
                 c->tile_base, tile_list(c));
 }
 

@@ -374,8 +374,8 @@ __global__ void TILE_BOUNDS
     k_rates_t(Grid g, Phys ph, float dt, const uint32_t* __restrict__ cell_start, const float4* __restrict__ P,
               const float4* __restrict__ L, const float4* __restrict__ U, const float4* __restrict__ S1,
               const float2* __restrict__ S2, float4* __restrict__ YP, float4* __restrict__ YL, float4* __restrict__ YU,
-              float4* __restrict__ YS1, float2* __restrict__ YS2, uint16_t* __restrict__ list,
-              uint32_t* __restrict__ nlist, uint32_t* __restrict__ count_all, const uint32_t* __restrict__ cell_of,
+              float4* __restrict__ YS1, float2* __restrict__ YS2, const uint16_t* __restrict__ list,
+              const uint32_t* __restrict__ nlist,
               ListShape ls, float4* __restrict__ macc, Debug dbg, int dbg_on, ErrLatch* err,
               const uint32_t* __restrict__ ids, long long step, long long tile_base,
               const uint32_t* __restrict__ tile_list) {
