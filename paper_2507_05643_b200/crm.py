@@ -7,6 +7,7 @@ fallback: if libcrm.so is missing or no sm_100 device is visible the calls raise
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 import os
 
 import numpy as np
@@ -154,6 +155,10 @@ def group_step(ctxs, dt: float, n: int = 1):
         raise CrmError(rc, f"crm_group_step: {msgs}")
 
 
+# library stream handle -> the Crm that created it (weak: borrowers hold strong references)
+_STREAM_OWNERS: "weakref.WeakValueDictionary[int, Crm]" = weakref.WeakValueDictionary()
+
+
 class CrmError(RuntimeError):
     def __init__(self, code: int, msg: str):
         super().__init__(f"crm error {code}: {msg}")
@@ -207,9 +212,16 @@ class Crm:
         if rc:
             raise CrmError(rc, self._L.crm_strerror(rc).decode())
         self.h = h
+        # a context on another context's stream keeps that context (and its stream) alive
+        self._stream_owner = _STREAM_OWNERS.get(int(stream)) if stream else None
+        if not stream:
+            _STREAM_OWNERS[int(self.stream())] = self
 
     def close(self):
         if getattr(self, "h", None):
+            sid = int(self.stream())
+            if _STREAM_OWNERS.get(sid) is self:
+                del _STREAM_OWNERS[sid]
             self._L.crm_destroy(self.h)
             self.h = None
 

@@ -20,11 +20,13 @@ namespace crmk {
 constexpr int TX = 2, TY = 2, TZ = 4;
 constexpr int WRX = TX + 2, WRY = TY + 2, WR = WRX * WRY;   // 16 window runs
 constexpr int NCOL = TX * TY;                               // i columns per tile
-constexpr int TILE_THREADS = 288;
-// 2 CTAs of 288 threads per SM (ptxas caps at 96 registers; measured: __maxnreg__(112) removes the
-// small spills but drops residency to 1 CTA/SM, 1.5x slower)
+constexpr int TILE_THREADS = 384;
+// 2 CTAs of 384 threads per SM (80 registers; the pair loops do not spill).  A tile holds 250-330
+// particles on the C5 lattice (2h = 2.6 d0 cells alias the lattice: up to 396 with walls): with
+// 288 threads a quarter of the tiles ran a second round for a few particles and took twice as long
+// (measured: 288 -> 384 threads, rates kernels -14 %; 448 threads spill and are slower)
 #define TILE_BOUNDS __launch_bounds__(TILE_THREADS, 2)
-constexpr int WMAX = 1920;                                  // staged window capacity (particles)
+constexpr int WMAX = 1968;   // staged window capacity (particles): 1920 sent 6 % of the C5 tiles to global mode
 
 // tile geometry shared by every tile kernel (the window arrays follow in the derived structs)
 struct TileHead {
