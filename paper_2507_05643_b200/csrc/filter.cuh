@@ -18,9 +18,15 @@
 
 namespace crmk {
 
+// The window is staged as three coordinate arrays (structure of arrays), so one 8-byte load gives a
+// candidate PAIR's x (or y, z) and the B2 predicate of two candidates runs on the packed f32x2
+// FP32 instructions of sm_100 (FADD2/FMUL2/FFMA2: per element the same IEEE round-to-nearest
+// results as the scalar instructions, half the issue slots; this kernel is issue-bound).
 struct FilterSmem : TileHead {
-  float4 P[WMAX + 8];        // absolute positions (the last 8-group may read past a segment)
-  uint8_t bce[WMAX + 8];     // 1 = BCE marker
+  alignas(16) float X[WMAX + 40];   // absolute positions (a chunk may read up to 39 slots past a segment)
+  float Y[WMAX + 40];
+  float Z[WMAX + 40];
+  uint8_t bce[WMAX + 40];    // 1 = BCE marker
 };
 
 // positions + flags of the window (LDGSTS for the positions)
@@ -33,10 +39,45 @@ __device__ __forceinline__ void filter_stage(const float4* __restrict__ P, const
 #pragma unroll
     for (int k = 1; k < WR; ++k) r += (sm.run_base[k] <= idx) ? 1 : 0;
     const uint32_t gidx = sm.run_start[r] + (idx - sm.run_base[r]);
-    __pipeline_memcpy_async(&sm.P[idx], &P[gidx], sizeof(float4));
+    const float* pg = reinterpret_cast<const float*>(&P[gidx]);
+    __pipeline_memcpy_async(&sm.X[idx], pg + 0, sizeof(float));
+    __pipeline_memcpy_async(&sm.Y[idx], pg + 1, sizeof(float));
+    __pipeline_memcpy_async(&sm.Z[idx], pg + 2, sizeof(float));
     sm.bce[idx] = tag_is_bce(tag_of(U[gidx].w)) ? 1 : 0;
   }
   __pipeline_commit();
+}
+
+// packed fp32 pairs (element 0 in the low word)
+__device__ __forceinline__ unsigned long long f2_sub(unsigned long long a, unsigned long long b) {
+  unsigned long long d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ unsigned long long f2_mul(unsigned long long a, unsigned long long b) {
+  unsigned long long d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ unsigned long long f2_fma(unsigned long long a, unsigned long long b, unsigned long long c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ unsigned long long f2_splat(float a) {
+  const unsigned long long u = __float_as_uint(a);
+  return (u << 32) | u;
+}
+
+// rule B2 for the candidate pair (j, j + 1), j even: bits 0 and 1 = "neighbour"
+__device__ __forceinline__ uint32_t b2_pred2(const FilterSmem& sm, uint32_t j, unsigned long long xi2,
+                                             unsigned long long yi2, unsigned long long zi2, float R2) {
+  const unsigned long long xj = *reinterpret_cast<const unsigned long long*>(&sm.X[j]);
+  const unsigned long long yj = *reinterpret_cast<const unsigned long long*>(&sm.Y[j]);
+  const unsigned long long zj = *reinterpret_cast<const unsigned long long*>(&sm.Z[j]);
+  const unsigned long long dx = f2_sub(xj, xi2), dy = f2_sub(yj, yi2), dz = f2_sub(zj, zi2);   // x_j - x_i
+  const unsigned long long r2 = f2_fma(dz, dz, f2_fma(dy, dy, f2_mul(dx, dx)));
+  return (__uint_as_float((uint32_t)r2) < R2 ? 1u : 0u) | (__uint_as_float((uint32_t)(r2 >> 32)) < R2 ? 2u : 0u);
 }
 
 // Alg. 1 over one contiguous candidate range [ob, oe) of window offsets: chunks of 32 candidates,
@@ -46,25 +87,28 @@ template <bool STAGED, bool STORE_BCE>
 __device__ __forceinline__ void filter_range(float R2, const FilterSmem& sm, const float4* __restrict__ P,
                                              const float4* __restrict__ U, uint32_t ob, uint32_t oe, uint32_t gshift,
                                              const float4& pi, uint32_t& cnt, ListWriter& w) {
-  for (uint32_t base = ob; base < oe; base += 32) {
+  const unsigned long long xi2 = f2_splat(pi.x), yi2 = f2_splat(pi.y), zi2 = f2_splat(pi.z);
+  // staged: chunks start on an even slot (8-byte pair loads); the slot before ob is masked off
+  for (uint32_t base = STAGED ? (ob & ~1u) : ob; base < oe; base += 32) {
     const uint32_t nc = min(32u, oe - base);
     uint32_t m = 0, mf = 0;
     if (STAGED) {
-      // groups of 8 with compile-time bit positions; the last group may read up to 7 slots past
-      // the segment (inside FilterSmem), masked off below
+      // groups of 8 (4 pairs) with compile-time bit positions; the last group may read up to 7
+      // slots past the segment (inside FilterSmem), masked off below
       for (uint32_t k8 = 0; k8 < nc; k8 += 8) {
         uint32_t gm = 0, gf = 0;
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const float4 pj = sm.P[base + k8 + e];
-          const uint32_t bit = b2_pred(pi.x, pi.y, pi.z, pj.x, pj.y, pj.z, R2) ? (1u << e) : 0u;
-          gm |= bit;
-          if (!STORE_BCE) gf |= sm.bce[base + k8 + e] ? 0u : bit;
+        for (int e = 0; e < 8; e += 2) gm |= b2_pred2(sm, base + k8 + e, xi2, yi2, zi2, R2) << e;
+        if (!STORE_BCE) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) gf |= sm.bce[base + k8 + e] ? 0u : (1u << e);
+          gf &= gm;
         }
         m |= gm << k8;
         mf |= gf << k8;
       }
-      const uint32_t valid = nc >= 32 ? 0xffffffffu : ((1u << nc) - 1u);
+      uint32_t valid = nc >= 32 ? 0xffffffffu : ((1u << nc) - 1u);
+      if (base < ob) valid &= ~1u;
       m &= valid;
       mf &= valid;
     } else {
@@ -127,7 +171,7 @@ __device__ __forceinline__ int filter_tile(const Grid& g, const FilterSmem& sm, 
     const int r_self = (1 + q / TY) * WRY + (1 + q % TY);
     const uint32_t self = sm.run_base[r_self] + (i - sm.run_start[r_self]);
     const int cz = (int)(cell_of[i] % (uint32_t)g.dims[2]);
-    const float4 pi = STAGED ? sm.P[self] : P[i];
+    const float4 pi = STAGED ? make_float4(sm.X[self], sm.Y[self], sm.Z[self], 0.f) : P[i];
     const bool bce = tag_is_bce(tag_of(U[i].w));
     has_marker |= bce ? 1 : 0;
     const bool fluid_only = !store_all && bce;
