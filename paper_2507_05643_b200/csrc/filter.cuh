@@ -48,27 +48,6 @@ __device__ __forceinline__ void filter_stage(const float4* __restrict__ P, const
   __pipeline_commit();
 }
 
-// packed fp32 pairs (element 0 in the low word)
-__device__ __forceinline__ unsigned long long f2_sub(unsigned long long a, unsigned long long b) {
-  unsigned long long d;
-  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-__device__ __forceinline__ unsigned long long f2_mul(unsigned long long a, unsigned long long b) {
-  unsigned long long d;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-__device__ __forceinline__ unsigned long long f2_fma(unsigned long long a, unsigned long long b, unsigned long long c) {
-  unsigned long long d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-  return d;
-}
-__device__ __forceinline__ unsigned long long f2_splat(float a) {
-  const unsigned long long u = __float_as_uint(a);
-  return (u << 32) | u;
-}
-
 // rule B2 for the candidate pair (j, j + 1), j even: bits 0 and 1 = "neighbour"
 __device__ __forceinline__ uint32_t b2_pred2(const FilterSmem& sm, uint32_t j, unsigned long long xi2,
                                              unsigned long long yi2, unsigned long long zi2, float R2) {
