@@ -33,17 +33,18 @@ struct FilterSmem : TileHead {
 __device__ __forceinline__ void filter_stage(const float4* __restrict__ P, const float4* __restrict__ U,
                                              FilterSmem& sm) {
   if (!sm.staged) return;
-  const uint32_t W = sm.run_base[WR];
-  for (uint32_t idx = threadIdx.x; idx < W; idx += blockDim.x) {
-    int r = 0;
-#pragma unroll
-    for (int k = 1; k < WR; ++k) r += (sm.run_base[k] <= idx) ? 1 : 0;
-    const uint32_t gidx = sm.run_start[r] + (idx - sm.run_base[r]);
-    const float* pg = reinterpret_cast<const float*>(&P[gidx]);
-    __pipeline_memcpy_async(&sm.X[idx], pg + 0, sizeof(float));
-    __pipeline_memcpy_async(&sm.Y[idx], pg + 1, sizeof(float));
-    __pipeline_memcpy_async(&sm.Z[idx], pg + 2, sizeof(float));
-    sm.bce[idx] = tag_is_bce(tag_of(U[gidx].w)) ? 1 : 0;
+  const uint32_t lane = threadIdx.x & 31u, nw = blockDim.x >> 5;
+  for (uint32_t r = threadIdx.x >> 5; r < (uint32_t)WR; r += nw) {   // one warp per window run
+    const uint32_t b = sm.run_base[r], e = sm.run_base[r + 1];
+    const int shift = (int)sm.run_start[r] - (int)b;
+    for (uint32_t idx = b + lane; idx < e; idx += 32) {
+      const uint32_t gidx = (uint32_t)((int)idx + shift);
+      const float* pg = reinterpret_cast<const float*>(&P[gidx]);
+      __pipeline_memcpy_async(&sm.X[idx], pg + 0, sizeof(float));
+      __pipeline_memcpy_async(&sm.Y[idx], pg + 1, sizeof(float));
+      __pipeline_memcpy_async(&sm.Z[idx], pg + 2, sizeof(float));
+      sm.bce[idx] = tag_is_bce(tag_of(U[gidx].w)) ? 1 : 0;
+    }
   }
   __pipeline_commit();
 }
