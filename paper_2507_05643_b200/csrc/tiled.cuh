@@ -385,12 +385,29 @@ __global__ void TILE_BOUNDS
   tile_setup(g, G, cell_start, sm);
   const uint32_t n_i = sm.col_pref[NCOL];
   if (n_i == 0) return;
+  if (sm.run_base[WR] > 65535u) {
+    if (threadIdx.x == 0) latch_error(err, -9, -1, step, (long long)sm.run_base[WR]);
+    return;
+  }
+  // the window copy starts right away (a tile of markers only, rare, stages for nothing); the
+  // own state of each thread's first particle is requested beside it
+  tile_stage(P, U, S1, S2, sm);
+  Prefetch pre;
+  if (threadIdx.x < n_i) {
+    int q;
+    pre.i = tile_particle(sm, threadIdx.x, q);
+    pre.u = U[pre.i];
+    pre.p = P[pre.i];
+    pre.l = L[pre.i];
+    pre.nl = nlist[pre.i];
+    pre.c0 = reinterpret_cast<const uint4*>(list)[pre.i];
+  }
   // marker bookkeeping that needs no window; detect whether the tile has pair work
   int work = 0;
   for (uint32_t t = threadIdx.x; t < n_i; t += blockDim.x) {
     int q;
-    const uint32_t i = tile_particle(sm, t, q);
-    const float4 ui = U[i];
+    const uint32_t i = t == threadIdx.x ? pre.i : tile_particle(sm, t, q);
+    const float4 ui = t == threadIdx.x ? pre.u : U[i];
     const uint32_t tag = tag_of(ui.w);
     if (!tag_is_bce(tag)) {
       work = 1;
@@ -407,23 +424,9 @@ __global__ void TILE_BOUNDS
       if (tag_moving(tag)) work = 1;
     }
   }
-  if (!__syncthreads_or(work)) return;
-  if (sm.run_base[WR] > 65535u) {
-    if (threadIdx.x == 0) latch_error(err, -9, -1, step, (long long)sm.run_base[WR]);
-    return;
-  }
-  Prefetch pre;
-  if (threadIdx.x < n_i) {
-    int q;
-    pre.i = tile_particle(sm, threadIdx.x, q);
-    pre.u = U[pre.i];
-    pre.p = P[pre.i];
-    pre.l = L[pre.i];
-    pre.nl = nlist[pre.i];
-    pre.c0 = reinterpret_cast<const uint4*>(list)[pre.i];
-  }
-  tile_stage(P, U, S1, S2, sm);
+  const bool any = __syncthreads_or(work);
   tile_stage_wait();
+  if (!any) return;
   __syncthreads();
   tile_relativize<true>(L, sm, ph.m);
   __syncthreads();
