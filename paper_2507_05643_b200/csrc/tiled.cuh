@@ -425,10 +425,15 @@ __global__ void TILE_BOUNDS
     }
   }
   const bool any = __syncthreads_or(work);
+  if (!any) {
+    tile_stage_wait();
+    return;
+  }
+  RelPre rp;
+  relativize_load(L, sm, rp);
   tile_stage_wait();
-  if (!any) return;
   __syncthreads();
-  tile_relativize<true>(L, sm, ph.m);
+  relativize_apply<true>(sm, rp, ph.m);
   __syncthreads();
   if (sm.staged)
     rates_tile<STAGE, KER, true>(ph, dt, sm, P, L, U, S1, S2, YP, YL, YU, YS1, YS2, list, nlist, ls, macc, dbg, dbg_on,

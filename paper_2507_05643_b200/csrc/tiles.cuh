@@ -206,9 +206,43 @@ __device__ __forceinline__ float signed_volume(float rho, float tagw, float m) {
   return tag_is_bce(tag_of(tagw)) ? -V : V;
 }
 
-// convert the staged window from absolute hi to relative compensated positions (after the filter);
+// convert the staged window from absolute hi to relative compensated positions;
 // TO_V: the rates kernels also replace rho_j by the signed volume V_j (one division per staged
-// particle instead of one reciprocal per pair)
+// particle instead of one reciprocal per pair).  Split in two: relativize_load requests the lo parts
+// of the thread's window slots (registers) BEFORE the staging wait, relativize_apply converts after
+// it, so the global latency of lo hides behind the staging.
+constexpr int RELK = (WMAX + 383) / 384;   // window slots per thread (blockDim >= 384)
+struct RelPre {
+  float4 l[RELK];
+};
+__device__ __forceinline__ void relativize_load(const float4* __restrict__ L, const TileSmem& sm, RelPre& rp) {
+  if (!sm.staged) return;
+  const uint32_t W = sm.run_base[WR];
+#pragma unroll
+  for (int k = 0; k < RELK; ++k) {
+    const uint32_t idx = threadIdx.x + (uint32_t)k * blockDim.x;
+    if (idx < W) {
+      int r = 0;
+#pragma unroll
+      for (int step = WR / 2; step > 0; step >>= 1) r += (sm.run_base[r + step] <= idx) ? step : 0;
+      rp.l[k] = L[sm.run_start[r] + (idx - sm.run_base[r])];
+    }
+  }
+}
+template <bool TO_V>
+__device__ __forceinline__ void relativize_apply(TileSmem& sm, const RelPre& rp, float m) {
+  if (!sm.staged) return;
+  const uint32_t W = sm.run_base[WR];
+#pragma unroll
+  for (int k = 0; k < RELK; ++k) {
+    const uint32_t idx = threadIdx.x + (uint32_t)k * blockDim.x;
+    if (idx < W) {
+      float4 p = rel_pos(sm.P[idx], rp.l[k], sm);
+      if (TO_V) p.w = signed_volume(p.w, sm.U[idx].w, m);
+      sm.P[idx] = p;
+    }
+  }
+}
 template <bool TO_V>
 __device__ __forceinline__ void tile_relativize(const float4* __restrict__ L, TileSmem& sm, float m) {
   if (!sm.staged) return;
