@@ -322,23 +322,24 @@ struct ListShape {
 };
 
 struct ListWriter {
-  uint2* dst;        // half h of chunk c of the particle at dst[c * stride2 + h] (8-B units)
-  size_t stride2;
+  uint2* cur;        // the next 8-B half-chunk to store (chunk-major layout, see ListShape)
+  size_t step;       // from half 1 of chunk c to half 0 of chunk c + 1: 2 * stride - 1 halves
   uint32_t b0, b1;   // the last 4 entries (16 bits each, oldest in the low half of b0)
   int k;             // entries found (may exceed cap: overflow is reported by the caller)
   int cap;
   __device__ __forceinline__ void init(uint16_t* list, size_t i, ListShape ls) {
-    dst = reinterpret_cast<uint2*>(list) + 2 * i;
-    stride2 = 2 * (size_t)ls.stride;
+    cur = reinterpret_cast<uint2*>(list) + 2 * i;
+    step = 2 * (size_t)ls.stride - 1;
     b0 = b1 = 0u;
     k = 0;
     cap = ls.cap;
   }
   // (measured: 4-entry buffer + 8-B stores with the capacity test only at the store beat the
-  //  16-B funnel buffer with a per-entry capacity branch, and one 2-B store per entry)
+  //  16-B funnel buffer with a per-entry capacity branch, and one 2-B store per entry; the store
+  //  address advances incrementally — recomputing it from k cost 13 instructions per store)
   __device__ __forceinline__ void store(int kk) {   // entries kk - 4 .. kk - 1 are in (b0, b1)
-    const int p = kk - 4;
-    if (kk <= cap) dst[(size_t)(p >> 3) * stride2 + ((p >> 2) & 1)] = make_uint2(b0, b1);
+    if (kk <= cap) *cur = make_uint2(b0, b1);
+    cur += (kk & 4) ? 1 : step;   // kk % 8 == 4: the second half of the chunk is next
   }
   __device__ __forceinline__ void push(uint32_t off) {
     b0 = __funnelshift_r(b0, b1, 16);
