@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcrm.so")
+LIB_PATH = os.environ.get("CRM_LIB") or os.path.join(_HERE, "libcrm.so")
 
 CRM_OK, CRM_E_INVALID, CRM_E_DOMAIN, CRM_E_NONFINITE, CRM_E_UNSUPPORTED = 0, -1, -2, -3, -4
 CRM_E_STATE, CRM_E_OOM, CRM_E_CUDA, CRM_E_COMM, CRM_E_CAPACITY = -5, -6, -7, -8, -9

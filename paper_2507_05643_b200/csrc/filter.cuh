@@ -167,8 +167,12 @@ __device__ __forceinline__ int filter_tile(const Grid& g, const FilterSmem& sm, 
   return has_marker;
 }
 
-constexpr int FILTER_THREADS = 160;
-__global__ void __launch_bounds__(FILTER_THREADS, 6)
+#ifndef CRM_FILTER_THREADS
+#define CRM_FILTER_THREADS 160
+#define CRM_FILTER_MINB 6
+#endif
+constexpr int FILTER_THREADS = CRM_FILTER_THREADS;
+__global__ void __launch_bounds__(FILTER_THREADS, CRM_FILTER_MINB)
     k_filter_t(Grid g, const uint32_t* __restrict__ cell_start, const float4* __restrict__ P,
                const float4* __restrict__ U, uint16_t* __restrict__ list, uint32_t* __restrict__ nlist,
                uint32_t* __restrict__ count_all, const uint32_t* __restrict__ cell_of, ListShape ls, int store_all,

@@ -20,13 +20,19 @@ namespace crmk {
 constexpr int TX = 2, TY = 2, TZ = 4;
 constexpr int WRX = TX + 2, WRY = TY + 2, WR = WRX * WRY;   // 16 window runs
 constexpr int NCOL = TX * TY;                               // i columns per tile
-constexpr int TILE_THREADS = 384;
+#ifndef CRM_TILE_THREADS
+#define CRM_TILE_THREADS 384
+#endif
+constexpr int TILE_THREADS = CRM_TILE_THREADS;
 // 2 CTAs of 384 threads per SM (80 registers; the pair loops do not spill).  A tile holds 250-330
 // particles on the C5 lattice (2h = 2.6 d0 cells alias the lattice: up to 396 with walls): with
 // 288 threads a quarter of the tiles ran a second round for a few particles and took twice as long
 // (measured: 288 -> 384 threads, rates kernels -14 %; 448 threads spill and are slower)
 #define TILE_BOUNDS __launch_bounds__(TILE_THREADS, 2)
-constexpr int WMAX = 1968;   // staged window capacity (particles): 1920 sent 6 % of the C5 tiles to global mode
+#ifndef CRM_WMAX
+#define CRM_WMAX 1968
+#endif
+constexpr int WMAX = CRM_WMAX;   // staged window capacity (particles): 1920 sent 6 % of the C5 tiles to global mode
 
 // tile geometry shared by every tile kernel (the window arrays follow in the derived structs)
 struct TileHead {
@@ -211,7 +217,7 @@ __device__ __forceinline__ float signed_volume(float rho, float tagw, float m) {
 // particle instead of one reciprocal per pair).  Split in two: relativize_load requests the lo parts
 // of the thread's window slots (registers) BEFORE the staging wait, relativize_apply converts after
 // it, so the global latency of lo hides behind the staging.
-constexpr int RELK = (WMAX + 383) / 384;   // window slots per thread (blockDim >= 384)
+constexpr int RELK = (WMAX + TILE_THREADS - 1) / TILE_THREADS;   // window slots per thread (blockDim == TILE_THREADS)
 struct RelPre {
   float4 l[RELK];
 };
