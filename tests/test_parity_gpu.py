@@ -176,6 +176,32 @@ def test_rates_settling_block_bilateral(crm):
     assert rel_linf(da[:nf], db[:nf]) <= 1e-3
 
 
+def test_slope_rotated_gravity(crm):
+    """Slopes as in the MGRU3 runs ('we modified the direction of the gravitational
+    acceleration vector ... instead of tilting all the elements'): a 20 deg ramp, gravity
+    g (sin 20, 0, -cos 20).  Rates at S0 within the bar, and the block creeps downhill (+x) on both
+    sides by the same amount over 60 steps."""
+    th = np.radians(20.0)
+    sc = workloads.rate_state_S0(workloads.block_settle())
+    sc.params["gravity"] = (9.81 * np.sin(th), 0.0, -9.81 * np.cos(th))
+    g, o = run_one_armed(crm, sc, sc.dt)
+    nf = sc.n_fluid
+    for stage in (0, 1):
+        for a_g, a_o in zip(g.last_rates(stage), o.last_rates(stage)):
+            assert rel_linf(a_g[:nf], a_o[:nf]) <= RATE_TOL, stage
+        for a_g, a_o in zip(g.last_bce(stage), o.last_bce(stage)):
+            assert rel_linf(a_g[nf:], a_o[nf:]) <= RATE_TOL, stage
+    sc = workloads.block_settle()
+    sc.params["gravity"] = (9.81 * np.sin(th), 0.0, -9.81 * np.cos(th))
+    g, o = both(crm, sc)
+    g.step(sc.dt, 60)
+    o.step(sc.dt, 60)
+    ug, uo = g.get_state()[1][:nf], o.get_state()[1][:nf]
+    assert ug[:, 0].mean() > 0 and uo[:, 0].mean() > 0            # downhill
+    assert abs(ug[:, 0].mean() - uo[:, 0].mean()) <= 0.02 * abs(uo[:, 0].mean())
+    assert np.abs(g.get_state()[0][:nf] - o.get_state()[0][:nf]).max() < 0.02 * sc.params["d0"]
+
+
 # ---------------------------------------------------------------- macroscopic (2 %)
 def settled_height(pos, ids_top, d0):
     return pos[ids_top, 2].mean() + 0.5 * d0
