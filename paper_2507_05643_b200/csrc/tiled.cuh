@@ -32,7 +32,7 @@ __device__ __forceinline__ void load_all(const TileSmem& sm, const float4* __res
   }
 }
 
-// the same for the rates pair loops: .w = the signed volume V_j (see tile_relativize<true>)
+// the same for the rates pair loops: .w = the signed volume V_j (see relativize_apply<true>)
 template <bool STAGED>
 __device__ __forceinline__ void load_rates(const TileSmem& sm, const float4* __restrict__ P, const float4* __restrict__ L,
                                            const float4* __restrict__ U, const float4* __restrict__ S1,
@@ -152,7 +152,7 @@ __global__ void TILE_BOUNDS
     tile_stage(P, U, S1, S2, sm);
     tile_stage_wait();
     __syncthreads();
-    tile_relativize<false>(L, sm, 0.f);
+    tile_relativize(L, sm);
     __syncthreads();
     if (sm.staged) bce_tile<STAGE, KER, true>(ph, sm, P, L, U, S1, S2, list, nlist, pose, ls, dbg, dbg_on);
     else bce_tile<STAGE, KER, false>(ph, sm, P, L, U, S1, S2, list, nlist, pose, ls, dbg, dbg_on);

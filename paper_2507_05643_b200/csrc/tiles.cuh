@@ -41,7 +41,7 @@ struct TileHead {
   uint32_t wcs[WR][TZ + 3];     // cellStart of the run's cells zlo..zhi, plus the end
   uint32_t col_start[NCOL];     // first i of each tile column
   uint32_t col_pref[NCOL + 1];  // prefix of i counts
-  int zlo, zhi, staged, any;
+  int zlo, zhi, staged;
   int X0, Y0;
   float ox, oy, oz;             // tile origin: pair loops use positions relative to it
 };
@@ -167,7 +167,6 @@ __device__ __forceinline__ void tile_setup(const Grid& g, const TileGeom& G, con
       sm.oy = g.lo[1] + (float)G.Y0 * g.s;
       sm.oz = g.lo[2] + (float)G.z0 * g.s;
       sm.staged = total <= (uint32_t)WMAX;
-      sm.any = 0;
     }
   }
   __syncthreads();
@@ -249,8 +248,8 @@ __device__ __forceinline__ void relativize_apply(TileSmem& sm, const RelPre& rp,
     }
   }
 }
-template <bool TO_V>
-__device__ __forceinline__ void tile_relativize(const float4* __restrict__ L, TileSmem& sm, float m) {
+// the BCE kernels' single-pass variant (densities kept: the Adami stress needs rho_f)
+__device__ __forceinline__ void tile_relativize(const float4* __restrict__ L, TileSmem& sm) {
   if (!sm.staged) return;
   // a flat element loop (balanced over the threads, unlike one warp per run); the run of an
   // element by binary search over the 16 run bases
@@ -259,10 +258,7 @@ __device__ __forceinline__ void tile_relativize(const float4* __restrict__ L, Ti
     int r = 0;
 #pragma unroll
     for (int step = WR / 2; step > 0; step >>= 1) r += (sm.run_base[r + step] <= idx) ? step : 0;
-    const uint32_t gidx = sm.run_start[r] + (idx - sm.run_base[r]);
-    float4 p = rel_pos(sm.P[idx], L[gidx], sm);
-    if (TO_V) p.w = signed_volume(p.w, sm.U[idx].w, m);
-    sm.P[idx] = p;
+    sm.P[idx] = rel_pos(sm.P[idx], L[sm.run_start[r] + (idx - sm.run_base[r])], sm);
   }
 }
 
