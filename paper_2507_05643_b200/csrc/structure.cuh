@@ -60,26 +60,35 @@ __global__ void k_bin(int n, const float4* __restrict__ P, const float4* __restr
                       uint32_t* __restrict__ key, uint32_t* __restrict__ arrival, uint32_t* __restrict__ cell_count,
                       ErrLatch* err, long long step) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  if ((drop_mask && (tag_of(U[i].w) & drop_mask)) || (act && act[i] == 2)) {
-    key[i] = g.M;
-    arrival[i] = atomicAdd(&cell_count[g.M], 1u);
-    return;
-  }
-  const float4 p = P[i];
-  float f[3] = {b1_floor(p.x, g.lo[0], g.s), b1_floor(p.y, g.lo[1], g.s), b1_floor(p.z, g.lo[2], g.s)};
-  int c3[3];
-  bool ok = true;
+  const bool valid = i < n;
+  uint32_t c = g.M;
+  if (valid && !((drop_mask && (tag_of(U[i].w) & drop_mask)) || (act && act[i] == 2))) {
+    const float4 p = P[i];
+    float f[3] = {b1_floor(p.x, g.lo[0], g.s), b1_floor(p.y, g.lo[1], g.s), b1_floor(p.z, g.lo[2], g.s)};
+    int c3[3];
+    bool ok = true;
 #pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    const bool in = (f[a] >= 0.0f) && (f[a] < (float)g.dims[a]);   // false for NaN too
-    ok = ok && in;
-    c3[a] = in ? (int)f[a] : 0;
+    for (int a = 0; a < 3; ++a) {
+      const bool in = (f[a] >= 0.0f) && (f[a] < (float)g.dims[a]);   // false for NaN too
+      ok = ok && in;
+      c3[a] = in ? (int)f[a] : 0;
+    }
+    if (!ok) latch_error(err, -2 /*CRM_E_DOMAIN*/, (long long)ids[i], step, 0);
+    c = (uint32_t)c3[0] * (uint32_t)(g.dims[1] * g.dims[2]) + (uint32_t)c3[1] * (uint32_t)g.dims[2] + (uint32_t)c3[2];
   }
-  if (!ok) latch_error(err, -2 /*CRM_E_DOMAIN*/, (long long)ids[i], step, 0);
-  const uint32_t c = (uint32_t)c3[0] * (uint32_t)(g.dims[1] * g.dims[2]) + (uint32_t)c3[1] * (uint32_t)g.dims[2] + (uint32_t)c3[2];
+  // arrival rank inside the cell: one atomic per distinct cell of the warp (the input is in the
+  // previous step's cell order, so a warp covers few cells); only a temporary slot — the final
+  // order inside a cell is by id (k_reorder)
+  const unsigned vm = __ballot_sync(0xffffffffu, valid);
+  if (!valid) return;
+  const int lane = threadIdx.x & 31;
+  const unsigned peers = __match_any_sync(vm, c);
+  const int leader = __ffs(peers) - 1;
+  uint32_t base = 0;
+  if (lane == leader) base = atomicAdd(&cell_count[c], (uint32_t)__popc(peers));
+  base = __shfl_sync(peers, base, leader);
   key[i] = c;
-  arrival[i] = atomicAdd(&cell_count[c], 1u);
+  arrival[i] = base + (uint32_t)__popc(peers & ((1u << lane) - 1u));
 }
 
 // ---------------------------------------------------------------------------------------
