@@ -113,6 +113,27 @@ def test_rates_stage_A_and_B_S0(crm, visc):
         assert rel_linf(tg[nf:], to[nf:]) <= RATE_TOL, ("bce sigma", stage)
 
 
+def test_rates_state_S100(crm):
+    """rate parity at S100 — the GPU's own state after 100 steps of the jittered
+    settling block, loaded into the oracle with set_state (identical fp32 inputs, so identical
+    neighbour sets): one more armed step, stage-A and stage-B rates and BCE values within 1e-4."""
+    sc = workloads.block_settle(jitter=0.05, seed=0)
+    g = crm.load_scenario(sc)
+    g.step(sc.dt, 100)
+    o = oracle.load_scenario(sc)
+    o.set_state(0, *g.get_state())
+    assert_structure_equal(g, o)
+    g.debug_arm(True)
+    g.step(sc.dt, 1)
+    o.step(sc.dt, 1)
+    nf = sc.n_fluid
+    for stage in (0, 1):
+        for a_g, a_o in zip(g.last_rates(stage), o.last_rates(stage)):
+            assert rel_linf(a_g[:nf], a_o[:nf]) <= RATE_TOL, stage
+        for a_g, a_o in zip(g.last_bce(stage), o.last_bce(stage)):
+            assert rel_linf(a_g[nf:], a_o[nf:]) <= RATE_TOL, stage
+
+
 @pytest.mark.parametrize("visc", [workloads.VISC_BILATERAL, workloads.VISC_UNILATERAL])
 def test_rates_wendland_S0(crm, visc):
     """Quintic Wendland kernel (A28): same bars as the cubic spline."""
