@@ -29,9 +29,9 @@ def build(force: bool = False) -> str:
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < max(
             os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "crm_oracle.h"))):
         cmd = ["gcc", "-std=gnu11", "-O2", "-fopenmp", "-ffp-contract=off", "-fno-fast-math",
-               "-fPIC", "-shared", "-o", _LIB + ".tmp", _SRC, "-lm"]
+               "-fPIC", "-shared", "-o", f"{_LIB}.{os.getpid()}.tmp", _SRC, "-lm"]
         subprocess.check_call(cmd, cwd=_HERE)
-        os.replace(_LIB + ".tmp", _LIB)
+        os.replace(f"{_LIB}.{os.getpid()}.tmp", _LIB)
     return _LIB
 
 

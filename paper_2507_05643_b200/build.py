@@ -33,20 +33,34 @@ def nccl_paths():
         return None, None
 
 
+def _fresh() -> bool:
+    return os.path.exists(LIB) and os.path.getmtime(LIB) >= max(os.path.getmtime(s) for s in _sources())
+
+
 def build_library(force: bool = False, verbose: bool = False) -> str:
-    srcs = _sources()
-    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= max(os.path.getmtime(s) for s in srcs):
+    if not force and _fresh():
         return LIB
+    # several processes (torchrun ranks) may get here at once: one builds, the others wait for it
+    import fcntl
+    with open(LIB + ".lock", "w") as lock:
+        fcntl.flock(lock, fcntl.LOCK_EX)
+        if not force and _fresh():
+            return LIB
+        return _build(verbose)
+
+
+def _build(verbose: bool) -> str:
     nvcc = os.environ.get("NVCC", "nvcc")
     inc, lib = nccl_paths()
     if inc is None:
         raise RuntimeError("nccl.h not found (nvidia-nccl wheel)")
-    cmd = [nvcc, *NVCC_FLAGS, "-I", inc, f'-DCRM_NCCL_DEFAULT="{lib}"', "-o", LIB + ".tmp",
+    tmp = f"{LIB}.{os.getpid()}.tmp"
+    cmd = [nvcc, *NVCC_FLAGS, "-I", inc, f'-DCRM_NCCL_DEFAULT="{lib}"', "-o", tmp,
            os.path.join(CSRC, "crm.cu"), "-ldl"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.check_call(cmd, cwd=ROOT)
-    os.replace(LIB + ".tmp", LIB)
+    os.replace(tmp, LIB)
     return LIB
 
 
