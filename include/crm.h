@@ -84,7 +84,10 @@ typedef struct {
   double gamma_a;         /* artificial viscosity coefficient */
   double xi2;             /* regulariser xi^2 of Eq. 13; <= 0 -> 0.01 h^2 (A10) */
   double cs;              /* speed of sound; <= 0 -> sqrt(K / rho0) (A10) */
-  int    ps_freq;         /* neighbour-list rebuild period (Alg. 2); 0 -> 1 */
+  int    ps_freq;         /* neighbour-list rebuild period (Alg. 2); 0 -> 1.  With ps_freq > 1
+                             the stored lists are permuted into a bank-conflict-avoiding order at each
+                             rebuild (same neighbour sets; A34; env CRM_LIST_ORDER=rr|scan
+                             overrides the choice at crm_create) */
   double gravity[3];      /* body force per unit mass f_b */
   int    max_neighbors;   /* neighbour-list capacity per particle; 0 -> derived from h/d0 */
 } crm_kernel_t;

@@ -2,7 +2,7 @@
 //
 // One crm_step(dt, n) issues, per step, on the context's stream:
 //   memset counts | k_bin | scan (k_scan_tiles, k_scan_add) | k_scatter | k_reorder |
-//   k_filter_t (Alg. 1 lists, rebuild steps) | k_bce_t<0> (extrapolation) | k_rates_t<0> (rates + half step) |
+//   k_filter_t (Alg. 1 lists, rebuild steps) [| k_list_rr (ps_freq > 1)] | k_bce_t<0> (extrapolation) | k_rates_t<0> (rates + half step) |
 //   [k_markers_place(mid)] | k_bce_t<1> | k_rates_t<1> (rates + full step + return map) |
 //   [k_body_update | k_body_poses | k_markers_place]
 // and synchronises once at the end to read the device error latch.  With world > 1 the same
@@ -42,6 +42,7 @@ void set_attrs(crm_t* c) {
   if (c->attrs_set) return;
   const int sm = (int)sizeof(TileSmem);
   cudaFuncSetAttribute(k_filter_t, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FilterSmem));
+  cudaFuncSetAttribute(k_list_rr, cudaFuncAttributeMaxDynamicSharedMemorySize, c->cap * RR_THREADS * 2);
   cudaFuncSetAttribute(k_bce_t<0, KER_CUBIC>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
   cudaFuncSetAttribute(k_bce_t<1, KER_CUBIC>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
   cudaFuncSetAttribute(k_rates_t<0, KER_CUBIC>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
@@ -367,9 +368,21 @@ void issue_filter(crm_t* c, long long step, int store_all) {
               (const uint32_t*)c->ids[y], step, c->tile_base, tile_list(c), c->d_mtiles, c->d_mtile_cnt);
 }
 
+// the lists in bank-group round-robin order (listorder.cuh): a permutation of every stored row
+void issue_list_rr(crm_t* c) {
+  const long long rows = c->boxes.empty() ? (long long)c->n : (long long)c->n_ae;
+  if (rows == 0) return;
+  launch_smem(c, KID_LISTORDER, k_list_rr, dim3(blocks(rows, RR_THREADS)), dim3(RR_THREADS),
+              (size_t)c->cap * RR_THREADS * 2, (int)rows, c->grid, (const uint32_t*)c->cell_of,
+              (const uint32_t*)c->cell_start, c->list, (const uint32_t*)c->nlist, list_shape(c));
+}
+
 void issue_bce(crm_t* c, int stage, float dt, long long step, int store_all) {
   (void)dt;
-  if (stage == 0 && c->ph.build_lists) issue_filter(c, step, store_all);
+  if (stage == 0 && c->ph.build_lists) {
+    issue_filter(c, step, store_all);
+    if (c->list_rr && !store_all) issue_list_rr(c);
+  }
   if (!c->n_bce) return;
   if (c->ker.kernel == CRM_KERNEL_WENDLAND) issue_bce_k<KER_WENDLAND>(c, stage, step);
   else issue_bce_k<KER_CUBIC>(c, stage, step);
@@ -656,6 +669,13 @@ int crm_create(const crm_material_t* mat, const crm_kernel_t* ker, const crm_bou
   } else {
     const double ball = 4.0 / 3.0 * M_PI * std::pow(R / k.d0, 3.0);
     c->cap = std::max(32, (int)(32 * std::ceil(2.0 * ball / 32.0)));
+  }
+  // bank-group round-robin list order: pays where lists are reused (Alg. 2, ps_freq > 1);
+  // CRM_LIST_ORDER=rr|scan overrides (measurement); byte counters need cap <= 255
+  {
+    const char* lo = std::getenv("CRM_LIST_ORDER");
+    c->list_rr = lo ? std::strcmp(lo, "rr") == 0 : c->ps_freq > 1;
+    if (c->cap > 255) c->list_rr = false;
   }
   // distribution
   if (dist && dist->world > 1) {
