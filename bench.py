@@ -365,6 +365,14 @@ def main():
     hbm = {"bytes_per_step": alg_bytes, "achieved_gbs": alg_bytes / (ms_step * 1e-3) / 1e9,
            "peak_gbs": pk["hbm_gbs"], "frac": alg_bytes / (ms_step * 1e-3) / 1e9 / pk["hbm_gbs"]}
     kernels = {k: {"ms_per_step": v[0] / args.steps, "launches": v[1]} for k, v in sorted(prof.items())}
+    # the same ALU roofline for each of the three hot kernels (the line's `roofline` is the largest)
+    n_own_k = g.count(crm.CRM_OWNED) if world > 1 else n_fluid
+    for k in ("k_filter", "k_rates_A", "k_rates_B"):
+        if k in prof and prof[k][1]:
+            fl = ((cand_local + cand_markers) * FLOPS_PER_CANDIDATE if k == "k_filter"
+                  else pairs_local * FLOPS_PER_PAIR + min(n_own_k, n_fluid) * FLOPS_EPILOGUE[k])
+            tf = fl / (prof[k][0] / prof[k][1] * 1e-3) / 1e12
+            kernels[k].update({"alu_tflops": tf, "alu_frac": tf / fp32_peak_tflops(pk["sm_max_mhz"])})
 
     # e2e through the public API with pinned host buffers
     e2e = None
