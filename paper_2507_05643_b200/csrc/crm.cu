@@ -1157,7 +1157,10 @@ int crm_debug_neighbors(crm_t* c, int64_t* offsets, int64_t* list) {
   issue_rates(c, 0, 0.0f, c->steps_done);
   const size_t n = (size_t)c->n;
   const size_t nv = c->boxes.empty() ? n : (size_t)c->n_ae;   // slots that have lists (Alg. 3)
-  if (!c->list32 && dalloc(c, &c->list32, n * (size_t)c->cap)) return CRM_E_OOM;
+  if (!c->list32) {
+    if (dalloc(c, &c->list32, n * (size_t)c->cap)) return CRM_E_OOM;
+    cudaMemsetAsync(c->list32, 0, n * (size_t)c->cap * 4, c->stream);   // rows are copied whole
+  }
   if (nv)
     launch(c, KID_DECODE, k_decode_lists, dim3(blocks((long long)nv, 256)), dim3(256), (int)nv, c->grid,
            (const uint32_t*)c->cell_start, (const uint32_t*)c->cell_of, (const uint16_t*)c->list,

@@ -349,11 +349,12 @@ struct ListWriter {
     ++k;
     if ((k & 3) == 0) store(k);
   }
-  // pad the last chunk of 8 with `fill` (a zero-weight entry); k keeps the unpadded count
+  // pad the last chunk of 8 with `fill` (a zero-weight entry); k keeps the unpadded count.  An empty
+  // list still gets one chunk of padding: the pair kernels prefetch chunk 0 of every list.
   __device__ __forceinline__ void flush(uint32_t fill) {
     if (k >= cap) return;   // cap % 8 == 0: the stored part ends on a chunk boundary
     int kk = k;
-    while (kk & 7) {
+    while ((kk & 7) || kk == 0) {
       b0 = __funnelshift_r(b0, b1, 16);
       b1 = __funnelshift_r(b1, fill, 16);
       ++kk;
