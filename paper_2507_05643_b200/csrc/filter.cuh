@@ -23,6 +23,7 @@ namespace crmk {
 // FP32 instructions of sm_100 (FADD2/FMUL2/FFMA2: per element the same IEEE round-to-nearest
 // results as the scalar instructions, half the issue slots; this kernel is issue-bound).
 struct FilterSmem : TileHead {
+  int mzmin, mzmax;                 // cells z of the tile's markers (min, max)
   alignas(16) float X[WMAX + 40];   // absolute positions (a chunk may read up to 39 slots past a segment)
   float Y[WMAX + 40];
   float Z[WMAX + 40];
@@ -179,6 +180,10 @@ __device__ __forceinline__ int filter_tile(const Grid& g, const FilterSmem& sm, 
     const float4 pi = STAGED ? make_float4(sm.X[self], sm.Y[self], sm.Z[self], 0.f) : P[i];
     const bool bce = tag_is_bce(tag_of(U[i].w));
     has_marker |= bce ? 1 : 0;
+    if (bce) {
+      atomicMin(const_cast<int*>(&sm.mzmin), cz);
+      atomicMax(const_cast<int*>(&sm.mzmax), cz);
+    }
     const bool fluid_only = !store_all && bce;
     ListWriter w;
     w.init(list, i, ls);
@@ -217,12 +222,20 @@ __global__ void __launch_bounds__(FILTER_THREADS, CRM_FILTER_MINB)
     return;
   }
   filter_stage(P, U, sm);
+  if (threadIdx.x == 0) {
+    sm.mzmin = 0x7fffffff;
+    sm.mzmax = -1;
+  }
   tile_stage_wait();
   __syncthreads();
   const int has = sm.staged ? filter_tile<true>(g, sm, P, U, list, nlist, count_all, cell_of, ls, store_all, err, ids, step)
                             : filter_tile<false>(g, sm, P, U, list, nlist, count_all, cell_of, ls, store_all, err, ids, step);
   // the tiles holding markers: the BCE kernels run over these only (any order: tiles are independent)
-  if (__syncthreads_or(has) && threadIdx.x == 0) mtiles[atomicAdd(mcount, 1u)] = (uint32_t)tile;
+  // with the rows z0 + zl .. z0 + zh (0 <= zl <= zh < TZ) that hold them in bits 28-31 (tiles < 2^28)
+  if (__syncthreads_or(has) && threadIdx.x == 0) {
+    const uint32_t zl = (uint32_t)(sm.mzmin - G.z0) & 3u, zh = (uint32_t)(sm.mzmax - G.z0) & 3u;
+    mtiles[atomicAdd(mcount, 1u)] = (uint32_t)tile | (zl << 28) | (zh << 30);
+  }
 }
 
 }  // namespace crmk

@@ -142,17 +142,22 @@ __global__ void TILE_BOUNDS
   const uint32_t ntile = *mcount;
   for (uint32_t k = blockIdx.x; k < ntile; k += gridDim.x) {
     __syncthreads();   // the previous tile's window is no longer read
-    const TileGeom G = tile_geom(g, (long long)mtiles[k]);
+    const uint32_t mt = mtiles[k];
+    const TileGeom G = tile_geom(g, (long long)(mt & 0x0fffffffu));
     tile_setup(g, G, cell_start, sm);
     if (sm.col_pref[NCOL] == 0) continue;
     if (sm.run_base[WR] > 65535u) {
       if (threadIdx.x == 0) latch_error(err, -9, -1, step, (long long)sm.run_base[WR]);
       continue;
     }
-    tile_stage(P, U, S1, S2, sm);
+    // only the cells within one of the markers' rows (z0 + zl .. z0 + zh, recorded by the filter):
+    // every entry of a marker's list lies there (floor tiles: about half of the window)
+    const int zmk = G.z0 + (int)((mt >> 28) & 3u), zMk = G.z0 + (int)(mt >> 30);
+    const int klo = max(zmk - 1, G.zlo) - G.zlo, khi = min(zMk + 1, G.zhi) - G.zlo + 1;
+    tile_stage_cells(P, U, S1, S2, sm, klo, khi);
     tile_stage_wait();
     __syncthreads();
-    tile_relativize(L, sm);
+    tile_relativize_cells(L, sm, klo, khi);
     __syncthreads();
     if (sm.staged) bce_tile<STAGE, KER, true>(ph, sm, P, L, U, S1, S2, list, nlist, pose, ls, dbg, dbg_on);
     else bce_tile<STAGE, KER, false>(ph, sm, P, L, U, S1, S2, list, nlist, pose, ls, dbg, dbg_on);

@@ -194,6 +194,28 @@ __device__ __forceinline__ void tile_stage(const float4* __restrict__ P, const f
   __pipeline_commit();
 }
 
+// BCE kernels: only the cells klo..khi-1 (relative to zlo) of every run, at their usual window
+// offsets (the markers' list entries lie within one cell of the markers' cells)
+__device__ __forceinline__ void tile_stage_cells(const float4* __restrict__ P, const float4* __restrict__ U,
+                                                 const float4* __restrict__ S1, const float2* __restrict__ S2,
+                                                 TileSmem& sm, int klo, int khi) {
+  if (!sm.staged) return;
+  const uint32_t lane = threadIdx.x & 31u, nw = blockDim.x >> 5;
+  for (uint32_t r = threadIdx.x >> 5; r < (uint32_t)WR; r += nw) {
+    const uint32_t rs = sm.run_start[r], rb = sm.run_base[r];
+    const uint32_t b = rb + (sm.wcs[r][klo] - rs), e = rb + (sm.wcs[r][khi] - rs);
+    const int shift = (int)rs - (int)rb;
+    for (uint32_t idx = b + lane; idx < e; idx += 32) {
+      const uint32_t gidx = (uint32_t)((int)idx + shift);
+      __pipeline_memcpy_async(&sm.P[idx], &P[gidx], sizeof(float4));
+      __pipeline_memcpy_async(&sm.U[idx], &U[gidx], sizeof(float4));
+      __pipeline_memcpy_async(&sm.S1[idx], &S1[gidx], sizeof(float4));
+      __pipeline_memcpy_async(&sm.S2[idx], &S2[gidx], sizeof(float2));
+    }
+  }
+  __pipeline_commit();
+}
+
 __device__ __forceinline__ void tile_stage_wait() { __pipeline_wait_prior(0); }
 
 // Positions are stored compensated, x = hi + lo (hi: the fp32 value the structural rules B1/B2
@@ -248,7 +270,18 @@ __device__ __forceinline__ void relativize_apply(TileSmem& sm, const RelPre& rp,
     }
   }
 }
-// the BCE kernels' single-pass variant (densities kept: the Adami stress needs rho_f)
+// the BCE kernels' variant (densities kept: the Adami stress needs rho_f) over the staged cells
+// klo..khi-1 of every run, one warp per run
+__device__ __forceinline__ void tile_relativize_cells(const float4* __restrict__ L, TileSmem& sm, int klo, int khi) {
+  if (!sm.staged) return;
+  const uint32_t lane = threadIdx.x & 31u, nw = blockDim.x >> 5;
+  for (uint32_t r = threadIdx.x >> 5; r < (uint32_t)WR; r += nw) {
+    const uint32_t rs = sm.run_start[r], rb = sm.run_base[r];
+    const uint32_t b = rb + (sm.wcs[r][klo] - rs), e = rb + (sm.wcs[r][khi] - rs);
+    for (uint32_t idx = b + lane; idx < e; idx += 32) sm.P[idx] = rel_pos(sm.P[idx], L[rs + (idx - rb)], sm);
+  }
+}
+// (whole-window single pass)
 __device__ __forceinline__ void tile_relativize(const float4* __restrict__ L, TileSmem& sm) {
   if (!sm.staged) return;
   // a flat element loop (balanced over the threads, unlike one warp per run); the run of an
