@@ -27,7 +27,7 @@ struct FilterSmem : TileHead {
   alignas(16) float X[WMAX + 40];   // absolute positions (a chunk may read up to 39 slots past a segment)
   float Y[WMAX + 40];
   float Z[WMAX + 40];
-  uint8_t bce[WMAX + 40];    // 1 = BCE marker
+  alignas(4) uint8_t bce[WMAX + 40];    // 1 = BCE marker
 };
 
 // positions + flags of the window (LDGSTS for the positions)
@@ -108,10 +108,11 @@ __device__ __forceinline__ void filter_range(float R2, const FilterSmem& sm, con
       for (uint32_t k8 = 0; k8 < nc; k8 += 8) {
         uint32_t gm = 0, gf = 0;
         gm = b2_group8(sm, base + k8, xi2, yi2, zi2, R2x2);
-        if (!STORE_BCE) {
-#pragma unroll
-          for (int e = 0; e < 8; ++e) gf |= sm.bce[base + k8 + e] ? 0u : (1u << e);
-          gf &= gm;
+        if (!STORE_BCE) {   // the 8 flags (bytes 0/1) in two 4-B loads, packed to bits by multiplies
+          const uint32_t f0 = *reinterpret_cast<const uint32_t*>(&sm.bce[base + k8]);
+          const uint32_t f1 = *reinterpret_cast<const uint32_t*>(&sm.bce[base + k8 + 4]);
+          const uint32_t fb = ((f0 * 0x01020408u) >> 24) | (((f1 * 0x01020408u) >> 20) & 0xf0u);
+          gf = gm & ~fb;
         }
         m |= gm << k8;
         mf |= gf << k8;
