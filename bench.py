@@ -156,6 +156,10 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        # torchrun pins OMP_NUM_THREADS=1 per rank; rank 0 runs alone here, so the oracle gets the
+        # host's cores as at N = 1 (read by libgomp when liboracle loads, below)
+        os.environ["OMP_NUM_THREADS"] = str(len(os.sched_getaffinity(0)))
     cb = oracle_rate(args.config, max(1, args.steps + args.warmup) if args.config == "block8k" else 1)
     # warm-up + timed steps of the oracle itself on the sample (bounded: one sample step per bench step)
     import oracle
