@@ -223,13 +223,16 @@ __device__ __forceinline__ void pair_loop(PairAcc& A, const Phys& ph, const Tile
   const uint4* seg = reinterpret_cast<const uint4*>(list) + i;
   const size_t ls_stride = ls.stride;
   const uint32_t nch = (nl + 7) >> 3;
-  // the list streams from HBM (written by the filter, larger than L2): chunk c + 1 is requested
-  // before chunk c is processed so its latency hides behind 8 pair evaluations; chunk 0 comes
-  // from the caller (requested before the window staging)
+  // the list streams from HBM (written by the filter, larger than L2): chunks c + 1 and c + 2 are in
+  // flight while chunk c is processed, so their latency hides behind 8-16 pair evaluations; chunk 0
+  // comes from the caller (requested before the window staging).  Two ahead instead of one:
+  // k_rates_A 13.52 -> 13.37 ms, k_rates_B 13.94 -> 13.74 ms (4 more spilled words, outside the loop)
   uint4 vn = first;
+  uint4 vn2 = seg[nch > 1 ? ls_stride : 0];   // an empty list (nch = 0) has only chunk 0
   for (uint32_t c = 0; c < nch; ++c) {   // whole padded chunks of 8, branch-free
     const uint4 v = vn;
-    vn = seg[(size_t)min(c + 1, nch - 1) * ls_stride];
+    vn = vn2;
+    vn2 = seg[(size_t)min(c + 2, nch - 1) * ls_stride];
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       float4 pj, uj, s1;
