@@ -226,7 +226,8 @@ __device__ __forceinline__ void pair_loop(PairAcc& A, const Phys& ph, const Tile
   // the list streams from HBM (written by the filter, larger than L2): chunks c + 1 and c + 2 are in
   // flight while chunk c is processed, so their latency hides behind 8-16 pair evaluations; chunk 0
   // comes from the caller (requested before the window staging).  Two ahead instead of one:
-  // k_rates_A 13.52 -> 13.37 ms, k_rates_B 13.94 -> 13.74 ms (4 more spilled words, outside the loop)
+  // k_rates_A 13.52 -> 13.37 ms, k_rates_B 13.94 -> 13.74 ms (4 more spilled words, outside the loop);
+  // three ahead ran 14.26 / 14.54 ms (register pressure)
   uint4 vn = first;
   uint4 vn2 = seg[nch > 1 ? ls_stride : 0];   // an empty list (nch = 0) has only chunk 0
   for (uint32_t c = 0; c < nch; ++c) {   // whole padded chunks of 8, branch-free
