@@ -109,7 +109,7 @@ typedef struct {
 
 /* Rigid body carrying BCE markers.  Body 0 = the static walls. */
 typedef struct {
-  double mass, inertia[3];        /* inertia: principal moments, treated as world-axis aligned */
+  double mass, inertia[3];        /* inertia: principal moments about the body axes (Euler equations) */
   double pos[3], quat[4];         /* centre of mass, orientation (w, x, y, z) */
   double vel[3], omega[3];
   int    motion;                  /* CRM_BODY_* */
@@ -132,8 +132,10 @@ int  crm_add_body(crm_t* ctx, const crm_body_t* body, int32_t* body_id);
 int  crm_add_bce(crm_t* ctx, int32_t body, int64_t n, const double* pos_world, int64_t* first_id);
 
 /* Advance nsteps explicit RK2 steps of size dt (synchronous).  Returns the first error latched
- * on the device (CRM_E_DOMAIN, CRM_E_NONFINITE, CRM_E_CAPACITY) with the id and step in
- * crm_last_error.  With world > 1 and an NCCL id, every rank calls crm_step with the same
+ * on the device (CRM_E_DOMAIN, CRM_E_NONFINITE, CRM_E_CAPACITY) with the id and the step in
+ * which it occurred in crm_last_error (a device step counter, also inside replayed CUDA graphs).
+ * The steps after the failing one compute nothing: the state is the one the failing step left,
+ * and the call returns after nsteps launches with that first error.  With world > 1 and an NCCL id, every rank calls crm_step with the same
  * arguments; ghost planes are exchanged with NCCL point-to-point transfers (CRM_E_COMM). */
 int  crm_step(crm_t* ctx, double dt, int64_t nsteps);
 
@@ -221,7 +223,10 @@ int     crm_candidate_count(crm_t* ctx, int64_t* fluid_candidates, int64_t* mark
 int  crm_debug_arm(crm_t* ctx, int on);
 /* Structure of the CURRENT state (what the next step builds first): cell id per particle id,
  * the sorted id order, neighbour counts per id (all fluid + BCE neighbours), cellStart (M+1).
- * Any pointer may be NULL; *n_cells receives M. */
+ * Any pointer may be NULL; *n_cells receives M.  Both structure exports re-sort the state and
+ * rebuild the lists off the Alg. 2 schedule, so the step after an export is a rebuild step
+ * (with ps_freq > 1 an inspected run therefore differs from an uninspected one; at ps_freq = 1,
+ * where every step rebuilds, it does not). */
 int  crm_debug_structure(crm_t* ctx, uint32_t* cell_by_id, int64_t* sorted_ids,
                          uint32_t* nbr_count_by_id, uint32_t* cell_start, int64_t* n_cells);
 /* Neighbour sets of the CURRENT state by id, CSR (offsets n+1), rows ascending by id. */

@@ -911,11 +911,24 @@ static int step_once(oc_sim* s, double dt) {
     }
     for (int c = 0; c < 3; ++c) { r->force[c] = F[c]; r->torque[c] = T[c]; }
     if (r->b.motion == OC_BODY_FREE) {
-      /* semi-implicit Euler (the multibody engine itself is out of scope) */
+      /* semi-implicit Euler (the multibody engine itself is out of scope).  Rotation by
+       * Euler's equations in the body's principal frame (inertia = principal moments about the
+       * body axes): I alpha_b = T_b - omega_b x (I omega_b), with T_b = R^T T, omega_b = R^T omega
+       * at t_n, and alpha = R alpha_b; the DOF mask locks world axes (a locked axis keeps its
+       * omega component). */
+      double Rb[9], wb[3], Tb[3], Iw[3], gyro[3], ab[3];
+      quat_to_R(r->b.quat, Rb);
+      for (int a = 0; a < 3; ++a) {
+        wb[a] = Rb[a] * r->b.omega[0] + Rb[3 + a] * r->b.omega[1] + Rb[6 + a] * r->b.omega[2];
+        Tb[a] = Rb[a] * T[0] + Rb[3 + a] * T[1] + Rb[6 + a] * T[2];
+      }
+      for (int a = 0; a < 3; ++a) Iw[a] = r->b.inertia[a] * wb[a];
+      cross(wb, Iw, gyro);
+      for (int a = 0; a < 3; ++a) ab[a] = r->b.inertia[a] > 0 ? (Tb[a] - gyro[a]) / r->b.inertia[a] : 0.0;
       for (int c = 0; c < 3; ++c) {
         const int tfree = (r->b.dof_mask >> c) & 1, rfree = (r->b.dof_mask >> (3 + c)) & 1;
         r->acc[c] = tfree ? F[c] / r->b.mass + s->P.gravity[c] : 0.0;
-        r->alpha[c] = (rfree && r->b.inertia[c] > 0) ? T[c] / r->b.inertia[c] : 0.0;
+        r->alpha[c] = rfree ? Rb[3 * c] * ab[0] + Rb[3 * c + 1] * ab[1] + Rb[3 * c + 2] * ab[2] : 0.0;
         r->b.vel[c] += dt * r->acc[c];
         r->b.omega[c] += dt * r->alpha[c];
         r->b.pos[c] += dt * r->b.vel[c];

@@ -46,7 +46,7 @@ typedef struct {
 enum { OC_KERNEL_CUBIC = 0, OC_KERNEL_WENDLAND = 1 };
 
 typedef struct {
-  double mass, inertia[3], pos[3], quat[4], vel[3], omega[3];
+  double mass, inertia[3], pos[3], quat[4], vel[3], omega[3];   /* inertia: principal moments about the body axes */
   int motion;                     /* OC_BODY_* */
   int dof_mask;                   /* FREE: bit k set = DOF k free (0..2 translation x,y,z; 3..5 rotation) */
 } oc_body;

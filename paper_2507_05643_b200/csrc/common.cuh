@@ -160,21 +160,37 @@ struct BodyState {
   int motion, dof_mask, pad0, pad1;
 };
 
-// first-error latch (written with atomicCAS on `code`)
+// first-error latch (written with atomicCAS on `code`).  cur_step is the device's step counter:
+// k_step_begin sets it (per-kernel launches) or advances it (a replayed CUDA graph, captured with
+// step = -1), and stops advancing once an error is latched, so an error names its real step.  The
+// state-writing kernels return at entry once the latch is set: the steps after the first bad one
+// compute nothing (the state stays as the failing step left it).
 struct ErrLatch {
   int code;
   int pad;
   long long step;
   long long id;
   long long aux;
+  long long cur_step;
 };
 
 __device__ __forceinline__ void latch_error(ErrLatch* e, int code, long long id, long long step, long long aux) {
   if (atomicCAS(&e->code, 0, code) == 0) {
     e->id = id;
-    e->step = step;
+    e->step = step >= 0 ? step : e->cur_step;
     e->aux = aux;
   }
+}
+
+// true once an error is latched (read at kernel entry: skip the work of the steps after it)
+__device__ __forceinline__ bool latched(const ErrLatch* e) { return *(volatile const int*)&e->code != 0; }
+
+__global__ void k_latch_set_step(ErrLatch* e, long long step) { e->cur_step = step; }
+
+// first kernel of every step: step >= 0 sets the counter, step < 0 (graph replay) advances it
+__global__ void k_step_begin(ErrLatch* e, long long step) {
+  if (e->code) return;
+  e->cur_step = step >= 0 ? step : e->cur_step + 1;
 }
 
 // Debug capture buffers (sorted order), written only when armed.

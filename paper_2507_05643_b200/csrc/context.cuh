@@ -26,13 +26,13 @@ namespace {
 enum KernelId {
   KID_MARKERS = 0, KID_BIN, KID_SCAN, KID_SCAN_ADD, KID_SCATTER, KID_REORDER,
   KID_BCE_A, KID_RATES_A, KID_BCE_B, KID_RATES_B, KID_BODY, KID_POSES, KID_STATE, KID_COPY, KID_DECODE,
-  KID_SLAB, KID_ACTIVITY, KID_FILTER, KID_LISTORDER, KID_COUNT
+  KID_SLAB, KID_ACTIVITY, KID_FILTER, KID_LISTORDER, KID_STEP, KID_COUNT
 };
 const char* kKernelNames[KID_COUNT] = {"k_markers_place", "k_bin", "k_scan_tiles", "k_scan_add", "k_scatter",
                                        "k_reorder", "k_bce_A", "k_rates_A", "k_bce_B", "k_rates_B",
                                        "k_body_update", "k_body_poses", "k_get_set_state", "k_copy_u32",
                                        "k_decode_lists", "k_slab_util", "k_activity", "k_filter",
-                                       "k_list_rr"};
+                                       "k_list_rr", "k_step_begin"};
 
 struct ProfRec {
   int kid;
@@ -110,7 +110,8 @@ struct crm {
   bool graphs = true;
   // captured single-GPU steps, keyed by (buffer parity before the step, rebuild step of Alg. 2)
   cudaGraphExec_t gexec[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
-  float gdt[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
+  double gdt[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+  double dt_d = 0.0;                    // the step of the current crm_step call (fp64: body updates)
   int gcur_after[2][2] = {{0, 0}, {0, 0}};
   int64_t gkernels[2][2] = {{0, 0}, {0, 0}};
   int ps_freq = 1;                      // Alg. 2: lists rebuilt when step % ps_freq == 0

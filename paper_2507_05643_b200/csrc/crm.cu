@@ -42,7 +42,8 @@ void set_attrs(crm_t* c) {
   if (c->attrs_set) return;
   const int sm = (int)sizeof(TileSmem);
   cudaFuncSetAttribute(k_filter_t, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FilterSmem));
-  cudaFuncSetAttribute(k_list_rr, cudaFuncAttributeMaxDynamicSharedMemorySize, c->cap * RR_THREADS * 2);
+  // the attribute belongs to the function, not the context: the largest rr buffer (cap <= 255)
+  cudaFuncSetAttribute(k_list_rr, cudaFuncAttributeMaxDynamicSharedMemorySize, 256 * RR_THREADS * 2);
   cudaFuncSetAttribute(k_bce_t<0, KER_CUBIC>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
   cudaFuncSetAttribute(k_bce_t<1, KER_CUBIC>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
   cudaFuncSetAttribute(k_rates_t<0, KER_CUBIC>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
@@ -417,20 +418,22 @@ void issue_rates(crm_t* c, int stage, float dt, long long step) {
 
 // one RK2 step on one GPU (everything on the stream, no host sync)
 // moving bodies: this rank's partial loads into its block of d_bpart (A13)
-void issue_body_partial(crm_t* c, float dt) {
+void issue_body_partial(crm_t* c) {
+  const double dt = c->dt_d;   // the caller's fp64 step (the fluid kernels take it as fp32)
   launch(c, KID_BODY, k_body_partial, dim3(c->n_moving_bodies), dim3(BODY_BS), (const int*)c->d_moving_bodies,
          (const uint32_t*)c->d_mstart, (const uint32_t*)c->d_moving_ids, (const uint32_t*)c->slot_of_id,
          (const float4*)c->U[c->cur], (const float4*)c->macc, (const float4*)c->Pm, (const float4*)c->Lm,
-         (const BodyState*)c->d_bodies, (double)dt, c->d_bpart + (size_t)c->rank * c->n_moving_bodies * 6);
+         (const BodyState*)c->d_bodies, dt, c->d_bpart + (size_t)c->rank * c->n_moving_bodies * 6);
 }
 
 // sum of the ranks' partial loads (rank order), rigid update, poses, markers at t_{n+1}
-void issue_body_finish(crm_t* c, float dt) {
+void issue_body_finish(crm_t* c) {
+  const double dt = c->dt_d;
   launch(c, KID_BODY, k_body_integrate, dim3(blocks(c->n_moving_bodies, 64)), dim3(64), c->n_moving_bodies,
-         (const int*)c->d_moving_bodies, (const double*)c->d_bpart, c->world, c->d_bodies, (double)dt, c->ph.g[0],
-         c->ph.g[1], c->ph.g[2]);
-  launch(c, KID_POSES, k_body_poses, dim3(1), dim3(64), (int)c->bodies.size(), (const BodyState*)c->d_bodies,
-         0.5 * (double)dt, c->d_pose0, c->d_posem);
+         (const int*)c->d_moving_bodies, (const double*)c->d_bpart, c->world, c->d_bodies, dt, c->ker.gravity[0],
+         c->ker.gravity[1], c->ker.gravity[2], (const ErrLatch*)c->d_err);
+  launch(c, KID_POSES, k_body_poses, dim3(blocks((long long)c->bodies.size(), 64)), dim3(64), (int)c->bodies.size(), (const BodyState*)c->d_bodies,
+         0.5 * dt, c->d_pose0, c->d_posem);
   const int y = c->cur;
   if (c->n_moving_markers)
     launch(c, KID_MARKERS, k_markers_place, dim3(blocks(c->n_moving_markers, 128)), dim3(128), c->n_moving_markers,
@@ -442,6 +445,7 @@ int issue_step(crm_t* c, float dt, long long step) {
   // Alg. 2: rebuild (sort + filtered lists) when t mod ps_freq == 0; otherwise the particles keep
   // their slots and the stored lists are reused without a distance re-check (A17)
   const bool rebuild = !c->lists_valid || (step % c->ps_freq) == 0;
+  launch(c, KID_STEP, k_step_begin, dim3(1), dim3(1), c->d_err, step);
   if (rebuild) {
     const int r = issue_rebuild_sort(c, step);
     if (r) return r;
@@ -458,8 +462,8 @@ int issue_step(crm_t* c, float dt, long long step) {
   issue_bce(c, 1, dt, step, 0);
   issue_rates(c, 1, dt, step);
   if (c->n_moving_bodies) {
-    issue_body_partial(c, dt);
-    issue_body_finish(c, dt);
+    issue_body_partial(c);
+    issue_body_finish(c);
   }
   if (c->dbg_on) cudaMemcpyAsync(c->dbg_ids, c->ids[y], (size_t)c->nl * 4, cudaMemcpyDeviceToDevice, c->stream);
   return CRM_OK;
@@ -474,7 +478,7 @@ int run_step(crm_t* c, float dt, long long step) {
   // (active domains resize arrays between steps from host-read counts: launched one by one)
   if (!c->graphs || c->prof || c->dbg_on || !c->boxes.empty()) return issue_step(c, dt, step);
   const int p = c->cur, q = rebuild ? 1 : 0;
-  if (!c->gexec[p][q] || c->gdt[p][q] != dt) {
+  if (!c->gexec[p][q] || c->gdt[p][q] != c->dt_d) {
     if (c->gexec[p][q]) cudaGraphExecDestroy(c->gexec[p][q]);
     c->gexec[p][q] = nullptr;
     const int64_t l0 = c->launches;
@@ -488,7 +492,7 @@ int run_step(crm_t* c, float dt, long long step) {
     cudaError_t e = cudaGraphInstantiate(&c->gexec[p][q], graph, 0);
     cudaGraphDestroy(graph);
     if (e != cudaSuccess) return fail(c, CRM_E_CUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(e));
-    c->gdt[p][q] = dt;
+    c->gdt[p][q] = c->dt_d;
     c->gcur_after[p][q] = c->cur;
     c->gkernels[p][q] = c->launches - l0;
     c->launches = l0;
@@ -543,8 +547,11 @@ int begin_steps(crm_t* c, double dt) {
   cudaSetDevice(c->device);
   int r = commit(c);
   if (r) return r;
+  c->dt_d = dt;
+  // the device step counter of the error latch: graph replays advance it from here
+  launch(c, KID_STEP, k_latch_set_step, dim3(1), dim3(1), c->d_err, (long long)c->steps_done - 1);
   if (c->poses_dt != dt) {
-    launch(c, KID_POSES, k_body_poses, dim3(1), dim3(64), (int)c->bodies.size(), (const BodyState*)c->d_bodies,
+    launch(c, KID_POSES, k_body_poses, dim3(blocks((long long)c->bodies.size(), 64)), dim3(64), (int)c->bodies.size(), (const BodyState*)c->d_bodies,
            0.5 * dt, c->d_pose0, c->d_posem);
     c->poses_dt = dt;
   }
@@ -1141,6 +1148,7 @@ int crm_debug_structure(crm_t* c, uint32_t* cell_by_id, int64_t* sorted_ids, uin
     if (nbr_count_by_id) nbr_count_by_id[ids[s]] = cnt[s];
   }
   if (cell_start) CK(cudaMemcpy(cell_start, c->cell_start, ((size_t)c->grid.M + 1) * 4, cudaMemcpyDeviceToHost));
+  c->lists_valid = false;   // the export built lists off the Alg. 2 schedule: the next step rebuilds
   return CRM_OK;
 }
 
@@ -1167,6 +1175,7 @@ int crm_debug_neighbors(crm_t* c, int64_t* offsets, int64_t* list) {
            (const uint32_t*)c->nlist, list_shape(c), c->list32, c->tmp_id /* decoded counts (scratch) */);
   r = read_latch(c);
   if (r) return r;
+  c->lists_valid = false;   // store_all lists (markers list all neighbours): the next step rebuilds
   std::vector<uint32_t> ids(n), nl(n, 0u);
   CK(cudaMemcpy(ids.data(), c->ids[c->cur], n * 4, cudaMemcpyDeviceToHost));
   if (nv) CK(cudaMemcpy(nl.data(), c->tmp_id, nv * 4, cudaMemcpyDeviceToHost));

@@ -203,8 +203,8 @@ int post_counts(crm_t* c, uint32_t l0, uint32_t l1, uint32_t r0, uint32_t r1) {
 void issue_sort(crm_t* c, long long step, uint32_t drop_mask);
 void issue_bce(crm_t* c, int stage, float dt, long long step, int store_all);
 void issue_rates(crm_t* c, int stage, float dt, long long step);
-void issue_body_partial(crm_t* c, float dt);
-void issue_body_finish(crm_t* c, float dt);
+void issue_body_partial(crm_t* c);
+void issue_body_finish(crm_t* c);
 
 // ---------------------------------------------------------------------------------------
 // the phases of one slab step (each ends with posts; the transport flushes between phases)
@@ -214,6 +214,7 @@ int slab_phase(crm_t* c, int k, float dt, long long step) {
     case 0: {   // sort owned particles (drop last step's ghosts), count emigrants
       // Alg. 2: between rebuilds the slots, ghost sets and lists stay; only values move (phase 3)
       c->slab_rebuild = !c->lists_valid || (step % c->ps_freq) == 0;
+      launch(c, KID_STEP, k_step_begin, dim3(1), dim3(1), c->d_err, step);
       if (!c->slab_rebuild) return CRM_OK;
       issue_sort(c, step, TAG_GHOST | TAG_DROP);
       const int ps[4] = {c->x_lo, c->x_lo + 1, c->x_hi - 1, c->x_hi};
@@ -342,7 +343,7 @@ int slab_phase(crm_t* c, int k, float dt, long long step) {
     case 7:   // rates + full step; moving bodies: this slab's partial loads to every other slab
       issue_rates(c, 1, dt, step);
       if (c->n_moving_bodies) {
-        issue_body_partial(c, dt);
+        issue_body_partial(c);
         const size_t blk = (size_t)c->n_moving_bodies * 6;
         for (int p = 0; p < c->world; ++p) {
           if (p == c->rank) continue;
@@ -352,7 +353,7 @@ int slab_phase(crm_t* c, int k, float dt, long long step) {
       }
       return CRM_OK;
     case 8:   // moving bodies: loads summed over slabs in rank order (identical on every rank), update
-      if (c->n_moving_bodies) issue_body_finish(c, dt);
+      if (c->n_moving_bodies) issue_body_finish(c);
       return CRM_OK;
   }
   return CRM_OK;

@@ -214,6 +214,7 @@ __global__ void __launch_bounds__(FILTER_THREADS, CRM_FILTER_MINB)
                const uint32_t* __restrict__ tile_list, uint32_t* __restrict__ mtiles, uint32_t* __restrict__ mcount) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   FilterSmem& sm = *reinterpret_cast<FilterSmem*>(smem_raw);
+  if (latched(err)) return;
   const long long tile = tile_list ? (long long)tile_list[blockIdx.x] : tile_base + (long long)blockIdx.x;
   const TileGeom G = tile_geom(g, tile);
   tile_setup(g, G, cell_start, sm);

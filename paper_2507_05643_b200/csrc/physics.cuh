@@ -25,13 +25,19 @@ __device__ __forceinline__ void quat_advance_d(double q[4], const double w[3], d
   for (int k = 0; k < 4; ++k) q[k] = r[k] / nn;
 }
 
+// unit quaternion (w, x, y, z) -> rotation matrix (row-major, body -> world)
+__device__ __forceinline__ void quat_R_d(const double q[4], double R[9]) {
+  const double w = q[0], x = q[1], y = q[2], z = q[3];
+  R[0] = 1 - 2 * (y * y + z * z); R[1] = 2 * (x * y - w * z);     R[2] = 2 * (x * z + w * y);
+  R[3] = 2 * (x * y + w * z);     R[4] = 1 - 2 * (x * x + z * z); R[5] = 2 * (y * z - w * x);
+  R[6] = 2 * (x * z - w * y);     R[7] = 2 * (y * z + w * x);     R[8] = 1 - 2 * (x * x + y * y);
+}
+
 __device__ __forceinline__ void make_pose(const BodyState& b, double tau, Pose& out) {
   double q[4] = {b.quat[0], b.quat[1], b.quat[2], b.quat[3]};
   quat_advance_d(q, b.omega, tau);
-  const double w = q[0], x = q[1], y = q[2], z = q[3];
-  const double R[9] = {1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y),
-                       2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x),
-                       2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)};
+  double R[9];
+  quat_R_d(q, R);
   for (int k = 0; k < 9; ++k) out.R[k] = (float)R[k];
   for (int a = 0; a < 3; ++a) {
     out.pos[a] = (float)(b.pos[a] + tau * b.vel[a]);
@@ -136,9 +142,10 @@ __global__ void __launch_bounds__(BODY_BS) k_body_partial(const int* __restrict_
 
 // parts: world blocks of nbm x 6 partial sums (rank order); one thread per moving body
 __global__ void k_body_integrate(int nbm, const int* __restrict__ moving_bodies, const double* __restrict__ parts,
-                                 int world, BodyState* __restrict__ bodies, double dt, float g0, float g1, float g2) {
+                                 int world, BodyState* __restrict__ bodies, double dt, double g0, double g1, double g2,
+                                 const ErrLatch* err) {
   const int bi = blockIdx.x * blockDim.x + threadIdx.x;
-  if (bi >= nbm) return;
+  if (bi >= nbm || latched(err)) return;
   BodyState& B = bodies[moving_bodies[bi]];
   double F[3], T[3];
   for (int c = 0; c < 3; ++c) { F[c] = parts[bi * 6 + c]; T[c] = parts[bi * 6 + 3 + c]; }
@@ -150,10 +157,23 @@ __global__ void k_body_integrate(int nbm, const int* __restrict__ moving_bodies,
   const double g[3] = {g0, g1, g2};
   for (int c = 0; c < 3; ++c) { B.force[c] = F[c]; B.torque[c] = T[c]; }
   if (B.motion == 1) {   // FREE
+    // rotation by Euler's equations in the principal (body) frame at t_n:
+    // I alpha_b = T_b - omega_b x (I omega_b), T_b = R^T T, omega_b = R^T omega, alpha = R alpha_b;
+    // the DOF mask locks world axes
+    double R[9];
+    quat_R_d(B.quat, R);
+    double wb[3], Tb[3], ab[3];
+    for (int a = 0; a < 3; ++a) {
+      wb[a] = R[a] * B.omega[0] + R[3 + a] * B.omega[1] + R[6 + a] * B.omega[2];
+      Tb[a] = R[a] * T[0] + R[3 + a] * T[1] + R[6 + a] * T[2];
+    }
+    const double Iw[3] = {B.inertia[0] * wb[0], B.inertia[1] * wb[1], B.inertia[2] * wb[2]};
+    const double gy[3] = {wb[1] * Iw[2] - wb[2] * Iw[1], wb[2] * Iw[0] - wb[0] * Iw[2], wb[0] * Iw[1] - wb[1] * Iw[0]};
+    for (int a = 0; a < 3; ++a) ab[a] = B.inertia[a] > 0 ? (Tb[a] - gy[a]) / B.inertia[a] : 0.0;
     for (int c = 0; c < 3; ++c) {
       const int tfree = (B.dof_mask >> c) & 1, rfree = (B.dof_mask >> (3 + c)) & 1;
       B.acc[c] = tfree ? F[c] / B.mass + g[c] : 0.0;
-      B.alpha[c] = (rfree && B.inertia[c] > 0) ? T[c] / B.inertia[c] : 0.0;
+      B.alpha[c] = rfree ? R[3 * c] * ab[0] + R[3 * c + 1] * ab[1] + R[3 * c + 2] * ab[2] : 0.0;
       B.vel[c] += dt * B.acc[c];
       B.omega[c] += dt * B.alpha[c];
       B.pos[c] += dt * B.vel[c];

@@ -139,6 +139,7 @@ __global__ void TILE_BOUNDS
             const uint32_t* __restrict__ mcount) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
+  if (latched(err)) return;
   const uint32_t ntile = *mcount;
   for (uint32_t k = blockIdx.x; k < ntile; k += gridDim.x) {
     __syncthreads();   // the previous tile's window is no longer read
@@ -390,6 +391,7 @@ __global__ void TILE_BOUNDS
               const uint32_t* __restrict__ tile_list) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
+  if (latched(err)) return;
   const TileGeom G = tile_geom(g, tile_list ? (long long)tile_list[blockIdx.x] : tile_base + (long long)blockIdx.x);
   tile_setup(g, G, cell_start, sm);
   const uint32_t n_i = sm.col_pref[NCOL];

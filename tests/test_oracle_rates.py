@@ -186,3 +186,53 @@ def test_stress_rate_hydrostatic_rotation_shear_compression(oracle_mod):
     Lc = -a * np.eye(3)                                      # uniform compression tr eps = -3a
     out = oracle_mod.stress_rate(Lc, np.zeros(6), K, G)
     assert np.allclose(out, [-3 * a * K] * 3 + [0] * 3)
+
+
+# ---- artificial viscosity magnitude, worked two-particle example (Eq. 13; A9, A10) ----
+def _av_pair(oracle_mod, *, rho_i, rho_j, vi, cs, xi2, gamma, h_over_d0=1.3, visc=0, r_over_h=1.5):
+    d0 = 0.01
+    h = h_over_d0 * d0
+    pos = np.array([[0.05 + r_over_h * h, 0.05, 0.05], [0.05, 0.05, 0.05]])   # x_ij = +r e_x
+    vel = np.array([[vi, 0.0, 0.0], [0.0, 0.0, 0.0]])
+    lo, hi = pos.min(0) - 4 * d0, pos.max(0) + 4 * d0
+    p = workloads.base_params(rho0=1500.0, mu_s=0.5, mu_2=0.5, I0=0.08, cohesion=0.0, grain_d=1e-3, d0=d0,
+                              h=h, visc_mode=visc, gamma_a=gamma, lo=lo, hi=hi, gravity=(0.0, 0.0, 0.0))
+    p["cs"] = cs
+    p["xi2"] = xi2
+    s = oracle_mod.OracleSim(p)
+    s.add_fluid(pos, vel, None)
+    s.set_state(0, rho=np.array([rho_i, rho_j]))
+    _, acc, _ = stage_a_rates(s)
+    return acc[0], p
+
+
+def test_artificial_viscosity_magnitude_two_particles(oracle_mod):
+    """Pi_i = gamma_a h c_s (m_j / rho_bar_ij) (v_ij . r_ij)/(r_ij^2 + xi^2) grad_i W_ij (Eq. 13 with the
+    sign of reading A9, rho_bar = (rho_i + rho_j)/2 and xi^2, c_s as given, A10), written out for a pair
+    on the x axis at r = 1.5 h, where the cubic spline's derivative is W'(r) = -(3/4)(2 - q)^2/(pi h^4)
+    = -0.1875/(pi h^4) (A1): grad_i W_ij = W'(r) e_x.  sigma = 0 and g = 0, so a_i = Pi_i exactly.
+    Several (rho_i, rho_j, c_s, xi^2, gamma, v) so that m_j/rho_j, m_j/rho_i, a dropped h or c_s, xi in
+    place of xi^2 or a transposed v_ij . r_ij would each change the value."""
+    d0 = 0.01
+    cases = [dict(rho_i=1500.0, rho_j=1500.0, vi=-0.8, cs=20.0, xi2=1e-6, gamma=0.5),
+             dict(rho_i=1400.0, rho_j=1700.0, vi=-0.8, cs=20.0, xi2=1e-6, gamma=0.5),
+             dict(rho_i=1700.0, rho_j=1300.0, vi=0.3, cs=35.0, xi2=4e-5, gamma=0.2),
+             dict(rho_i=1450.0, rho_j=1600.0, vi=1.7, cs=11.0, xi2=2.5e-5, gamma=1.3, h_over_d0=1.2)]
+    for c in cases:
+        a, p = _av_pair(oracle_mod, **c)
+        h = p["h"]
+        r = 1.5 * h
+        m = p["rho0"] * d0 ** 3                       # m = rho0 d0^3 (S:27)
+        rho_bar = 0.5 * (c["rho_i"] + c["rho_j"])
+        vr = c["vi"] * r                              # (u_i - u_j) . (x_i - x_j)
+        dW = -0.1875 / (math.pi * h ** 4)
+        expect = c["gamma"] * h * c["cs"] * (m / rho_bar) * vr / (r * r + c["xi2"]) * dW
+        assert a[0] == pytest.approx(expect, rel=1e-12), c
+        assert a[1] == 0.0 and a[2] == 0.0
+    # unilateral (Eq. 14): the separating pair (v_ij . r_ij > 0) gets nothing, the approaching one
+    # the bilateral value
+    a_sep, _ = _av_pair(oracle_mod, rho_i=1500.0, rho_j=1600.0, vi=0.5, cs=20.0, xi2=1e-6, gamma=0.5, visc=1)
+    assert np.all(a_sep == 0.0)
+    a_app_u, _ = _av_pair(oracle_mod, rho_i=1500.0, rho_j=1600.0, vi=-0.5, cs=20.0, xi2=1e-6, gamma=0.5, visc=1)
+    a_app_b, _ = _av_pair(oracle_mod, rho_i=1500.0, rho_j=1600.0, vi=-0.5, cs=20.0, xi2=1e-6, gamma=0.5, visc=0)
+    assert a_app_u[0] == a_app_b[0] and a_app_u[0] > 0.0      # approaching: pushed apart (+x)

@@ -433,3 +433,67 @@ def test_work_counters_match_the_structure(crm):
     cand = s27[so["cell"]] - 1
     f, m = g.candidate_count()
     assert f == int(cand[:nf].sum()) and m == int(cand[nf:].sum())
+
+
+# ---------------------------------------------------------------- return map, every branch
+def _branches(sig_n, dsig_B, sig_new, dt, p):
+    """Branch of each particle from the step's own numbers (output-based, no return-map arithmetic):
+    0 cut-off (sigma_{n+1} = 0), 1 admissible (sigma_{n+1} = sigma*), 2 radial return with mu = mu_s,
+    3 radial return with mu(I) > mu_s; and whether the particle is clear of every branch boundary
+    (p* not within 1 Pa of p_cri; admissible only below (mu_s p* + c)(1 - 1e-3), where no mu(I) can
+    make it yield; radial with tau_bar scaled by < 1 - 1e-3; mu_eff = mu_s to 1e-4 or above it by > 1 %)."""
+    s_star = sig_n + dt * dsig_B
+    p_star = -s_star[:, :3].mean(1)
+    tau = s_star.copy(); tau[:, :3] += p_star[:, None]
+    tb_star = np.sqrt(0.5 * (tau[:, :3] ** 2).sum(1) + (tau[:, 3:] ** 2).sum(1))
+    tn = sig_new.copy(); pn = -sig_new[:, :3].mean(1); tn[:, :3] += pn[:, None]
+    tb_new = np.sqrt(0.5 * (tn[:, :3] ** 2).sum(1) + (tn[:, 3:] ** 2).sum(1))
+    scale = tb_new / np.maximum(tb_star, 1e-30)
+    cut = np.all(sig_new == 0.0, axis=1)
+    c, mu_s = p["cohesion"], p["mu_s"]
+    mu_rel = (tb_new - c) / np.maximum(p_star, 1e-30) / mu_s - 1.0
+    adm = ~cut & (np.abs(scale - 1.0) < 1e-5)
+    br = np.where(cut, 0, np.where(adm, 1, np.where(mu_rel > 1e-2, 3, 2)))
+    p_cri = -c / mu_s
+    clear = np.abs(p_star - p_cri) > 1.0
+    clear &= np.where(br == 1, tb_star < (mu_s * p_star + c) * (1 - 1e-3), True)
+    clear &= np.where(br >= 2, (scale < 1 - 1e-3) & ((np.abs(mu_rel) < 1e-4) | (mu_rel > 1e-2)), True)
+    return br, clear
+
+
+def test_return_map_every_branch_elementwise(crm):
+    """One step from a state that puts >= 100 particles in each branch of the return map (tension
+    cut-off, admissible, radial return at mu_s, radial return with mu(I) > mu_s): the branch of every
+    particle away from a branch boundary is the same on both sides, and sigma_{n+1} agrees element by
+    element within 1e-4 of max |sigma|."""
+    sc = workloads.return_map_state()
+    g, o = both(crm, sc)
+    g.debug_arm(True)
+    g.step(sc.dt, 1)
+    o.step(sc.dt, 1)
+    nf = sc.n_fluid
+    sig_n = sc.fluid_sig
+    sg = g.get_state()[3][:nf]
+    so = o.get_state()[3][:nf]
+    bg, cg = _branches(sig_n, g.last_rates(1)[2][:nf], sg, sc.dt, sc.params)
+    bo, co = _branches(sig_n, o.last_rates(1)[2][:nf], so, sc.dt, sc.params)
+    clear = cg & co
+    counts = np.bincount(bo[clear], minlength=4)
+    assert np.all(counts >= 100), counts
+    assert np.array_equal(bg[clear], bo[clear])
+    assert np.abs(sg[clear] - so[clear]).max() <= 1e-4 * np.abs(so).max()
+
+
+def test_structure_random_clouds_50(crm):
+    """bit-exact structure on 50 random clouds (N <= 5000, random h)."""
+    rng = np.random.default_rng(78)
+    for k in range(50):
+        n = int(rng.integers(1, 5000))
+        h = float(rng.uniform(0.01, 0.08))
+        x = workloads.random_cloud(n, seed=1000 + k)
+        p = workloads.base_params(rho0=1000.0, mu_s=0.5, mu_2=0.5, I0=0.08, cohesion=0.0, grain_d=1e-3,
+                                  d0=h / 1.3, h=h, visc_mode=0, gamma_a=0.0, lo=(-0.05,) * 3, hi=(1.05,) * 3)
+        sc = workloads.Scenario("cloud", p, x, None, None, np.zeros((0, 3)), [], 1e-5, 1)
+        g, o = both(crm, sc, max_neighbors=1024)
+        assert_structure_equal(g, o)
+        g.close()

@@ -345,7 +345,7 @@ def cylinder_markers(R: float, width: float, d0: float, layers: int) -> np.ndarr
 
 
 def mgru3_wheel(d0=1e-2, n=(500, 80, 25), R=0.2, width=0.2, vx=0.2, slip=0.3, sinkage=0.02,
-                active=True, dt=2.5e-4, free=False, omega=0.8, load=15.0) -> Scenario:
+                active=True, dt=2.5e-4, free=False, omega=0.8, load=15.0, x0=0.8) -> Scenario:
     """NEXT #2/#3 workload: the C4 MGRU3 soil bin with a rolling wheel (rim markers) and the paper's
     MGRU3 active box 0.6 x 0.6 x 0.8 m around it (P:950, P:960 'Active Box: 0.6 x 0.6 x 0.8 m',
     Alg. 3); fluid inside the wheel removed; lithostatic (settled) initial stress.
@@ -356,7 +356,7 @@ def mgru3_wheel(d0=1e-2, n=(500, 80, 25), R=0.2, width=0.2, vx=0.2, slip=0.3, si
     starting at rest on the surface; the slip follows from the steady forward speed."""
     sc = mgru3_bin(d0=d0, n=n, dt=dt)
     nx, ny, nz = n
-    c = np.array([0.8, 0.5 * ny * d0, nz * d0 + R - (0.0 if free else sinkage)])
+    c = np.array([x0, 0.5 * ny * d0, nz * d0 + R - (0.0 if free else sinkage)])
     rim = cylinder_markers(R, width, d0, bce_layers(sc.params["h"], d0))
     rel = sc.fluid_pos - c
     inside = (rel[:, 0] ** 2 + rel[:, 2] ** 2 < (R + 0.5 * d0) ** 2) & (np.abs(rel[:, 1]) < 0.5 * width + d0)
@@ -387,3 +387,29 @@ def random_cloud(n: int, seed: int, box: float = 1.0) -> np.ndarray:
     """Uniform random cloud in [0, box)^3, fp32-representable."""
     rng = np.random.default_rng(seed)
     return f32(rng.uniform(0.0, box, (n, 3)))
+
+
+def return_map_state(n=(14, 14, 14), seed=11, cohesion=500.0, mu_s=0.3, mu_2=0.6, A_scale=20.0) -> Scenario:
+    """A state whose one-step trial stresses populate every branch of the return map:
+    the C1 block in its walled box with cohesion c (so p_cri = -c/mu_s < 0) and mu_2 > mu_s; per
+    particle a pressure p ~ U(-2500, 3000) Pa and a deviator of random direction with
+    tau_bar ~ U(0, 2000) Pa (sigma = -p I + tau); velocities u = A (x - xbar), A ~ N(0, A_scale s^-1),
+    so that some particles load (gamma_dot > 0, mu(I) > mu_s) and some unload.  Seeded; generators
+    only (the branch logic lives in the oracle and the kernels)."""
+    sc = block_settle(n=n)
+    p = dict(sc.params, cohesion=cohesion, mu_s=mu_s, mu_2=mu_2)
+    pos = sc.fluid_pos
+    rng = np.random.default_rng(seed)
+    N = pos.shape[0]
+    pres = rng.uniform(-2500.0, 3000.0, N)
+    D = rng.normal(0.0, 1.0, (N, 3, 3))
+    D = 0.5 * (D + np.transpose(D, (0, 2, 1)))
+    D -= np.trace(D, axis1=1, axis2=2)[:, None, None] * np.eye(3) / 3.0
+    D /= np.sqrt(0.5 * np.einsum("kij,kij->k", D, D))[:, None, None]   # unit tau_bar
+    tb = rng.uniform(0.0, 2000.0, N)
+    S = -pres[:, None, None] * np.eye(3) + tb[:, None, None] * D
+    sig = np.stack([S[:, 0, 0], S[:, 1, 1], S[:, 2, 2], S[:, 0, 1], S[:, 0, 2], S[:, 1, 2]], -1)
+    A = rng.normal(0.0, A_scale, (3, 3))
+    vel = (pos - pos.mean(0)) @ A.T
+    return Scenario("return_map_state", p, pos, f32(vel), f32(sig), sc.wall_pos, [], sc.dt, 1,
+                    meta=dict(sc.meta, A=A))
