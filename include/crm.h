@@ -89,7 +89,7 @@ typedef struct {
                              rebuild (same neighbour sets; A34; env CRM_LIST_ORDER=rr|scan
                              overrides the choice at crm_create) */
   double gravity[3];      /* body force per unit mass f_b */
-  int    max_neighbors;   /* neighbour-list capacity per particle; 0 -> derived from h/d0 */
+  int    max_neighbors;   /* neighbour-list capacity per particle, a multiple of 8, <= 4096; 0 -> derived from h/d0 */
 } crm_kernel_t;
 
 /* Boundary handling and the fixed grid box. */

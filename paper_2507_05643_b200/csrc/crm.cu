@@ -609,7 +609,7 @@ int crm_create(const crm_material_t* mat, const crm_kernel_t* ker, const crm_bou
   if (k.visc_mode != CRM_VISC_BILATERAL && k.visc_mode != CRM_VISC_UNILATERAL) return CRM_E_INVALID;
   if (dist && (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world)) return CRM_E_INVALID;
   if (dist && dist->world > 1 && bnd->slab_axis != 0) return CRM_E_UNSUPPORTED;
-  if (k.max_neighbors > 0 && (k.max_neighbors % 8) != 0) return CRM_E_INVALID;
+  if (k.max_neighbors > 0 && ((k.max_neighbors % 8) != 0 || k.max_neighbors > 4096)) return CRM_E_INVALID;
   for (int a = 0; a < 3; ++a)
     if (!(bnd->hi[a] > bnd->lo[a])) return CRM_E_INVALID;
   crm_t* c = new crm();

@@ -22,12 +22,23 @@ namespace crmk {
 // four candidates' x (or y, z) and the B2 predicate of two candidates runs on the packed f32x2
 // FP32 instructions of sm_100 (FADD2/FMUL2/FFMA2: per element the same IEEE round-to-nearest
 // results as the scalar instructions, half the issue slots; this kernel is issue-bound).
+#ifndef CRM_FILTER_THREADS
+#define CRM_FILTER_THREADS 128
+#define CRM_FILTER_MINB 5
+#endif
+constexpr int FILTER_THREADS = CRM_FILTER_THREADS;
+constexpr int FMW = 24;   // stored 32-candidate hit masks per particle (more: drained early)
+
 struct FilterSmem : TileHead {
   int mzmin, mzmax;                 // cells z of the tile's markers (min, max)
   alignas(16) float X[WMAX + 40];   // absolute positions (a chunk may read up to 39 slots past a segment)
   float Y[WMAX + 40];
   float Z[WMAX + 40];
   alignas(4) uint8_t bce[WMAX + 40];    // 1 = BCE marker
+  // each thread's hit masks (word-major: thread t's word w at [w][t], bank = t) and the window
+  // offset of each mask's bit 0; drained into the list once the particle's sweep is complete
+  uint32_t mw[FMW][FILTER_THREADS];
+  uint16_t wb[FMW][FILTER_THREADS];
 };
 
 // positions + flags of the window (LDGSTS for the positions)
@@ -85,17 +96,37 @@ __device__ __forceinline__ uint32_t b2_group8(const FilterSmem& sm, uint32_t j, 
   return (a >> 28) | (b >> 24);
 }
 
+// drain the stored masks of this thread (words 0 .. nw-1) into the list, in candidate order; all
+// threads of a warp run it once, at the end of their sweeps, so they append in lockstep (the
+// k % 4 store points of ListWriter coincide)
+template <bool STAGED>
+__device__ __forceinline__ void drain_masks(const FilterSmem& sm, int nw, uint32_t nent, ListWriter& w) {
+  const uint32_t t = threadIdx.x;
+  int wi = 0;
+  uint32_t M = nw > 0 ? sm.mw[0][t] : 0u, base = nw > 0 ? sm.wb[0][t] : 0u;
+  for (uint32_t e = 0; e < nent; ++e) {
+    while (M == 0u) {   // (a thread advances every ~4 entries)
+      ++wi;
+      M = sm.mw[wi][t];
+      base = sm.wb[wi][t];
+    }
+    const uint32_t off = base + (__ffs(M) - 1);
+    M &= M - 1;
+    w.push(STAGED ? off << 4 : off);   // list entry: byte offset of the staged slot (global mode: the offset)
+  }
+}
+
 // Alg. 1 over one contiguous candidate range [ob, oe) of window offsets, skipping offset `self`
 // (j != i, A18; ~0u for runs without i): chunks of 32 candidates, a branch-free predicate sweep
-// builds a bitmask (and, for marker lists, a mask of the fluid candidates); the set bits are
-// appended in ascending order.
-// (measured: masking i's bit beats splitting its run in two ranges, 15.06 -> 14.80 ms; 64-candidate
-//  chunks with 64-bit masks, 17.1 ms: the fewer, longer append loops cost more in 64-bit bit
-//  arithmetic than they save in divergence)
+// builds a bitmask (and, for marker lists, a mask of the fluid candidates); the masks are stored
+// (drain_masks appends their set bits later; a thread whose FMW slots are full drains early).
+// (measured round 1: masking i's bit beats splitting its run in two ranges; 64-candidate chunks with
+//  64-bit masks cost more in 64-bit bit arithmetic than they save)
 template <bool STAGED, bool STORE_BCE>
-__device__ __forceinline__ void filter_range(float R2, const FilterSmem& sm, const float4* __restrict__ P,
+__device__ __forceinline__ void filter_range(float R2, FilterSmem& sm, const float4* __restrict__ P,
                                              const float4* __restrict__ U, uint32_t ob, uint32_t oe, uint32_t self,
-                                             uint32_t gshift, const float4& pi, uint32_t& cnt, ListWriter& w) {
+                                             uint32_t gshift, const float4& pi, uint32_t& cnt, int& nw,
+                                             uint32_t& nent, ListWriter& w) {
   const unsigned long long xi2 = f2_splat(pi.x), yi2 = f2_splat(pi.y), zi2 = f2_splat(pi.z);
   // staged: chunks start on an aligned slot (vector loads); the slots before ob are masked off
   const unsigned long long R2x2 = f2_splat(R2);
@@ -131,21 +162,28 @@ __device__ __forceinline__ void filter_range(float R2, const FilterSmem& sm, con
     if (self - base < nc) valid &= ~(1u << (self - base));
     m &= valid;
     cnt += __popc(m);
-    uint32_t s = STORE_BCE ? m : (mf & valid);
-    while (s) {   // (measured: branch-free funnel-shift appends beat paired/branchy appends, and
-                  //  ffs beats clz over a bit-reversed mask)
-      const uint32_t off = base + (__ffs(s) - 1);
-      w.push(STAGED ? off << 4 : off);   // list entry: byte offset of the staged slot (global mode: the offset)
-      s &= s - 1;
+    const uint32_t s = STORE_BCE ? m : (mf & valid);
+    if (s) {
+      if (nw == FMW) {   // this thread's mask slots are full: append what they hold now
+        drain_masks<STAGED>(sm, nw, nent, w);
+        nw = 0;
+        nent = 0;
+      }
+      sm.mw[nw][threadIdx.x] = s;
+      sm.wb[nw][threadIdx.x] = (uint16_t)base;
+      ++nw;
+      nent += __popc(s);
     }
   }
 }
 
 // the 9 candidate runs of particle i (window offset self, column q, cell z = cz); returns |P(i)|
 template <bool STAGED, bool STORE_BCE>
-__device__ __forceinline__ uint32_t filter_particle(float R2, const FilterSmem& sm, const float4* __restrict__ P,
+__device__ __forceinline__ uint32_t filter_particle(float R2, FilterSmem& sm, const float4* __restrict__ P,
                                                     const float4* __restrict__ U, int q, int cz, uint32_t self,
                                                     float4 pi, ListWriter& w) {
+  int nw = 0;
+  uint32_t nent = 0;
   // (measured: pruning neighbour cells by their box distance removes ~24 % of the candidates
   //  but costs more in divergence than it saves; the full 27-cell stencil is kept)
   uint32_t cnt = 0;
@@ -158,14 +196,16 @@ __device__ __forceinline__ uint32_t filter_particle(float R2, const FilterSmem& 
       cand_range(sm, q, da, db, cz, ob, oe, r);
       const uint32_t gshift = sm.run_start[r] - sm.run_base[r];
       // the own run holds i itself: its bit is masked off (j != i, A18)
-      filter_range<STAGED, STORE_BCE>(R2, sm, P, U, ob, oe, (da == 0 && db == 0) ? self : ~0u, gshift, pi, cnt, w);
+      filter_range<STAGED, STORE_BCE>(R2, sm, P, U, ob, oe, (da == 0 && db == 0) ? self : ~0u, gshift, pi, cnt, nw,
+                                      nent, w);
     }
   }
+  drain_masks<STAGED>(sm, nw, nent, w);
   return cnt;
 }
 
 template <bool STAGED>
-__device__ __forceinline__ int filter_tile(const Grid& g, const FilterSmem& sm, const float4* __restrict__ P,
+__device__ __forceinline__ int filter_tile(const Grid& g, FilterSmem& sm, const float4* __restrict__ P,
                                             const float4* __restrict__ U, uint16_t* __restrict__ list,
                                             uint32_t* __restrict__ nlist, uint32_t* __restrict__ count_all,
                                             const uint32_t* __restrict__ cell_of, ListShape ls, int store_all,
@@ -198,14 +238,7 @@ __device__ __forceinline__ int filter_tile(const Grid& g, const FilterSmem& sm, 
   return has_marker;
 }
 
-// 128 threads x 8 CTAs per SM (64 registers; shared memory allows 8 windows): measured 14.05 ms
-// against 14.82 for 160 x 6, 14.27 for 160 x 7 (56 registers), 14.12 for 160 x 8 (48 registers,
-// spills), 15.38 for 96 x 8
-#ifndef CRM_FILTER_THREADS
-#define CRM_FILTER_THREADS 128
-#define CRM_FILTER_MINB 8
-#endif
-constexpr int FILTER_THREADS = CRM_FILTER_THREADS;
+// 128 threads x 5 CTAs per SM (shared memory: the window's positions + the threads' mask slots)
 __global__ void __launch_bounds__(FILTER_THREADS, CRM_FILTER_MINB)
     k_filter_t(Grid g, const uint32_t* __restrict__ cell_start, const float4* __restrict__ P,
                const float4* __restrict__ U, uint16_t* __restrict__ list, uint32_t* __restrict__ nlist,
