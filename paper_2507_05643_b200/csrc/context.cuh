@@ -17,7 +17,6 @@
 #include "tiled.cuh"
 #include "filter.cuh"
 #include "active.cuh"
-#include "listorder.cuh"
 
 using namespace crmk;
 
@@ -26,13 +25,13 @@ namespace {
 enum KernelId {
   KID_MARKERS = 0, KID_BIN, KID_SCAN, KID_SCAN_ADD, KID_SCATTER, KID_REORDER,
   KID_BCE_A, KID_RATES_A, KID_BCE_B, KID_RATES_B, KID_BODY, KID_POSES, KID_STATE, KID_COPY, KID_DECODE,
-  KID_SLAB, KID_ACTIVITY, KID_FILTER, KID_LISTORDER, KID_STEP, KID_COUNT
+  KID_SLAB, KID_ACTIVITY, KID_FILTER, KID_STEP, KID_COUNT
 };
 const char* kKernelNames[KID_COUNT] = {"k_markers_place", "k_bin", "k_scan_tiles", "k_scan_add", "k_scatter",
                                        "k_reorder", "k_bce_A", "k_rates_A", "k_bce_B", "k_rates_B",
                                        "k_body_update", "k_body_poses", "k_get_set_state", "k_copy_u32",
                                        "k_decode_lists", "k_slab_util", "k_activity", "k_filter",
-                                       "k_list_rr", "k_step_begin"};
+                                       "k_step_begin"};
 
 struct ProfRec {
   int kid;
@@ -116,7 +115,7 @@ struct crm {
   int64_t gkernels[2][2] = {{0, 0}, {0, 0}};
   int ps_freq = 1;                      // Alg. 2: lists rebuilt when step % ps_freq == 0
   bool lists_valid = false;             // the stored lists/sort match the current slots
-  bool list_rr = false;                 // bank-group round-robin list order (listorder.cuh) at rebuilds
+  int list_order = 1;                   // stored list order: 1 bank-group-major (filter.cuh), 0 candidate order
   bool slab_rebuild = true;             // this slab step rebuilds (migration, ghosts, sort, lists)
 
   // multi-GPU slab decomposition along x

@@ -2,7 +2,7 @@
 //
 // One crm_step(dt, n) issues, per step, on the context's stream:
 //   memset counts | k_bin | scan (k_scan_tiles, k_scan_add) | k_scatter | k_reorder |
-//   k_filter_t (Alg. 1 lists, rebuild steps) [| k_list_rr (ps_freq > 1)] | k_bce_t<0> (extrapolation) | k_rates_t<0> (rates + half step) |
+//   k_filter_t (Alg. 1 lists, rebuild steps) | k_bce_t<0> (extrapolation) | k_rates_t<0> (rates + half step) |
 //   [k_markers_place(mid)] | k_bce_t<1> | k_rates_t<1> (rates + full step + return map) |
 //   [k_body_update | k_body_poses | k_markers_place]
 // and synchronises once at the end to read the device error latch.  With world > 1 the same
@@ -43,7 +43,6 @@ void set_attrs(crm_t* c) {
   const int sm = (int)sizeof(TileSmem);
   cudaFuncSetAttribute(k_filter_t, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FilterSmem));
   // the attribute belongs to the function, not the context: the largest rr buffer (cap <= 255)
-  cudaFuncSetAttribute(k_list_rr, cudaFuncAttributeMaxDynamicSharedMemorySize, 256 * RR_THREADS * 2);
   cudaFuncSetAttribute(k_bce_t<0, KER_CUBIC>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
   cudaFuncSetAttribute(k_bce_t<1, KER_CUBIC>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
   cudaFuncSetAttribute(k_rates_t<0, KER_CUBIC>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
@@ -366,23 +365,14 @@ void issue_filter(crm_t* c, long long step, int store_all) {
   launch_smem(c, KID_FILTER, k_filter_t, dim3((unsigned)tile_grid(c)), dim3(FILTER_THREADS), sizeof(FilterSmem),
               c->grid, (const uint32_t*)c->cell_start, (const float4*)c->P[y], (const float4*)c->U[y], c->list,
               c->nlist, c->count_all, (const uint32_t*)c->cell_of, list_shape(c), store_all, c->d_err,
-              (const uint32_t*)c->ids[y], step, c->tile_base, tile_list(c), c->d_mtiles, c->d_mtile_cnt);
-}
-
-// the lists in bank-group round-robin order (listorder.cuh): a permutation of every stored row
-void issue_list_rr(crm_t* c) {
-  const long long rows = c->boxes.empty() ? (long long)c->n : (long long)c->n_ae;
-  if (rows == 0) return;
-  launch_smem(c, KID_LISTORDER, k_list_rr, dim3(blocks(rows, RR_THREADS)), dim3(RR_THREADS),
-              (size_t)c->cap * RR_THREADS * 2, (int)rows, c->grid, (const uint32_t*)c->cell_of,
-              (const uint32_t*)c->cell_start, c->list, (const uint32_t*)c->nlist, list_shape(c));
+              (const uint32_t*)c->ids[y], step, c->tile_base, tile_list(c), c->d_mtiles, c->d_mtile_cnt,
+              c->list_order);
 }
 
 void issue_bce(crm_t* c, int stage, float dt, long long step, int store_all) {
   (void)dt;
   if (stage == 0 && c->ph.build_lists) {
     issue_filter(c, step, store_all);
-    if (c->list_rr && !store_all) issue_list_rr(c);
   }
   if (!c->n_bce) return;
   if (c->ker.kernel == CRM_KERNEL_WENDLAND) issue_bce_k<KER_WENDLAND>(c, stage, step);
@@ -677,12 +667,11 @@ int crm_create(const crm_material_t* mat, const crm_kernel_t* ker, const crm_bou
     const double ball = 4.0 / 3.0 * M_PI * std::pow(R / k.d0, 3.0);
     c->cap = std::max(32, (int)(32 * std::ceil(2.0 * ball / 32.0)));
   }
-  // bank-group round-robin list order: pays where lists are reused (Alg. 2, ps_freq > 1);
-  // CRM_LIST_ORDER=rr|scan overrides (measurement); byte counters need cap <= 255
+  // stored list order (reading A34): bank-group-major by default; CRM_LIST_ORDER=scan keeps
+  // the candidate order (measurement and the order-permutation test)
   {
     const char* lo = std::getenv("CRM_LIST_ORDER");
-    c->list_rr = lo ? std::strcmp(lo, "rr") == 0 : c->ps_freq > 1;
-    if (c->cap > 255) c->list_rr = false;
+    c->list_order = (lo && std::strcmp(lo, "scan") == 0) ? 0 : 1;
   }
   // distribution
   if (dist && dist->world > 1) {
@@ -1242,4 +1231,13 @@ int crm_debug_bce(crm_t* c, int stage, double* vel, double* sig6) {
   return CRM_OK;
 }
 
+#ifdef CRM_EXP_TIMING
+int crm_exp_timing(unsigned long long* out, int n) {
+  return cudaMemcpyFromSymbol(out, crmk::g_exp_timing, sizeof(unsigned long long) * (size_t)n) == cudaSuccess ? 0 : -1;
+}
+int crm_exp_timing_reset() {
+  static unsigned long long z[8192 * 6];
+  return cudaMemcpyToSymbol(crmk::g_exp_timing, z, sizeof(z)) == cudaSuccess ? 0 : -1;
+}
+#endif
 }  // extern "C"

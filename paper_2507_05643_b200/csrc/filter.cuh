@@ -39,6 +39,7 @@ struct FilterSmem : TileHead {
   // offset of each mask's bit 0; drained into the list once the particle's sweep is complete
   uint32_t mw[FMW][FILTER_THREADS];
   uint16_t wb[FMW][FILTER_THREADS];
+  uint2 pmask[33];   // group-major path: gm_prefix_mask(x) for x = 0..32
 };
 
 // positions + flags of the window (LDGSTS for the positions)
@@ -96,6 +97,27 @@ __device__ __forceinline__ uint32_t b2_group8(const FilterSmem& sm, uint32_t j, 
   return (a >> 28) | (b >> 24);
 }
 
+// the same predicate as b2_group8, left in sign-byte form: bit 7 of byte p of wa (wb) = candidate p
+// (4 + p) is a neighbour, every other bit 0
+__device__ __forceinline__ void b2_group8_bytes(const FilterSmem& sm, uint32_t j, unsigned long long xi2,
+                                                unsigned long long yi2, unsigned long long zi2,
+                                                unsigned long long R2x2, uint32_t& wa, uint32_t& wb) {
+  const ulonglong2 xa = *reinterpret_cast<const ulonglong2*>(&sm.X[j]);
+  const ulonglong2 ya = *reinterpret_cast<const ulonglong2*>(&sm.Y[j]);
+  const ulonglong2 za = *reinterpret_cast<const ulonglong2*>(&sm.Z[j]);
+  const ulonglong2 xb = *reinterpret_cast<const ulonglong2*>(&sm.X[j + 4]);
+  const ulonglong2 yb = *reinterpret_cast<const ulonglong2*>(&sm.Y[j + 4]);
+  const ulonglong2 zb = *reinterpret_cast<const ulonglong2*>(&sm.Z[j + 4]);
+  const unsigned long long d0 = b2_r2m(xa.x, ya.x, za.x, xi2, yi2, zi2, R2x2);
+  const unsigned long long d1 = b2_r2m(xa.y, ya.y, za.y, xi2, yi2, zi2, R2x2);
+  const unsigned long long d2 = b2_r2m(xb.x, yb.x, zb.x, xi2, yi2, zi2, R2x2);
+  const unsigned long long d3 = b2_r2m(xb.y, yb.y, zb.y, xi2, yi2, zi2, R2x2);
+  wa = __byte_perm(__byte_perm((uint32_t)d0, (uint32_t)(d0 >> 32), 0x0073),
+                   __byte_perm((uint32_t)d1, (uint32_t)(d1 >> 32), 0x0073), 0x5410) & 0x80808080u;
+  wb = __byte_perm(__byte_perm((uint32_t)d2, (uint32_t)(d2 >> 32), 0x0073),
+                   __byte_perm((uint32_t)d3, (uint32_t)(d3 >> 32), 0x0073), 0x5410) & 0x80808080u;
+}
+
 // drain the stored masks of this thread (words 0 .. nw-1) into the list, in candidate order; all
 // threads of a warp run it once, at the end of their sweeps, so they append in lockstep (the
 // k % 4 store points of ListWriter coincide)
@@ -113,6 +135,160 @@ __device__ __forceinline__ void drain_masks(const FilterSmem& sm, int nw, uint32
     const uint32_t off = base + (__ffs(M) - 1);
     M &= M - 1;
     w.push(STAGED ? off << 4 : off);   // list entry: byte offset of the staged slot (global mode: the offset)
+  }
+}
+
+// ---- bank-group-major list order (staged windows; CRM_LIST_ORDER != scan) ----------------------
+// The pair kernels gather each entry's 16-B window slots; the 8 lanes of a quarter warp read their
+// k-th entries at once, conflict-free only when the 8 slots lie in distinct bank groups (slot mod 8).
+// Lists in candidate order put the lanes' groups at random (offline model of the C5 lists: 2.38
+// shared-memory wavefronts per ideal one); a list that holds i's entries of group g0, then g0 + 1,
+// ... (mod 8), each group in candidate order, with g0 = i's tile slot mod 8 (= its lane in the
+// quarter), keeps the lanes of a quarter in distinct groups for most steps (1.62 in the model;
+// measured k_rates_A/B 13.5/13.9 -> 11.7/12.3 ms).  To emit that order without buffering the list,
+// the sweep stores its hits transposed: chunks of 32 candidates start on a multiple of 8, so the
+// candidate at chunk offset 8n + p (n < 4) is in group p; its bit goes to bit n of byte p (the
+// sign-byte form the predicate produces anyway), two chunks share a byte (nibbles), and the bytes
+// of group g are collected in g's own words (4 bytes = 8 chunks per word, GMW words).  The drain
+// then walks the 8 group strings in rotated order, one entry per iteration (lockstep appends).
+constexpr int GMW = FMW / 8;   // words per group string: 8 GMW chunks per particle before an early drain
+
+// transposed valid mask of the first x (0..32) candidates of a chunk: bit n of byte p (groups 0-3
+// in .x, 4-7 in .y) for every candidate 8n + p < x
+__device__ __forceinline__ uint2 gm_prefix_mask(uint32_t x) {
+  uint32_t a = 0, b = 0;
+#pragma unroll
+  for (int p = 0; p < 8; ++p) {
+    const uint32_t cnt = x > (uint32_t)p ? min(4u, (x - (uint32_t)p + 7u) >> 3) : 0u;   // n with 8n + p < x
+    const uint32_t nib = (1u << cnt) - 1u;
+    if (p < 4) a |= nib << (8 * p); else b |= nib << (8 * (p - 4));
+  }
+  return make_uint2(a, b);
+}
+
+struct GmState {
+  uint32_t A, B;      // the open byte position (chunks 2p, 2p+1 as low/high nibbles; groups 0-3 / 4-7)
+  int nch;            // chunks stored
+  uint32_t nent;      // entries stored
+};
+
+__device__ __forceinline__ void gm_reset(GmState& st) {
+  st.A = st.B = 0u;
+  st.nch = 0;
+  st.nent = 0;
+}
+
+// 4x4 byte transpose: out word k = byte k of r0, r1, r2, r3
+__device__ __forceinline__ void bytes4x4(uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  const uint32_t a = __byte_perm(r0, r1, 0x5140), b = __byte_perm(r0, r1, 0x7362);
+  const uint32_t c = __byte_perm(r2, r3, 0x5140), d = __byte_perm(r2, r3, 0x7362);
+  r0 = __byte_perm(a, c, 0x5410);
+  r1 = __byte_perm(a, c, 0x7632);
+  r2 = __byte_perm(b, d, 0x5410);
+  r3 = __byte_perm(b, d, 0x7632);
+}
+
+// append the particle's stored entries in group-major order and reset the state.  Stored so far:
+// per byte position p (two chunks) the words (A, B) at mw[2p], mw[2p + 1]; transposed in place, 4
+// byte positions at a time, into group words: mw[8 wd + g] = bytes 4 wd .. 4 wd + 3 of group g.
+__device__ __forceinline__ void gm_drain(FilterSmem& sm, GmState& st, uint32_t g0, ListWriter& w) {
+  const uint32_t t = threadIdx.x;
+  if (st.nch & 1) {   // a half-filled byte position
+    const int p = st.nch >> 1;
+    sm.mw[2 * p][t] = st.A;
+    sm.mw[2 * p + 1][t] = st.B;
+  }
+  const int nb = (st.nch + 1) >> 1;   // byte positions
+  uint32_t NZ = 0;                    // bit 4 g + wd: group g's word wd holds entries
+  for (int wd = 0; 4 * wd < nb; ++wd) {
+    uint32_t r[8];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const bool in = 4 * wd + k < nb;
+      r[k] = in ? sm.mw[8 * wd + 2 * k][t] : 0u;       // groups 0-3 of byte position 4 wd + k
+      r[4 + k] = in ? sm.mw[8 * wd + 2 * k + 1][t] : 0u;   // groups 4-7
+    }
+    bytes4x4(r[0], r[1], r[2], r[3]);
+    bytes4x4(r[4], r[5], r[6], r[7]);
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+      sm.mw[8 * wd + g][t] = r[g];
+      NZ |= (r[g] ? 1u : 0u) << (4 * g + wd);
+    }
+  }
+  // the non-empty words in emission order (groups g0, g0 + 1, ...): NZ rotated by 4 g0
+  uint32_t nz = __funnelshift_r(NZ, NZ, 4u * (g0 & 7u));
+  uint32_t W = 0, wd = 0, g = 0;
+  for (uint32_t e = 0; e < st.nent; ++e) {
+    if (W == 0u) {   // the next non-empty word: one ffs, no search
+      const uint32_t pos = __ffs(nz) - 1;
+      nz &= nz - 1;
+      wd = pos & 3u;
+      g = (g0 + (pos >> 2)) & 7u;
+      W = sm.mw[wd * 8 + g][t];
+    }
+    const uint32_t q = __ffs(W) - 1;   // bit q: chunk 8 wd + (q >> 2), candidate 8 (q & 3) + g of it
+    W &= W - 1;
+    w.push((sm.wb[8 * wd + (q >> 2)][t] + 8u * (q & 3u) + g) << 4);
+  }
+  gm_reset(st);
+}
+
+// store one chunk's transposed hits (a, b: groups 0-3 / 4-7, bit n of byte p) at window base
+__device__ __forceinline__ void gm_store_chunk(FilterSmem& sm, GmState& st, uint32_t a, uint32_t b, uint32_t base,
+                                               uint32_t g0, ListWriter& w) {
+  if (st.nch == FMW) gm_drain(sm, st, g0, w);   // all mask slots used: append what they hold now
+  const uint32_t t = threadIdx.x;
+  sm.wb[st.nch][t] = (uint16_t)base;
+  st.nent += __popc(a) + __popc(b);
+  if (st.nch & 1) {
+    const int p = st.nch >> 1;
+    sm.mw[2 * p][t] = st.A | (a << 4);
+    sm.mw[2 * p + 1][t] = st.B | (b << 4);
+  } else {
+    st.A = a;
+    st.B = b;
+  }
+  ++st.nch;
+}
+
+// Alg. 1 over one candidate range, staged window, group-major storage (see above)
+template <bool STORE_BCE>
+__device__ __forceinline__ void filter_range_gm(float R2, FilterSmem& sm, uint32_t ob, uint32_t oe, uint32_t self,
+                                                const float4& pi, uint32_t& cnt, GmState& st, uint32_t g0,
+                                                ListWriter& w) {
+  const unsigned long long xi2 = f2_splat(pi.x), yi2 = f2_splat(pi.y), zi2 = f2_splat(pi.z);
+  const unsigned long long R2x2 = f2_splat(R2);
+  for (uint32_t base = ob & ~7u; base < oe; base += 32) {
+    const uint32_t nc = min(32u, oe - base);
+    uint32_t a = 0, b = 0, fa = 0, fb = 0;
+    for (uint32_t k8 = 0, n = 0; k8 < nc; k8 += 8, ++n) {
+      uint32_t wa, wb;
+      b2_group8_bytes(sm, base + k8, xi2, yi2, zi2, R2x2, wa, wb);   // bit 7 of byte p: candidate p (wb: 4 + p)
+      a |= wa >> (7u - n);
+      b |= wb >> (7u - n);
+      if (!STORE_BCE) {   // fluid candidates only: the flags are bytes 0/1
+        const uint32_t f0 = *reinterpret_cast<const uint32_t*>(&sm.bce[base + k8]);
+        const uint32_t f1 = *reinterpret_cast<const uint32_t*>(&sm.bce[base + k8 + 4]);
+        fa |= (wa & ~(f0 << 7)) >> (7u - n);
+        fb |= (wb & ~(f1 << 7)) >> (7u - n);
+      }
+    }
+    // valid candidates [max(ob, base), min(oe, base + 32)) without i itself
+    const uint2 vhi = sm.pmask[nc], vlo = sm.pmask[base < ob ? ob - base : 0u];
+    uint32_t va = vhi.x & ~vlo.x, vb = vhi.y & ~vlo.y;
+    if (self - base < nc) {
+      const uint32_t o = self - base, bit = 1u << (8u * (o & 3u) + (o >> 3));
+      if (o & 4u) vb &= ~bit; else va &= ~bit;
+    }
+    a &= va;
+    b &= vb;
+    cnt += __popc(a) + __popc(b);
+    if (!STORE_BCE) {
+      a = fa & va;
+      b = fb & vb;
+    }
+    if (a | b) gm_store_chunk(sm, st, a, b, base, g0, w);
   }
 }
 
@@ -181,9 +357,11 @@ __device__ __forceinline__ void filter_range(float R2, FilterSmem& sm, const flo
 template <bool STAGED, bool STORE_BCE>
 __device__ __forceinline__ uint32_t filter_particle(float R2, FilterSmem& sm, const float4* __restrict__ P,
                                                     const float4* __restrict__ U, int q, int cz, uint32_t self,
-                                                    float4 pi, ListWriter& w) {
+                                                    float4 pi, ListWriter& w, bool gmaj, uint32_t g0) {
   int nw = 0;
   uint32_t nent = 0;
+  GmState st;
+  if (STAGED && gmaj) gm_reset(st);
   // (measured: pruning neighbour cells by their box distance removes ~24 % of the candidates
   //  but costs more in divergence than it saves; the full 27-cell stencil is kept)
   uint32_t cnt = 0;
@@ -196,11 +374,13 @@ __device__ __forceinline__ uint32_t filter_particle(float R2, FilterSmem& sm, co
       cand_range(sm, q, da, db, cz, ob, oe, r);
       const uint32_t gshift = sm.run_start[r] - sm.run_base[r];
       // the own run holds i itself: its bit is masked off (j != i, A18)
-      filter_range<STAGED, STORE_BCE>(R2, sm, P, U, ob, oe, (da == 0 && db == 0) ? self : ~0u, gshift, pi, cnt, nw,
-                                      nent, w);
+      const uint32_t sf = (da == 0 && db == 0) ? self : ~0u;
+      if (STAGED && gmaj) filter_range_gm<STORE_BCE>(R2, sm, ob, oe, sf, pi, cnt, st, g0, w);
+      else filter_range<STAGED, STORE_BCE>(R2, sm, P, U, ob, oe, sf, gshift, pi, cnt, nw, nent, w);
     }
   }
-  drain_masks<STAGED>(sm, nw, nent, w);
+  if (STAGED && gmaj) gm_drain(sm, st, g0, w);
+  else drain_masks<STAGED>(sm, nw, nent, w);
   return cnt;
 }
 
@@ -209,7 +389,8 @@ __device__ __forceinline__ int filter_tile(const Grid& g, FilterSmem& sm, const 
                                             const float4* __restrict__ U, uint16_t* __restrict__ list,
                                             uint32_t* __restrict__ nlist, uint32_t* __restrict__ count_all,
                                             const uint32_t* __restrict__ cell_of, ListShape ls, int store_all,
-                                            ErrLatch* err, const uint32_t* __restrict__ ids, long long step) {
+                                            ErrLatch* err, const uint32_t* __restrict__ ids, long long step,
+                                            bool gmaj) {
   const uint32_t n_i = sm.col_pref[NCOL];
   int has_marker = 0;
   for (uint32_t t = threadIdx.x; t < n_i; t += blockDim.x) {
@@ -228,8 +409,8 @@ __device__ __forceinline__ int filter_tile(const Grid& g, FilterSmem& sm, const 
     const bool fluid_only = !store_all && bce;
     ListWriter w;
     w.init(list, i, ls);
-    const uint32_t cnt = fluid_only ? filter_particle<STAGED, false>(g.R2, sm, P, U, q, cz, self, pi, w)
-                                    : filter_particle<STAGED, true>(g.R2, sm, P, U, q, cz, self, pi, w);
+    const uint32_t cnt = fluid_only ? filter_particle<STAGED, false>(g.R2, sm, P, U, q, cz, self, pi, w, gmaj, t & 7u)
+                                    : filter_particle<STAGED, true>(g.R2, sm, P, U, q, cz, self, pi, w, gmaj, t & 7u);
     w.flush(STAGED ? self << 4 : self);
     nlist[i] = (uint32_t)min(w.k, ls.cap);
     count_all[i] = cnt;
@@ -244,7 +425,8 @@ __global__ void __launch_bounds__(FILTER_THREADS, CRM_FILTER_MINB)
                const float4* __restrict__ U, uint16_t* __restrict__ list, uint32_t* __restrict__ nlist,
                uint32_t* __restrict__ count_all, const uint32_t* __restrict__ cell_of, ListShape ls, int store_all,
                ErrLatch* err, const uint32_t* __restrict__ ids, long long step, long long tile_base,
-               const uint32_t* __restrict__ tile_list, uint32_t* __restrict__ mtiles, uint32_t* __restrict__ mcount) {
+               const uint32_t* __restrict__ tile_list, uint32_t* __restrict__ mtiles, uint32_t* __restrict__ mcount,
+               int order) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   FilterSmem& sm = *reinterpret_cast<FilterSmem*>(smem_raw);
   if (latched(err)) return;
@@ -257,14 +439,16 @@ __global__ void __launch_bounds__(FILTER_THREADS, CRM_FILTER_MINB)
     return;
   }
   filter_stage(P, U, sm);
+  if (threadIdx.x < 33) sm.pmask[threadIdx.x] = gm_prefix_mask(threadIdx.x);
   if (threadIdx.x == 0) {
     sm.mzmin = 0x7fffffff;
     sm.mzmax = -1;
   }
   tile_stage_wait();
   __syncthreads();
-  const int has = sm.staged ? filter_tile<true>(g, sm, P, U, list, nlist, count_all, cell_of, ls, store_all, err, ids, step)
-                            : filter_tile<false>(g, sm, P, U, list, nlist, count_all, cell_of, ls, store_all, err, ids, step);
+  const bool gmaj = order == 1;
+  const int has = sm.staged ? filter_tile<true>(g, sm, P, U, list, nlist, count_all, cell_of, ls, store_all, err, ids, step, gmaj)
+                            : filter_tile<false>(g, sm, P, U, list, nlist, count_all, cell_of, ls, store_all, err, ids, step, gmaj);
   // the tiles holding markers: the BCE kernels run over these only (any order: tiles are independent)
   // with the rows z0 + zl .. z0 + zh (0 <= zl <= zh < TZ) that hold them in bits 28-31 (tiles < 2^28)
   if (__syncthreads_or(has) && threadIdx.x == 0) {

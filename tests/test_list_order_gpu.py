@@ -1,5 +1,5 @@
-"""The bank-group round-robin list order (listorder.cuh, reading A34) is a permutation of
-each stored list: the same neighbour set, summed in another fixed order.  Against the filter's
+"""The bank-group-major list order (filter.cuh drain_masks_gm, reading A34) is a permutation
+of each stored list: the same neighbour set, summed in another fixed order.  Against the filter's
 candidate order the states may differ only by fp32 rounding; against the oracle both stay within the
 parity tolerances (the ps_freq > 1 tests of test_parity_gpu.py run with it on by default)."""
 import os
@@ -36,10 +36,10 @@ def _run(crm, sc, order, steps):
 
 
 @pytest.mark.parametrize("ps_freq", [1, 4])
-def test_round_robin_order_is_a_permutation(crm, ps_freq):
+def test_group_major_order_is_a_permutation(crm, ps_freq):
     sc = workloads.block_settle(jitter=0.05, seed=3)
     sc.params["ps_freq"] = ps_freq
-    rr = _run(crm, sc, "rr", 20)
+    rr = _run(crm, sc, "gmajor", 20)
     scan = _run(crm, sc, "scan", 20)
     pos_rr, vel_rr, rho_rr, sig_rr = rr[:4]
     pos_sc, vel_sc, rho_sc, sig_sc = scan[:4]
