@@ -220,19 +220,22 @@ __device__ __forceinline__ void gm_drain(FilterSmem& sm, GmState& st, uint32_t g
   uint32_t nz = __funnelshift_r(NZ, NZ, 4u * (g0 & 7u));
   uint32_t W = 0, wd = 0, g = 0;
   for (uint32_t e = 0; e < st.nent; ++e) {
-    if (W == 0u) {   // the next non-empty word: one ffs, no search
-      const uint32_t pos = __ffs(nz) - 1;
-      nz &= nz - 1;
-      wd = pos & 3u;
-      g = (g0 + (pos >> 2)) & 7u;
-      W = sm.mw[wd * 8 + g][t];
-    }
+    // the next non-empty word when W is spent: one ffs, no search, no branch (the lanes of a warp
+    // reach the ends of their words at different entries)
+    const bool adv = W == 0u;
+    const uint32_t pos = __ffs(nz) - 1;
+    nz = adv ? (nz & (nz - 1)) : nz;
+    wd = adv ? (pos & 3u) : wd;
+    g = adv ? ((g0 + (pos >> 2)) & 7u) : g;
+    const uint32_t Wn = sm.mw[wd * 8 + g][t];
+    W = adv ? Wn : W;
     const uint32_t q = __ffs(W) - 1;   // bit q: chunk 8 wd + (q >> 2), candidate 8 (q & 3) + g of it
     W &= W - 1;
     w.push((sm.wb[8 * wd + (q >> 2)][t] + 8u * (q & 3u) + g) << 4);
   }
   gm_reset(st);
 }
+
 
 // store one chunk's transposed hits (a, b: groups 0-3 / 4-7, bit n of byte p) at window base
 __device__ __forceinline__ void gm_store_chunk(FilterSmem& sm, GmState& st, uint32_t a, uint32_t b, uint32_t base,
@@ -262,7 +265,10 @@ __device__ __forceinline__ void filter_range_gm(float R2, FilterSmem& sm, uint32
   for (uint32_t base = ob & ~7u; base < oe; base += 32) {
     const uint32_t nc = min(32u, oe - base);
     uint32_t a = 0, b = 0, fa = 0, fb = 0;
-    for (uint32_t k8 = 0, n = 0; k8 < nc; k8 += 8, ++n) {
+#pragma unroll
+    for (uint32_t n = 0; n < 4; ++n) {
+      const uint32_t k8 = 8 * n;
+      if (k8 >= nc) break;
       uint32_t wa, wb;
       b2_group8_bytes(sm, base + k8, xi2, yi2, zi2, R2x2, wa, wb);   // bit 7 of byte p: candidate p (wb: 4 + p)
       a |= wa >> (7u - n);

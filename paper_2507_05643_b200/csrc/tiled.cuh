@@ -218,61 +218,6 @@ __device__ __forceinline__ void pair_terms(PairAcc& A, const Phys& ph, const flo
   A.Pi[0] = fmaf(coef, dx, A.Pi[0]); A.Pi[1] = fmaf(coef, dy, A.Pi[1]); A.Pi[2] = fmaf(coef, dz, A.Pi[2]);
 }
 
-#ifndef CRM_PAIR_2PH
-#define CRM_PAIR_2PH 0
-#endif
-#ifndef CRM_PAIR_F2
-#define CRM_PAIR_F2 0
-#endif
-// The same pair on sm_100's packed FP32 pairs (FADD2/FMUL2/FFMA2, a scalar operand broadcast for
-// free): x/y halves of the vectors share one instruction, 57 instead of 68 instructions per pair.
-// Per element the IEEE results of the scalar instructions; only the association of a few sums
-// differs (r^2, v.r and (sigma_j g)_z are summed from pair halves), i.e. fp32 rounding.
-struct PairAccF2 {
-  unsigned long long L01, L34, L67, Gs01, Ms01, Ms2ab, Pi01;   // (element 0, element 1) pairs
-  float L2, L5, L8, Gs2, Ms2c, Pi2;
-};
-template <int KER>
-__device__ __forceinline__ void pair_terms_f2(PairAccF2& A, const Phys& ph, unsigned long long pixy, float piz,
-                                              float piw, unsigned long long uixy, float uiz, const float4& pj,
-                                              const float4& uj, const float4& sj1, const float2& sj2, bool with_L,
-                                              bool fluid_only) {
-  const unsigned long long dxy = f2_sub(pixy, f2_make(pj.x, pj.y));   // x_ij = x_i - x_j
-  const float dz = piz - pj.z;
-  const unsigned long long sq = f2_mul(dxy, dxy);
-  const float r2 = fmaf(dz, dz, f2_lo(sq)) + f2_hi(sq);
-  const float Vj = fabsf(pj.w);
-  const bool ok = r2 < ph.R2 && r2 > 0.f && (!fluid_only || pj.w > 0.f);
-  const float rinv = rsqrt_approx(r2);
-  const float F = kernel_F<KER>(r2 * rinv, rinv, ph);                 // W'(r)/r (A1 / A28)
-  const float w = ok ? Vj * F : 0.f;                                   // V_j W'/r (A7)
-  const unsigned long long gxy = f2_mul(f2_splat(w), dxy);            // V_j grad_i W_ij
-  const float gz = w * dz;
-  const unsigned long long duxy = f2_sub(f2_make(uj.x, uj.y), uixy);  // u_ji
-  const float duz = uj.z - uiz;
-  if (with_L) {   // L_ab += V_j u_ji,a gradW_b (F2, A4): rows (a, 0..1) packed, column 2 scalar
-    const float dux = f2_lo(duxy), duy = f2_hi(duxy);
-    A.L01 = f2_fma(f2_splat(dux), gxy, A.L01); A.L2 = fmaf(dux, gz, A.L2);
-    A.L34 = f2_fma(f2_splat(duy), gxy, A.L34); A.L5 = fmaf(duy, gz, A.L5);
-    A.L67 = f2_fma(f2_splat(duz), gxy, A.L67); A.L8 = fmaf(duz, gz, A.L8);
-  }
-  A.Gs01 = f2_add(A.Gs01, gxy); A.Gs2 += gz;
-  // sigma_j g with S1 = (xx, yy, zz, xy), S2 = (xz, yz):
-  //   (Ms0, Ms1) += (xx gx, yy gy) + (xz gz, yz gz) + (xy gy, xy gx);  Ms2 = xz gx + yz gy + zz gz
-  A.Ms01 = f2_fma(f2_make(sj1.x, sj1.y), gxy, A.Ms01);
-  A.Ms01 = f2_fma(f2_make(sj2.x, sj2.y), f2_splat(gz), A.Ms01);
-  A.Ms01 = f2_make(fmaf(sj1.w, f2_hi(gxy), f2_lo(A.Ms01)), fmaf(sj1.w, f2_lo(gxy), f2_hi(A.Ms01)));
-  A.Ms2ab = f2_fma(f2_make(sj2.x, sj2.y), gxy, A.Ms2ab);
-  A.Ms2c = fmaf(sj1.z, gz, A.Ms2c);
-  // artificial viscosity (as pair_terms)
-  const unsigned long long t = f2_mul(duxy, dxy);
-  const float vr = -(fmaf(duz, dz, f2_lo(t)) + f2_hi(t));
-  const float den = fmaf(piw, Vj, ph.m) * (r2 + ph.xi2);
-  const float cv = (ph.c_av * vr) * (w * rcp_approx(den));
-  const float coef = (!ph.unilateral || vr < 0.f) ? cv : 0.f;
-  A.Pi01 = f2_fma(f2_splat(coef), dxy, A.Pi01); A.Pi2 = fmaf(coef, dz, A.Pi2);
-}
-
 template <int KER, bool STAGED>
 __device__ __forceinline__ void pair_loop(PairAcc& A, const Phys& ph, const TileSmem& sm, const float4* __restrict__ P,
                                           const float4* __restrict__ L, const float4* __restrict__ U,
@@ -290,99 +235,21 @@ __device__ __forceinline__ void pair_loop(PairAcc& A, const Phys& ph, const Tile
   // three ahead ran 14.26 / 14.54 ms (register pressure)
   uint4 vn = first;
   uint4 vn2 = seg[nch > 1 ? ls_stride : 0];   // an empty list (nch = 0) has only chunk 0
-#if CRM_PAIR_F2
-  PairAccF2 B;
-  B.L01 = B.L34 = B.L67 = B.Gs01 = B.Ms01 = B.Ms2ab = B.Pi01 = 0ull;
-  B.L2 = B.L5 = B.L8 = B.Gs2 = B.Ms2c = B.Pi2 = 0.f;
-  const unsigned long long pixy = f2_make(pi.x, pi.y), uixy = f2_make(ui.x, ui.y);
-#endif
-#ifdef CRM_EXP_NOCONFLICT
-  // timing experiment only (wrong physics): synthetic conflict-free gathers, lanes of a quarter
-  // warp in distinct bank groups, same instruction shape
-  const uint32_t wlim = (sm.run_base[WR] & ~7u) * 16u;
-#ifdef CRM_EXP_BCAST
-  uint32_t soff = 0u;
-#else
-  uint32_t soff = (threadIdx.x & 7u) * 16u;
-#endif
-#endif
   for (uint32_t c = 0; c < nch; ++c) {   // whole padded chunks of 8, branch-free
     const uint4 v = vn;
     vn = vn2;
     vn2 = seg[(size_t)min(c + 2, nch - 1) * ls_stride];
-#if CRM_PAIR_2PH
-    if (STAGED) {
-#pragma unroll
-      for (int hh = 0; hh < 8; hh += CRM_PAIR_2PH) {
-        float gw[CRM_PAIR_2PH], gdx[CRM_PAIR_2PH], gdy[CRM_PAIR_2PH], gdz[CRM_PAIR_2PH], gden[CRM_PAIR_2PH];
-        uint32_t ge[CRM_PAIR_2PH];
-#pragma unroll
-        for (int k = 0; k < CRM_PAIR_2PH; ++k) {   // phase 1: geometry of the half chunk
-          ge[k] = list_entry(v, hh + k);
-          const float4 pj = win_P(sm, ge[k]);
-          const float dx = pi.x - pj.x, dy = pi.y - pj.y, dz = pi.z - pj.z;
-          const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-          const float Vj = fabsf(pj.w);
-          const bool ok = r2 < ph.R2 && r2 > 0.f && (!fluid_only || pj.w > 0.f);
-          const float rinv = rsqrt_approx(r2);
-          const float F = kernel_F<KER>(r2 * rinv, rinv, ph);
-          gw[k] = ok ? Vj * F : 0.f;
-          gdx[k] = dx; gdy[k] = dy; gdz[k] = dz;
-          gden[k] = fmaf(pi.w, Vj, ph.m) * (r2 + ph.xi2);
-        }
-#pragma unroll
-        for (int k = 0; k < CRM_PAIR_2PH; ++k) {   // phase 2: the sums
-          const float4 uj = win_U(sm, ge[k]), sj1 = win_S1(sm, ge[k]);
-          const float2 sj2 = win_S2(sm, ge[k]);
-          const float w = gw[k], dx = gdx[k], dy = gdy[k], dz = gdz[k];
-          const float gx = w * dx, gy = w * dy, gz = w * dz;
-          const float dux = uj.x - ui.x, duy = uj.y - ui.y, duz = uj.z - ui.z;
-          if (with_L) {
-            A.L[0] = fmaf(dux, gx, A.L[0]); A.L[1] = fmaf(dux, gy, A.L[1]); A.L[2] = fmaf(dux, gz, A.L[2]);
-            A.L[3] = fmaf(duy, gx, A.L[3]); A.L[4] = fmaf(duy, gy, A.L[4]); A.L[5] = fmaf(duy, gz, A.L[5]);
-            A.L[6] = fmaf(duz, gx, A.L[6]); A.L[7] = fmaf(duz, gy, A.L[7]); A.L[8] = fmaf(duz, gz, A.L[8]);
-          }
-          A.Gs[0] += gx; A.Gs[1] += gy; A.Gs[2] += gz;
-          A.Ms[0] = fmaf(sj1.x, gx, fmaf(sj1.w, gy, fmaf(sj2.x, gz, A.Ms[0])));
-          A.Ms[1] = fmaf(sj1.w, gx, fmaf(sj1.y, gy, fmaf(sj2.y, gz, A.Ms[1])));
-          A.Ms[2] = fmaf(sj2.x, gx, fmaf(sj2.y, gy, fmaf(sj1.z, gz, A.Ms[2])));
-          const float vr = -fmaf(duz, dz, fmaf(duy, dy, dux * dx));
-          const float cv = (ph.c_av * vr) * (w * rcp_approx(gden[k]));
-          const float coef = (!ph.unilateral || vr < 0.f) ? cv : 0.f;
-          A.Pi[0] = fmaf(coef, dx, A.Pi[0]); A.Pi[1] = fmaf(coef, dy, A.Pi[1]); A.Pi[2] = fmaf(coef, dz, A.Pi[2]);
-        }
-      }
-      continue;
-    }
-#endif
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       float4 pj, uj, s1;
       float2 s2;
-#ifdef CRM_EXP_NOCONFLICT
-      const uint32_t ereal = list_entry(v, e);
-      asm volatile("" ::"r"(ereal));
-      soff += 128u;
-      soff = soff >= wlim ? soff - wlim : soff;
-      load_rates<STAGED>(sm, P, L, U, S1, S2, STAGED ? soff : ereal, ph.m, pj, uj, s1, s2);
-#else
+      // (measured: the x/y halves on packed f32x2 instructions, 57 instead of 68 instructions per
+      //  pair, and a two-phase body (geometry of 4-8 entries, then their sums) ran 2 % slower and
+      //  the same: the pair loop is bound by the window gathers and the tile prologue, not issue)
       load_rates<STAGED>(sm, P, L, U, S1, S2, list_entry(v, e), ph.m, pj, uj, s1, s2);
-#endif
-#if CRM_PAIR_F2
-      pair_terms_f2<KER>(B, ph, pixy, pi.z, pi.w, uixy, ui.z, pj, uj, s1, s2, with_L, fluid_only);
-#else
       pair_terms<KER>(A, ph, pi, ui, pj, uj, s1, s2, with_L, fluid_only);
-#endif
     }
   }
-#if CRM_PAIR_F2
-  A.L[0] += f2_lo(B.L01); A.L[1] += f2_hi(B.L01); A.L[2] += B.L2;
-  A.L[3] += f2_lo(B.L34); A.L[4] += f2_hi(B.L34); A.L[5] += B.L5;
-  A.L[6] += f2_lo(B.L67); A.L[7] += f2_hi(B.L67); A.L[8] += B.L8;
-  A.Gs[0] += f2_lo(B.Gs01); A.Gs[1] += f2_hi(B.Gs01); A.Gs[2] += B.Gs2;
-  A.Ms[0] += f2_lo(B.Ms01); A.Ms[1] += f2_hi(B.Ms01); A.Ms[2] += (f2_lo(B.Ms2ab) + f2_hi(B.Ms2ab)) + B.Ms2c;
-  A.Pi[0] += f2_lo(B.Pi01); A.Pi[1] += f2_hi(B.Pi01); A.Pi[2] += B.Pi2;
-#endif
 }
 
 // STAGE 0: (P,L,U,S) = y_n; writes y_mid to (YP,YL,YU,YS).  STAGE 1: (P,L,U,S) = y_mid;

@@ -234,7 +234,7 @@ __device__ __forceinline__ float4 rel_pos(const float4& hi, const float4& lo, co
 // markers (A7, A8: markers are ordinary neighbours with V = m/rho0; the sign lets the marker-load
 // loop keep fluid neighbours only without reading the tag)
 __device__ __forceinline__ float signed_volume(float rho, float tagw, float m) {
-  const float V = m * rcp_approx(rho);   // (1 ulp of a weight; the IEEE division cost ~5 % of the tile prologue)
+  const float V = __fdiv_rn(m, rho);
   return tag_is_bce(tag_of(tagw)) ? -V : V;
 }
 
