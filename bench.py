@@ -50,6 +50,8 @@ BYTES_PER_BCE_UPDATE = 72
 # (the 56-B fp32 state of D4; the 16-B position compensation term L is this design's overhead)
 # bounded oracle sample of the bed workload (~1M fluid; ~1 s per oracle step on a 16-core host)
 SAMPLE_BED = (128, 128, 64)
+# the 1-thread oracle sample (~262k fluid, a few seconds per step on one core)
+SAMPLE_BED_1T = (64, 64, 64)
 # per-kernel bytes per particle of the HBM-bound kernels (reorder moves the 72-B state incl. L)
 KERNEL_BYTES = {"k_bin": 16 + 4 + 8 + 4, "k_scatter": 12 + 8, "k_reorder": 72 + 72 + 24 + 8}
 
@@ -133,8 +135,19 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ oracle timing
-def oracle_rate(name: str, steps: int):
-    """Time the fp64 oracle (as it stands) on a bounded sample of the workload."""
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_rate(name: str, steps: int, one_thread: bool = True):
+    """Time the fp64 oracle (as it stands) on a bounded sample of the workload on the host's cores,
+    and on one core (a smaller sample of the same recipe)."""
     import oracle
     oracle.build()
     if name.startswith("bed"):
@@ -148,8 +161,23 @@ def oracle_rate(name: str, steps: int):
     t0 = time.perf_counter()
     s.step(sample.dt, steps)
     t = time.perf_counter() - t0
-    return dict(value=sample.n_fluid * steps / t, unit=UNIT, cores=oracle.num_threads(), kind="oracle",
-                sample=f"{desc}; {steps} step(s) in {t:.2f} s; {sample.n_fluid + sample.n_bce} particles")
+    out = dict(value=sample.n_fluid * steps / t, unit=UNIT, cores=oracle.num_threads(), kind="oracle",
+               cpu_model=cpu_model(),
+               sample=f"{desc}; {steps} step(s) in {t:.2f} s; {sample.n_fluid + sample.n_bce} particles")
+    if one_thread:
+        nthr = oracle.num_threads()
+        s1 = workloads.bed(n=SAMPLE_BED_1T) if name.startswith("bed") else sample
+        o1 = oracle.load_scenario(s1)
+        oracle.set_num_threads(1)
+        try:
+            t0 = time.perf_counter()
+            o1.step(s1.dt, 1)
+            t1 = time.perf_counter() - t0
+        finally:
+            oracle.set_num_threads(nthr)
+        out["one_thread"] = {"value": s1.n_fluid / t1, "unit": UNIT, "cores": 1,
+                             "sample": f"{s1.n_fluid} fluid + {s1.n_bce} BCE; 1 step in {t1:.2f} s"}
+    return out
 
 
 def run_reference(args):
@@ -160,7 +188,7 @@ def run_reference(args):
         # torchrun pins OMP_NUM_THREADS=1 per rank; rank 0 runs alone here, so the oracle gets the
         # host's cores as at N = 1 (read by libgomp when liboracle loads, below)
         os.environ["OMP_NUM_THREADS"] = str(len(os.sched_getaffinity(0)))
-    cb = oracle_rate(args.config, max(1, args.steps + args.warmup) if args.config == "block8k" else 1)
+    cb = oracle_rate(args.config, max(1, args.steps + args.warmup) if args.config == "block8k" else 1, one_thread=False)
     # warm-up + timed steps of the oracle itself on the sample (bounded: one sample step per bench step)
     import oracle
     sample = workloads.bed(n=SAMPLE_BED) if args.config.startswith("bed") else scenario(args.config)
@@ -250,6 +278,7 @@ def main():
     ap.add_argument("--config", default="bed32M")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--repeats", type=int, default=3, help="timed K-step regions; the median is reported")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-next", action="store_true", help="skip the ps_freq = 10 (Alg. 2) measurement")
@@ -302,21 +331,31 @@ def main():
         dist.all_reduce(t)
         pairs_fluid = int(t.item())
 
-    # headline: K steps replayed from the library's CUDA graphs, CUDA events on its stream
+    # headline: K steps replayed from the library's CUDA graphs, CUDA events on its stream; the K-step
+    # region is timed R times (barrier + synchronize around each) and the median is reported
     clk = ClockSampler(local)
-    barrier()
-    torch.cuda.synchronize()
     clk.start()
-    n0 = g.launch_count()
-    ev0 = torch.cuda.Event(enable_timing=True); ev1 = torch.cuda.Event(enable_timing=True)
-    ev0.record(stream)
-    g.step(sc.dt, args.steps)
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    barrier()
+    reps = []
+    launches = 0
+    for _ in range(max(1, args.repeats)):
+        barrier()
+        torch.cuda.synchronize()
+        n0 = g.launch_count()
+        ev0 = torch.cuda.Event(enable_timing=True); ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        g.step(sc.dt, args.steps)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        launches = g.launch_count() - n0
+        r = ev0.elapsed_time(ev1)
+        if dist is not None:
+            t = torch.tensor([r], device=f"cuda:{local}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            r = float(t.item())
+        reps.append(r)
     clocks = clk.stop()
-    launches = g.launch_count() - n0
-    ms = ev0.elapsed_time(ev1)
+    ms = float(np.median(reps))
     # per-kernel device times: the same K steps again, launched kernel by kernel with an event
     # pair around every launch (crm_profile_*); not part of the headline
     g.profile(True)
@@ -327,10 +366,6 @@ def main():
     torch.cuda.synchronize()
     prof = g.profile_read()
     g.profile(False)
-    if dist is not None:
-        t = torch.tensor([ms], device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
     ms_step = ms / args.steps
     value = n_fluid / (ms_step * 1e-3)     # the whole job: every fluid particle, once per step
 
@@ -361,14 +396,26 @@ def main():
     roof["traffic"] = None
     prof_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof_path):
-        tr = json.load(open(prof_path)).get(args.config, {}).get(dname)
+        tj = json.load(open(prof_path))
+        tr = tj.get(args.config, {}).get(dname)
         if tr is not None:
             roof["traffic"] = tr
+            roof["traffic_source"] = ("committed ncu --set full capture (profiles/ncu_traffic.json, "
+                                      f"{tj.get('_source', 'see profiles/')}), not measured in this run")
     roof["peak_source"] = pk["source"]
     alg_bytes = n_fluid * BYTES_PER_FLUID_UPDATE + n_bce * BYTES_PER_BCE_UPDATE
     hbm = {"bytes_per_step": alg_bytes, "achieved_gbs": alg_bytes / (ms_step * 1e-3) / 1e9,
            "peak_gbs": pk["hbm_gbs"], "frac": alg_bytes / (ms_step * 1e-3) / 1e9 / pk["hbm_gbs"]}
     kernels = {k: {"ms_per_step": v[0] / args.steps, "launches": v[1]} for k, v in sorted(prof.items())}
+    # whole step against the FP32 ALU roof: the step's algorithmic flops (both pair
+    # stages, the Alg. 1 candidates, the epilogues) over the step time
+    n_own_s = g.count(crm.CRM_OWNED) if world > 1 else n_fluid
+    step_flops = (2 * pairs_local * FLOPS_PER_PAIR + (cand_local + cand_markers) * FLOPS_PER_CANDIDATE
+                  + min(n_own_s, n_fluid) * (FLOPS_EPILOGUE["k_rates_A"] + FLOPS_EPILOGUE["k_rates_B"]))
+    alu_step = {"flops_per_step": step_flops, "achieved_tflops": step_flops / (ms_step * 1e-3) / 1e12,
+                "peak_tflops": fp32_peak_tflops(pk["sm_max_mhz"]),
+                "frac": step_flops / (ms_step * 1e-3) / 1e12 / fp32_peak_tflops(pk["sm_max_mhz"]),
+                "note": "per rank; 2 x pairs x 84 + candidates x 8 + epilogues 110 + 170 per fluid particle"}
     # the same ALU roofline for each of the three hot kernels (the line's `roofline` is the largest)
     n_own_k = g.count(crm.CRM_OWNED) if world > 1 else n_fluid
     for k in ("k_filter", "k_rates_A", "k_rates_B"):
@@ -452,13 +499,14 @@ def main():
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+                "repeats_ms_per_step": [r / args.steps for r in reps],
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "config": {"workload": args.config, "n_fluid": n_fluid, "n_bce": n_bce, "d0": sc.params["d0"],
                            "h": sc.params["h"], "dt": sc.dt, "pairs_fluid": pairs_fluid,
                            "particle_updates_incl_bce_per_s": (n_fluid + n_bce) / (ms_step * 1e-3),
                            "l2": "inputs larger than L2 (56 B x N state >> 126 MB), no flush",
                            "parallelism": f"x-slabs x{world}, NCCL ghost planes" if world > 1 else "single GPU"},
-                "roofline": roof, "hbm_roofline": hbm, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
+                "roofline": roof, "hbm_roofline": hbm, "alu_roofline_step": alu_step, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clocks, "next_alg2": nxt, "next_active": nxt_active,
                 "next_cone": nxt_cone}
         print(json.dumps(line), flush=True)

@@ -90,6 +90,7 @@ def lib():
         L.oc_last_bce.argtypes = [C.c_void_p, C.c_int, _D, _D]
         L.oc_last_error.restype = C.c_char_p; L.oc_last_error.argtypes = [C.c_void_p]
         L.oc_num_threads.restype = C.c_int
+        L.oc_set_num_threads.argtypes = [C.c_int]; L.oc_set_num_threads.restype = None
         L.oc_activity.restype = C.c_int
         L.oc_activity.argtypes = [_D, C.c_int, _D, _D, _D, C.c_double]
         L.oc_manage_capacity.restype = C.c_int64
@@ -193,6 +194,10 @@ def return_map(sig_star, sig_n, params: dict, dt: float) -> np.ndarray:
 
 def num_threads() -> int:
     return lib().oc_num_threads()
+
+
+def set_num_threads(n: int) -> None:
+    lib().oc_set_num_threads(int(n))
 
 
 # ---------------- simulation ----------------

@@ -1035,3 +1035,13 @@ int oc_num_threads(void) {
   return 1;
 #endif
 }
+
+/* thread count of the following parallel loops (timing the oracle on 1 core; no arithmetic effect:
+   every loop is a gather with per-particle results) */
+void oc_set_num_threads(int n) {
+#ifdef _OPENMP
+  if (n > 0) omp_set_num_threads(n);
+#else
+  (void)n;
+#endif
+}

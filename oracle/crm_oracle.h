@@ -117,6 +117,7 @@ int  oc_set_active_delay(oc_sim* s, double t_delay);
 int  oc_get_activity(const oc_sim* s, uint8_t* flags);
 const char* oc_last_error(const oc_sim* s);
 int  oc_num_threads(void);
+void oc_set_num_threads(int n);
 
 #ifdef __cplusplus
 }

@@ -191,7 +191,8 @@ __device__ __forceinline__ void bytes4x4(uint32_t& r0, uint32_t& r1, uint32_t& r
 // append the particle's stored entries in group-major order and reset the state.  Stored so far:
 // per byte position p (two chunks) the words (A, B) at mw[2p], mw[2p + 1]; transposed in place, 4
 // byte positions at a time, into group words: mw[8 wd + g] = bytes 4 wd .. 4 wd + 3 of group g.
-__device__ __forceinline__ void gm_drain(FilterSmem& sm, GmState& st, uint32_t g0, ListWriter& w) {
+__device__ __forceinline__ void gm_drain(FilterSmem& sm, GmState& st, uint32_t g0, ListWriter& w, uint32_t fill,
+                                         bool final) {
   const uint32_t t = threadIdx.x;
   if (st.nch & 1) {   // a half-filled byte position
     const int p = st.nch >> 1;
@@ -219,19 +220,42 @@ __device__ __forceinline__ void gm_drain(FilterSmem& sm, GmState& st, uint32_t g
   // the non-empty words in emission order (groups g0, g0 + 1, ...): NZ rotated by 4 g0
   uint32_t nz = __funnelshift_r(NZ, NZ, 4u * (g0 & 7u));
   uint32_t W = 0, wd = 0, g = 0;
-  for (uint32_t e = 0; e < st.nent; ++e) {
-    // the next non-empty word when W is spent: one ffs, no search, no branch (the lanes of a warp
-    // reach the ends of their words at different entries)
+  // one entry: advance to the next non-empty word when W is spent (one ffs, no search, no branch:
+  // the lanes of a warp reach the ends of their words at different entries), take its lowest bit
+  auto next = [&]() -> uint32_t {
+    // (the indices stay inside the mask slots after the last entry, when nz and W are 0: the padded
+    //  tail of the last chunk calls this too)
     const bool adv = W == 0u;
-    const uint32_t pos = __ffs(nz) - 1;
+    const uint32_t pos = (__ffs(nz) - 1) & 31u;
     nz = adv ? (nz & (nz - 1)) : nz;
-    wd = adv ? (pos & 3u) : wd;
+    wd = adv ? min(pos & 3u, (uint32_t)GMW - 1u) : wd;
     g = adv ? ((g0 + (pos >> 2)) & 7u) : g;
     const uint32_t Wn = sm.mw[wd * 8 + g][t];
     W = adv ? Wn : W;
-    const uint32_t q = __ffs(W) - 1;   // bit q: chunk 8 wd + (q >> 2), candidate 8 (q & 3) + g of it
+    const uint32_t q = (__ffs(W) - 1) & 31u;   // bit q: chunk 8 wd + (q >> 2), candidate 8 (q & 3) + g of it
     W &= W - 1;
-    w.push((sm.wb[8 * wd + (q >> 2)][t] + 8u * (q & 3u) + g) << 4);
+    return (sm.wb[8 * wd + (q >> 2)][t] + 8u * (q & 3u) + g) << 4;
+  };
+  if (final && w.k == 0 && (int)st.nent <= w.cap) {
+    // the whole list at once (no early drain): whole chunks of 8 entries, one 16-B store each, the
+    // last chunk padded with the particle's own slot; e = 8c + u is the same on every lane of a
+    // warp, so the chunk's register positions are compile-time
+    uint4* row = reinterpret_cast<uint4*>(w.cur);
+    const uint32_t nchk = max(1u, (st.nent + 7u) >> 3);
+    for (uint32_t c = 0; c < nchk; ++c) {
+      uint32_t v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const uint32_t x = next();
+        v[u] = 8u * c + (uint32_t)u < st.nent ? x : fill;
+      }
+      row[(size_t)c * w.stride] = make_uint4(v[0] | (v[1] << 16), v[2] | (v[3] << 16), v[4] | (v[5] << 16),
+                                             v[6] | (v[7] << 16));
+    }
+    w.k = (int)st.nent;
+    w.closed = true;
+  } else {
+    for (uint32_t e = 0; e < st.nent; ++e) w.push(next());
   }
   gm_reset(st);
 }
@@ -240,7 +264,7 @@ __device__ __forceinline__ void gm_drain(FilterSmem& sm, GmState& st, uint32_t g
 // store one chunk's transposed hits (a, b: groups 0-3 / 4-7, bit n of byte p) at window base
 __device__ __forceinline__ void gm_store_chunk(FilterSmem& sm, GmState& st, uint32_t a, uint32_t b, uint32_t base,
                                                uint32_t g0, ListWriter& w) {
-  if (st.nch == FMW) gm_drain(sm, st, g0, w);   // all mask slots used: append what they hold now
+  if (st.nch == FMW) gm_drain(sm, st, g0, w, 0u, false);   // all mask slots used: append what they hold now
   const uint32_t t = threadIdx.x;
   sm.wb[st.nch][t] = (uint16_t)base;
   st.nent += __popc(a) + __popc(b);
@@ -385,7 +409,7 @@ __device__ __forceinline__ uint32_t filter_particle(float R2, FilterSmem& sm, co
       else filter_range<STAGED, STORE_BCE>(R2, sm, P, U, ob, oe, sf, gshift, pi, cnt, nw, nent, w);
     }
   }
-  if (STAGED && gmaj) gm_drain(sm, st, g0, w);
+  if (STAGED && gmaj) gm_drain(sm, st, g0, w, self << 4, true);
   else drain_masks<STAGED>(sm, nw, nent, w);
   return cnt;
 }

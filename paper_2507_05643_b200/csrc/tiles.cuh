@@ -364,15 +364,19 @@ struct ListShape {
 struct ListWriter {
   uint2* cur;        // the next 8-B half-chunk to store (chunk-major layout, see ListShape)
   size_t step;       // from half 1 of chunk c to half 0 of chunk c + 1: 2 * stride - 1 halves
+  size_t stride;     // uint4 rows per chunk
   uint32_t b0, b1;   // the last 4 entries (16 bits each, oldest in the low half of b0)
   int k;             // entries found (may exceed cap: overflow is reported by the caller)
   int cap;
+  bool closed;       // the list was written whole (padded) by its producer; flush does nothing
   __device__ __forceinline__ void init(uint16_t* list, size_t i, ListShape ls) {
     cur = reinterpret_cast<uint2*>(list) + 2 * i;
     step = 2 * (size_t)ls.stride - 1;
+    stride = ls.stride;
     b0 = b1 = 0u;
     k = 0;
     cap = ls.cap;
+    closed = false;
   }
   // (measured: 4-entry buffer + 8-B stores with the capacity test only at the store beat the
   //  16-B funnel buffer with a per-entry capacity branch, and one 2-B store per entry; the store
@@ -390,7 +394,7 @@ struct ListWriter {
   // pad the last chunk of 8 with `fill` (a zero-weight entry); k keeps the unpadded count.  An empty
   // list still gets one chunk of padding: the pair kernels prefetch chunk 0 of every list.
   __device__ __forceinline__ void flush(uint32_t fill) {
-    if (k >= cap) return;   // cap % 8 == 0: the stored part ends on a chunk boundary
+    if (closed || k >= cap) return;   // cap % 8 == 0: the stored part ends on a chunk boundary
     int kk = k;
     while ((kk & 7) || kk == 0) {
       b0 = __funnelshift_r(b0, b1, 16);

@@ -31,7 +31,7 @@ rep = os.path.join(g, "full_bed32M.ncu-rep")
 summ = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_summary.py"), rep], capture_output=True, text=True).stdout
 stalls = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_stalls.py"), rep], capture_output=True, text=True).stdout
 with open(os.path.join(out, f"{tag}_ncu_full_bed32M.txt"), "w") as f:
-    f.write(f"# ncu --set full --clock-control none --import-source on, tools/prof_step.py bed32M 3 (-s 4 -c 4). {note}\n")
+    f.write(f"# ncu --set full --clock-control none --import-source on -k regex:\"k_filter_t|k_rates_t|k_bce_t\" -s 5 -c 5, tools/prof_step.py bed32M 3. {note}\n")
     f.write(summ + "\n" + stalls + "\n# serialized launch list shares (ncu --metrics gpu__time_duration.sum, bench.py --steps 2 --warmup 3)\n" + shares + "\n")
 traffic, cur = {}, None
 for ln in summ.splitlines():
