@@ -58,6 +58,10 @@ struct crm {
   int cap = 0;
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t comm_stream = nullptr;   // slabs: halo transfers that overlap interior tiles (NCCL)
+  cudaEvent_t ev_boundary = nullptr, ev_comm = nullptr;
+  bool comm_pending = false;            // the compute stream must wait for ev_comm
+  bool halo_async = false;              // the next NCCL flush goes to comm_stream (phase 5)
   bool own_stream = false;
 
   // host staging (id order) until the first device use

@@ -226,6 +226,11 @@ int commit(crm_t* c) {
     ncclResult_t nr = api.commInitRank(&comm, c->world, id, c->rank);
     if (nr != ncclSuccess) return fail(c, CRM_E_COMM, std::string("ncclCommInitRank: ") + api.errorString(nr));
     c->nccl_comm = comm;
+    // the communication stream of the overlapped y_mid halo (dist.cuh, phases 5-7)
+    if (cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_boundary, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_comm, cudaEventDisableTiming) != cudaSuccess)
+      return fail(c, CRM_E_CUDA, "communication stream");
   }
   return CRM_OK;
 }
@@ -380,30 +385,39 @@ void issue_bce(crm_t* c, int stage, float dt, long long step, int store_all) {
 }
 
 // rates: stage 0 (fluid filter + rates at y_n -> y_mid), stage 1 (rates at y_mid -> y_{n+1})
+// (first, count): a range of the slab's tiles in launch order (slabs overlap the y_mid halo with the
+// interior columns); count < 0 = all tiles
 template <int KER>
-void issue_rates_k(crm_t* c, int stage, float dt, long long step) {
+void issue_rates_k(crm_t* c, int stage, float dt, long long step, long long first = 0, long long count = -1) {
   const int y = c->cur;
   const int dbg = c->dbg_on ? 1 : 0;
   if (tile_grid(c) == 0) return;
-  const dim3 tg((unsigned)tile_grid(c)), tb(TILE_THREADS);
+  if (count == 0) return;
+  const dim3 tg((unsigned)(count < 0 ? tile_grid(c) : count)), tb(TILE_THREADS);
+  const long long tbase = c->tile_base + (count < 0 ? 0 : first);
   const size_t sm = sizeof(TileSmem);
   if (stage == 0)
     launch_smem(c, KID_RATES_A, k_rates_t<0, KER>, tg, tb, sm, c->grid, c->ph, dt, (const uint32_t*)c->cell_start,
                 (const float4*)c->P[y], (const float4*)c->L[y], (const float4*)c->U[y], (const float4*)c->S1[y],
                 (const float2*)c->S2[y], c->Pm, c->Lm, c->Um, c->S1m, c->S2m, (const uint16_t*)c->list,
                 (const uint32_t*)c->nlist, list_shape(c), c->macc, c->dbg, dbg, c->d_err, (const uint32_t*)c->ids[y], step,
-                c->tile_base, tile_list(c));
+                tbase, count < 0 ? tile_list(c) : nullptr);
   else
     launch_smem(c, KID_RATES_B, k_rates_t<1, KER>, tg, tb, sm, c->grid, c->ph, dt, (const uint32_t*)c->cell_start,
                 (const float4*)c->Pm, (const float4*)c->Lm, (const float4*)c->Um, (const float4*)c->S1m,
                 (const float2*)c->S2m, c->P[y], c->L[y], c->U[y], c->S1[y], c->S2[y], (const uint16_t*)c->list,
                 (const uint32_t*)c->nlist, list_shape(c), c->macc, c->dbg, dbg, c->d_err, (const uint32_t*)c->ids[y], step,
-                c->tile_base, tile_list(c));
+                tbase, count < 0 ? tile_list(c) : nullptr);
 }
 
 void issue_rates(crm_t* c, int stage, float dt, long long step) {
   if (c->ker.kernel == CRM_KERNEL_WENDLAND) issue_rates_k<KER_WENDLAND>(c, stage, dt, step);
   else issue_rates_k<KER_CUBIC>(c, stage, dt, step);
+}
+
+void issue_rates_range(crm_t* c, int stage, float dt, long long step, long long first, long long count) {
+  if (c->ker.kernel == CRM_KERNEL_WENDLAND) issue_rates_k<KER_WENDLAND>(c, stage, dt, step, first, count);
+  else issue_rates_k<KER_CUBIC>(c, stage, dt, step, first, count);
 }
 
 // one RK2 step on one GPU (everything on the stream, no host sync)
@@ -718,7 +732,11 @@ void crm_destroy(crm_t* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->comm_stream) cudaStreamSynchronize(c->comm_stream);
   if (c->nccl_comm && nccl().commDestroy) nccl().commDestroy((ncclComm_t)c->nccl_comm);
+  if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+  if (c->ev_boundary) cudaEventDestroy(c->ev_boundary);
+  if (c->ev_comm) cudaEventDestroy(c->ev_comm);
   for (auto& r : c->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   for (int b = 0; b < 2; ++b) {

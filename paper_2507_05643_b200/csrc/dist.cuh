@@ -90,19 +90,40 @@ void post_mid_slice(crm_t* c, int peer, bool send, uint32_t b, uint32_t e) {
   post(c, peer, send, c->S2m + b, k * 8);
 }
 
-// NCCL transport: issue every pending transfer of this rank as one group on the stream
+// the compute stream waits for an asynchronous halo (phase 5's) before touching ghost slots
+void wait_comm(crm_t* c) {
+  if (!c->comm_pending) return;
+  cudaStreamWaitEvent(c->stream, c->ev_comm, 0);
+  c->comm_pending = false;
+}
+
+// NCCL transport: issue every pending transfer of this rank as one group on the stream (or, for the
+// y_mid halo of phase 5, on the communication stream after the boundary tiles: it overlaps the
+// interior tiles of phase 6)
 int nccl_flush(crm_t* c) {
+  const bool async = c->halo_async;
+  c->halo_async = false;
   if (c->posts.empty()) return CRM_OK;
   NcclApi& api = nccl();
   ncclComm_t comm = (ncclComm_t)c->nccl_comm;
+  cudaStream_t st = c->stream;
+  if (async) {
+    cudaEventRecord(c->ev_boundary, c->stream);
+    cudaStreamWaitEvent(c->comm_stream, c->ev_boundary, 0);
+    st = c->comm_stream;
+  }
   ncclResult_t r = api.groupStart();
   for (const Post& p : c->posts) {
     if (r != ncclSuccess) break;
-    r = p.send ? api.send(p.ptr, p.bytes, ncclUint8, p.peer, comm, c->stream)
-               : api.recv(p.ptr, p.bytes, ncclUint8, p.peer, comm, c->stream);
+    r = p.send ? api.send(p.ptr, p.bytes, ncclUint8, p.peer, comm, st)
+               : api.recv(p.ptr, p.bytes, ncclUint8, p.peer, comm, st);
   }
   ncclResult_t r2 = api.groupEnd();
   c->posts.clear();
+  if (async) {
+    cudaEventRecord(c->ev_comm, c->comm_stream);
+    c->comm_pending = true;
+  }
   if (r != ncclSuccess || r2 != ncclSuccess)
     return fail(c, CRM_E_COMM, std::string("NCCL: ") + (api.errorString ? api.errorString(r != ncclSuccess ? r : r2) : "error"));
   return CRM_OK;
@@ -110,6 +131,7 @@ int nccl_flush(crm_t* c) {
 
 // loopback transport: match every send of rank a to rank b with b's receives from a (FIFO)
 int loopback_flush(crm_t** cs, int world) {
+  for (int a = 0; a < world; ++a) cs[a]->halo_async = false;   // one shared stream: serial copies
   std::vector<std::vector<size_t>> used(world);
   for (int a = 0; a < world; ++a) used[a].assign(cs[a]->posts.size(), 0);
   for (int a = 0; a < world; ++a) {
@@ -203,6 +225,7 @@ int post_counts(crm_t* c, uint32_t l0, uint32_t l1, uint32_t r0, uint32_t r1) {
 void issue_sort(crm_t* c, long long step, uint32_t drop_mask);
 void issue_bce(crm_t* c, int stage, float dt, long long step, int store_all);
 void issue_rates(crm_t* c, int stage, float dt, long long step);
+void issue_rates_range(crm_t* c, int stage, float dt, long long step, long long first, long long count);
 void issue_body_partial(crm_t* c);
 void issue_body_finish(crm_t* c);
 
@@ -217,12 +240,11 @@ int slab_phase(crm_t* c, int k, float dt, long long step) {
       launch(c, KID_STEP, k_step_begin, dim3(1), dim3(1), c->d_err, step);
       if (!c->slab_rebuild) return CRM_OK;
       issue_sort(c, step, TAG_GHOST | TAG_DROP);
-      const int ps[4] = {c->x_lo, c->x_lo + 1, c->x_hi - 1, c->x_hi};
-      uint32_t st[4], nk;
-      if (int r = read_plane_starts(c, ps, 4, st)) return r;
-      const int pm[1] = {c->grid.dims[0]};
-      if (int r = read_plane_starts(c, pm, 1, &nk)) return r;
-      c->nl = nk;
+      // one host read: the plane starts and the end of the sorted cells (one sync per read)
+      const int ps[5] = {c->x_lo, c->x_lo + 1, c->x_hi - 1, c->x_hi, c->grid.dims[0]};
+      uint32_t st[5];
+      if (int r = read_plane_starts(c, ps, 5, st)) return r;
+      c->nl = st[4];
       c->s_lo = st[0]; c->s_lo1 = st[1]; c->s_hi1 = st[2]; c->s_hi = st[3];
       c->mig_l = c->s_lo;
       c->mig_r = (uint32_t)c->nl - c->s_hi;
@@ -290,12 +312,10 @@ int slab_phase(crm_t* c, int k, float dt, long long step) {
         if (ng) launch(c, KID_SLAB, k_or_tag, dim3(blocks(ng, 256)), dim3(256), c->U[y0], c->n_app, c->n_app + ng, TAG_GHOST);
         c->nl = c->n_app + ng;
         issue_sort(c, step, TAG_DROP);
-        const int ps[6] = {c->x_lo - 1, c->x_lo, c->x_lo + 1, c->x_hi - 1, c->x_hi, c->x_hi + 1};
-        uint32_t st[6], nk;
-        if (int r = read_plane_starts(c, ps, 6, st)) return r;
-        const int pm[1] = {c->grid.dims[0]};
-        if (int r = read_plane_starts(c, pm, 1, &nk)) return r;
-        c->nl = nk;
+        const int ps[7] = {c->x_lo - 1, c->x_lo, c->x_lo + 1, c->x_hi - 1, c->x_hi, c->x_hi + 1, c->grid.dims[0]};
+        uint32_t st[7];
+        if (int r = read_plane_starts(c, ps, 7, st)) return r;
+        c->nl = st[6];
         c->s_lom1 = c->rank > 0 ? st[0] : st[1];
         c->s_lo = st[1]; c->s_lo1 = st[2]; c->s_hi1 = st[3]; c->s_hi = st[4];
         c->s_hip1 = c->rank < c->world - 1 ? st[5] : st[4];
@@ -317,8 +337,18 @@ int slab_phase(crm_t* c, int k, float dt, long long step) {
       post_slice(c, R, false, y, c->s_hi, c->s_hip1, false);
       return CRM_OK;
     }
-    case 5:   // rates + half step; y_mid boundary planes -> ghosts
-    case 6: { // BCE at y_mid; y_mid boundary planes -> ghosts
+    case 5:   // rates + half step on the boundary tile columns (all tiles with moving bodies); y_mid halo
+    case 6:   // rates + half step on the interior tile columns, overlapping the y_mid halo (NCCL)
+    case 7: { // BCE at y_mid; y_mid boundary planes -> ghosts
+      // Overlap: the ghost planes a neighbour needs are the y_mid of this slab's first and last
+      // planes, which lie in its first and last tile columns (TX planes each).  Stage A runs on
+      // those columns first, their y_mid goes out on the communication stream while the interior
+      // columns compute (the interior reads y_n only and writes owned slots only; the ghost slots
+      // the halo fills are read by stage B).  Moving bodies re-place their markers in y_mid after
+      // the whole stage A, so that case keeps one launch and a serial halo.
+      const long long per_x = (long long)tiles_y(c->grid) * tiles_z(c->grid);
+      const long long ntx = per_x ? c->ntiles / per_x : 0;
+      const bool split = c->n_moving_markers == 0 && c->boxes.empty() && ntx > 2;
       if (k == 5) {
         // the copies of E4 carried the owners' tags: mark the ghost planes as ghosts again
         const int y = c->cur;
@@ -326,12 +356,22 @@ int slab_phase(crm_t* c, int k, float dt, long long step) {
           launch(c, KID_SLAB, k_or_tag, dim3(blocks(c->s_lo - c->s_lom1, 256)), dim3(256), c->U[y], c->s_lom1, c->s_lo, TAG_GHOST);
         if (c->s_hip1 > c->s_hi)
           launch(c, KID_SLAB, k_or_tag, dim3(blocks(c->s_hip1 - c->s_hi, 256)), dim3(256), c->U[y], c->s_hi, c->s_hip1, TAG_GHOST);
-        issue_rates(c, 0, dt, step);
-        if (c->n_moving_markers)   // moving markers at the mid-step pose, before the y_mid halo
-          launch(c, KID_MARKERS, k_markers_place, dim3(blocks(c->n_moving_markers, 128)), dim3(128),
-                 c->n_moving_markers, (const uint32_t*)c->d_moving_ids, (const float4*)c->d_xlocal,
-                 (const uint32_t*)c->slot_of_id, (const Pose*)c->d_posem, c->Pm, c->Lm, (const float4*)c->Um);
+        if (split) {
+          issue_rates_range(c, 0, dt, step, 0, per_x);                    // first tile column
+          issue_rates_range(c, 0, dt, step, (ntx - 1) * per_x, per_x);    // last tile column
+          c->halo_async = true;   // the flush after this phase runs on the communication stream
+        } else {
+          issue_rates(c, 0, dt, step);
+          if (c->n_moving_markers)   // moving markers at the mid-step pose, before the y_mid halo
+            launch(c, KID_MARKERS, k_markers_place, dim3(blocks(c->n_moving_markers, 128)), dim3(128),
+                   c->n_moving_markers, (const uint32_t*)c->d_moving_ids, (const float4*)c->d_xlocal,
+                   (const uint32_t*)c->slot_of_id, (const Pose*)c->d_posem, c->Pm, c->Lm, (const float4*)c->Um);
+        }
+      } else if (k == 6) {
+        if (split) issue_rates_range(c, 0, dt, step, per_x, (ntx - 2) * per_x);
+        return CRM_OK;
       } else {
+        wait_comm(c);
         issue_bce(c, 1, dt, step, 0);
       }
       post_mid_slice(c, L, true, c->s_lo, c->s_lo1);
@@ -340,7 +380,8 @@ int slab_phase(crm_t* c, int k, float dt, long long step) {
       post_mid_slice(c, R, false, c->s_hi, c->s_hip1);
       return CRM_OK;
     }
-    case 7:   // rates + full step; moving bodies: this slab's partial loads to every other slab
+    case 8:   // rates + full step; moving bodies: this slab's partial loads to every other slab
+      wait_comm(c);
       issue_rates(c, 1, dt, step);
       if (c->n_moving_bodies) {
         issue_body_partial(c);
@@ -352,12 +393,12 @@ int slab_phase(crm_t* c, int k, float dt, long long step) {
         }
       }
       return CRM_OK;
-    case 8:   // moving bodies: loads summed over slabs in rank order (identical on every rank), update
+    case 9:   // moving bodies: loads summed over slabs in rank order (identical on every rank), update
       if (c->n_moving_bodies) issue_body_finish(c);
       return CRM_OK;
   }
   return CRM_OK;
 }
-constexpr int kSlabPhases = 9;
+constexpr int kSlabPhases = 10;
 
 }  // namespace
