@@ -731,7 +731,10 @@ int crm_create(const crm_material_t* mat, const crm_kernel_t* ker, const crm_bou
 void crm_destroy(crm_t* c) {
   if (!c) return;
   cudaSetDevice(c->device);
-  if (c->stream) cudaStreamSynchronize(c->stream);
+  // a borrowed stream (dist->cuda_stream, e.g. another in-process slab context's) may already be
+  // destroyed by its owner: wait on the device instead of on the stream handle
+  if (c->own_stream && c->stream) cudaStreamSynchronize(c->stream);
+  else cudaDeviceSynchronize();
   if (c->comm_stream) cudaStreamSynchronize(c->comm_stream);
   if (c->nccl_comm && nccl().commDestroy) nccl().commDestroy((ncclComm_t)c->nccl_comm);
   if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
