@@ -419,6 +419,9 @@ __global__ void TILE_BOUNDS
   // lo parts of the window's positions and the own state of each thread's first particle are
   // requested beside it (before the bookkeeping barrier: issued after it, the lo loads queued
   // behind the copy and added ~3k cycles to every tile's prologue)
+  // (measured: the copy on the bulk-copy engine, 48 cp.async.bulk of ~1.7 KB per tile with an
+  //  mbarrier byte count, ran 1.5 % slower — here and in round 1: the window's arrival rate, not the
+  //  copy instructions, bounds the prologue)
   tile_stage(P, U, S1, S2, sm);
   RelPre rp;
   relativize_load(L, sm, rp);
@@ -456,11 +459,8 @@ __global__ void TILE_BOUNDS
   }
   const bool any = __syncthreads_or(work);
   EXP_T(2)
-  if (!any) {
-    tile_stage_wait();
-    return;
-  }
   tile_stage_wait();
+  if (!any) return;
   __syncthreads();
   EXP_T(3)
   relativize_apply<true>(sm, rp, ph.m);
