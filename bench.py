@@ -44,6 +44,10 @@ FLOPS_PER_PAIR = 84
 FLOPS_PER_CANDIDATE = 8
 FLOPS_PER_BCE_PAIR = 30
 FLOPS_EPILOGUE = {"k_rates_A": 110, "k_rates_B": 170}
+# FP32-pipe issue slots per unit of algorithmic work (~63 per directed pair of the
+# rates loop, ~7 per neighbour-search candidate) against 148 SM x 128 lanes x f_SM slots/s (D5)
+SLOTS_PER_PAIR = 63
+SLOTS_PER_CANDIDATE = 7
 # algorithmic HBM bytes per fluid particle-update and per BCE marker
 BYTES_PER_FLUID_UPDATE = 404
 BYTES_PER_BCE_UPDATE = 72
@@ -387,6 +391,11 @@ def main():
                 "pairs": pairs_local, "candidates": cand_local + cand_markers,
                 "flops_per_candidate": FLOPS_PER_CANDIDATE,
                 "share_of_step": dms / args.steps / ms_step,
+                "fp32_issue_frac": ((cand_local + cand_markers) * SLOTS_PER_CANDIDATE if dname == "k_filter"
+                                    else pairs_local * SLOTS_PER_PAIR) / per_launch_s
+                                   / (148 * 128 * pk["sm_max_mhz"] * 1e6),
+                "fp32_issue_note": "SURVEY D3/D5: 7 issue slots per candidate, 63 per directed pair, over "
+                                   "148 x 128 lanes x sm_max_mhz",
                 "peak_note": "148 SM x 128 FP32 lanes x 2 x sm_max_mhz (DESIGN.md §Roofline)"}
     else:
         nbytes = (n_fluid + n_bce) * KERNEL_BYTES.get(dname, 56)
@@ -424,6 +433,10 @@ def main():
                   else pairs_local * FLOPS_PER_PAIR + min(n_own_k, n_fluid) * FLOPS_EPILOGUE[k])
             tf = fl / (prof[k][0] / prof[k][1] * 1e-3) / 1e12
             kernels[k].update({"alu_tflops": tf, "alu_frac": tf / fp32_peak_tflops(pk["sm_max_mhz"])})
+            slots = ((cand_local + cand_markers) * SLOTS_PER_CANDIDATE if k == "k_filter"
+                     else pairs_local * SLOTS_PER_PAIR)
+            kernels[k]["fp32_issue_frac"] = (slots / (prof[k][0] / prof[k][1] * 1e-3)
+                                             / (148 * 128 * pk["sm_max_mhz"] * 1e6))
 
     # e2e through the public API with pinned host buffers
     e2e = None
