@@ -135,7 +135,9 @@ struct crm {
   // per-step slab bookkeeping (slots in the current buffer)
   uint32_t s_lo = 0, s_lo1 = 0, s_hi1 = 0, s_hi = 0;   // starts of planes x_lo, x_lo+1, x_hi-1, x_hi
   uint32_t s_lom1 = 0, s_hip1 = 0;                     // starts of planes x_lo-1 and x_hi+1 (ghost ranges)
-  uint32_t mig_l = 0, mig_r = 0, rcv_l = 0, rcv_r = 0, gh_l = 0, gh_r = 0, n_app = 0;
+  uint32_t pk_n[4] = {0, 0, 0, 0};     // packed at this rebuild: E_left, G_left, E_right, G_right
+  uint32_t rv_n[4] = {0, 0, 0, 0};     // received: E / G from the left, E / G from the right
+  SlabPack pk{};                       // pack buffers of the slab rebuild (structure.cuh k_slab_pack)
 
   // active domains (Alg. 3): boxes per body, the active-set capacity of
   // the arrays indexed by sorted slot (lists, mid state, marker loads) and its ManageArrayMemory policy

@@ -104,6 +104,22 @@ int commit(crm_t* c) {
   r |= dalloc(c, &c->d_err, 1);
   r |= dalloc(c, &c->d_mtiles, (size_t)std::max<long long>(num_tiles(c->grid), 1)); r |= dalloc(c, &c->d_mtile_cnt, 1);
   r |= dalloc(c, &c->d_xcount, 8);
+  if (c->slab) {   // pack buffers: emigrants (E) and a boundary plane (G) per side
+    int64_t maxp = 0;
+    {
+      std::vector<int64_t> cnt(c->grid.dims[0], 0);
+      for (int64_t i = 0; i < c->n; ++i) cnt[host_plane(c->grid, c->hP[i].x)]++;
+      for (int64_t v : cnt) maxp = std::max(maxp, v);
+    }
+    c->pk.cap_e = (uint32_t)(maxp + 1024);
+    c->pk.cap_g = (uint32_t)(2 * maxp + 1024);
+    const size_t pc = (size_t)c->pk.cap_e + c->pk.cap_g;
+    for (int d = 0; d < 2; ++d) {
+      r |= dalloc(c, &c->pk.P[d], pc); r |= dalloc(c, &c->pk.L[d], pc); r |= dalloc(c, &c->pk.U[d], pc);
+      r |= dalloc(c, &c->pk.S1[d], pc); r |= dalloc(c, &c->pk.S2[d], pc); r |= dalloc(c, &c->pk.id[d], pc);
+    }
+    r |= dalloc(c, &c->pk.cnt, 4);
+  }
   c->acap = (int64_t)n;
   if (!c->boxes.empty()) {   // active domains (Alg. 3)
     r |= dalloc(c, &c->d_boxes, c->boxes.size());
@@ -269,8 +285,8 @@ void issue_sort(crm_t* c, long long step, uint32_t drop_mask) {
   }
   launch(c, KID_SCATTER, k_scatter, dim3(blocks(n, 256)), dim3(256), n, (const uint32_t*)c->key,
          (const uint32_t*)c->arrival, (const uint32_t*)c->cell_start, (const uint32_t*)c->ids[a], c->tmp_src, c->tmp_id);
-  if (c->slab)
-    launch(c, KID_SLAB, k_fill_u32, dim3(blocks(c->n, 256)), dim3(256), c->slot_of_id, (long long)c->n, 0xffffffffu);
+  if (c->slab && n)
+    launch(c, KID_SLAB, k_clear_slots, dim3(blocks(n, 256)), dim3(256), n, (const uint32_t*)c->ids[a], c->slot_of_id);
   launch(c, KID_REORDER, k_reorder, dim3(blocks(n, 256)), dim3(256), n, (const uint32_t*)c->tmp_src,
          (const uint32_t*)c->tmp_id, (const uint32_t*)c->key, (const uint32_t*)c->cell_start,
          (const float4*)c->P[a], (const float4*)c->L[a], (const float4*)c->U[a], (const float4*)c->S1[a],
@@ -759,6 +775,11 @@ void crm_destroy(crm_t* c) {
   for (auto p : c->scan_sums_x) cudaFree(p);
   cudaFree(c->d_bodies); cudaFree(c->d_pose0); cudaFree(c->d_posem);
   cudaFree(c->d_moving_ids); cudaFree(c->d_xlocal); cudaFree(c->d_mstart); cudaFree(c->d_moving_bodies);
+  for (int d = 0; d < 2; ++d) {
+    cudaFree(c->pk.P[d]); cudaFree(c->pk.L[d]); cudaFree(c->pk.U[d]); cudaFree(c->pk.S1[d]); cudaFree(c->pk.S2[d]);
+    cudaFree(c->pk.id[d]);
+  }
+  cudaFree(c->pk.cnt);
   cudaFree(c->macc); cudaFree(c->d_bpart); cudaFree(c->d_err); cudaFree(c->d_xcount); cudaFree(c->dbg_ids); cudaFree(c->d_stage);
   if (c->h_err) cudaFreeHost(c->h_err);
   if (c->h_pin) cudaFreeHost(c->h_pin);

@@ -3,16 +3,19 @@
 // Each rank owns the cell planes [x_lo, x_hi) (boundaries from a prefix sum of per-plane particle
 // counts, aligned to the tile width) and keeps one ghost plane (one 2h cell) on each interior
 // face.  With the B3 cell order a plane is one contiguous index range of the sorted state, so
-// every exchange is a handful of contiguous slices (zero pack).  Per step:
-//   P0  sort (previous ghosts dropped); emigrants = particles now outside [x_lo, x_hi)
-//   E0  counts of emigrants                      E1  emigrant payloads (id + 56 B state)
-//   P2  emigrants marked dropped, immigrants checked to sit in the boundary plane
-//   E2  counts of boundary planes                E3  boundary planes -> neighbour ghost planes
-//   P4  sort (ghosts in, emigrants out), BCE extrapolation at y_n on owned tiles
+// every exchange is a handful of contiguous slices.  Per step:
+//   P0  one pass over the local particles (k_slab_pack): last step's ghosts dropped; owned particles
+//       now in a neighbour's first plane packed as emigrants (kept here as ghosts); owned particles of
+//       the first / last plane packed as the neighbours' ghost planes;      E0  counts
+//   P1  E1  payloads (id + 72-B state), appended: immigrants, then ghosts
+//   P2  immigrants checked to sit in the boundary plane, received ghosts flagged
+//   P4  the one sort of the step (ghosts in, emigrants and old ghosts out), BCE at y_n on owned tiles
 //   E4  boundary planes (markers now extrapolated) -> ghosts
-//   P5  rates + half step on owned tiles         E5  y_mid boundary planes -> ghosts
-//   P6  BCE extrapolation at y_mid               E6  y_mid boundary planes -> ghosts
-//   P7  rates + full step + return map on owned tiles
+//   P5  rates + half step, boundary tile columns     E5  y_mid boundary planes -> ghosts
+//   P6  rates + half step, interior columns (overlaps E5 on the NCCL transport)
+//   P7  BCE extrapolation at y_mid                   E7  y_mid boundary planes -> ghosts
+//   P8  rates + full step + return map on owned tiles
+// (Alg. 2 reuse steps skip P0-P2 and the sort and refresh the ghost values in P3.)
 // Neighbour iteration order is the global (cell, id) order restricted to the local planes, so
 // owned particles follow bit-identical trajectories to a one-GPU run.
 // Transports: NCCL point-to-point (ncclSend/ncclRecv in a group, on the context stream; NCCL is
@@ -234,83 +237,78 @@ void issue_body_finish(crm_t* c);
 int slab_phase(crm_t* c, int k, float dt, long long step) {
   const int L = c->rank - 1, R = c->rank + 1;
   switch (k) {
-    case 0: {   // sort owned particles (drop last step's ghosts), count emigrants
+    case 0: {   // rebuild: one pass packs emigrants and boundary planes per side (no sort here)
       // Alg. 2: between rebuilds the slots, ghost sets and lists stay; only values move (phase 3)
       c->slab_rebuild = !c->lists_valid || (step % c->ps_freq) == 0;
       launch(c, KID_STEP, k_step_begin, dim3(1), dim3(1), c->d_err, step);
       if (!c->slab_rebuild) return CRM_OK;
-      issue_sort(c, step, TAG_GHOST | TAG_DROP);
-      // one host read: the plane starts and the end of the sorted cells (one sync per read)
-      const int ps[5] = {c->x_lo, c->x_lo + 1, c->x_hi - 1, c->x_hi, c->grid.dims[0]};
-      uint32_t st[5];
-      if (int r = read_plane_starts(c, ps, 5, st)) return r;
-      c->nl = st[4];
-      c->s_lo = st[0]; c->s_lo1 = st[1]; c->s_hi1 = st[2]; c->s_hi = st[3];
-      c->mig_l = c->s_lo;
-      c->mig_r = (uint32_t)c->nl - c->s_hi;
-      return post_counts(c, c->mig_l, 0, c->mig_r, 0);
-    }
-    case 1: {   // emigrant payloads: [0, s_lo) -> left, [s_hi, nl) -> right; immigrants appended
-      if (!c->slab_rebuild) return CRM_OK;
-      if (int r = read_counts(c, &c->rcv_l, nullptr, &c->rcv_r, nullptr)) return r;
-      const uint32_t nl = (uint32_t)c->nl;
-      if ((int64_t)nl + c->rcv_l + c->rcv_r > c->ncap) return fail(c, CRM_E_CAPACITY, "slab capacity exceeded (immigrants)");
       const int y = c->cur;
-      post_slice(c, L, true, y, 0, c->mig_l, true);
-      post_slice(c, R, true, y, c->s_hi, nl, true);
-      post_slice(c, L, false, y, nl, nl + c->rcv_l, true);
-      post_slice(c, R, false, y, nl + c->rcv_l, nl + c->rcv_l + c->rcv_r, true);
-      return CRM_OK;
+      CK(cudaMemsetAsync(c->pk.cnt, 0, 16, c->stream));
+      if (c->nl)
+        launch(c, KID_SLAB, k_slab_pack, dim3(blocks(c->nl, 256)), dim3(256), (int)c->nl, (const float4*)c->P[y],
+               (const float4*)c->L[y], c->U[y], (const float4*)c->S1[y], (const float2*)c->S2[y],
+               (const uint32_t*)c->ids[y], c->grid, c->x_lo, c->x_hi, c->rank > 0 ? 1 : 0,
+               c->rank < c->world - 1 ? 1 : 0, c->pk, c->d_err, step);
+      CK(cudaMemcpyAsync(c->h_pin + 32, c->pk.cnt, 16, cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      for (int k = 0; k < 4; ++k) c->pk_n[k] = c->h_pin[32 + k];
+      if (c->pk_n[0] > c->pk.cap_e || c->pk_n[2] > c->pk.cap_e || c->pk_n[1] > c->pk.cap_g || c->pk_n[3] > c->pk.cap_g)
+        return fail(c, CRM_E_CAPACITY, "slab pack buffers exceeded (emigrants or boundary plane)");
+      return post_counts(c, c->pk_n[0], c->pk_n[1], c->pk_n[2], c->pk_n[3]);
     }
-    case 2: {   // mark emigrants dropped, check immigrants, count boundary planes
+    case 1: {   // rebuild: payloads — emigrants (owned there) and boundary planes (ghosts there), appended
       if (!c->slab_rebuild) return CRM_OK;
-      const int y = c->cur;
+      uint32_t el, gl, er, gr;
+      if (int r = read_counts(c, &el, &gl, &er, &gr)) return r;
+      c->rv_n[0] = el; c->rv_n[1] = gl; c->rv_n[2] = er; c->rv_n[3] = gr;
       const uint32_t nl = (uint32_t)c->nl;
-      if (c->mig_l) launch(c, KID_SLAB, k_or_tag, dim3(blocks(c->mig_l, 256)), dim3(256), c->U[y], 0u, c->mig_l, TAG_DROP);
-      if (c->mig_r) launch(c, KID_SLAB, k_or_tag, dim3(blocks(c->mig_r, 256)), dim3(256), c->U[y], c->s_hi, nl, TAG_DROP);
-      if (c->rcv_l)
-        launch(c, KID_SLAB, k_check_plane, dim3(blocks(c->rcv_l, 256)), dim3(256), (const float4*)c->P[y],
-               (const uint32_t*)c->ids[y], nl, nl + c->rcv_l, c->grid, c->x_lo, c->d_err, step);
-      if (c->rcv_r)
-        launch(c, KID_SLAB, k_check_plane, dim3(blocks(c->rcv_r, 256)), dim3(256), (const float4*)c->P[y],
-               (const uint32_t*)c->ids[y], nl + c->rcv_l, nl + c->rcv_l + c->rcv_r, c->grid, c->x_hi - 1, c->d_err, step);
-      c->n_app = nl + c->rcv_l + c->rcv_r;
-      // boundary plane = (owned particles of the plane, immigrants into it): two parts per side
-      return post_counts(c, c->s_lo1 - c->s_lo, c->rcv_l, c->s_hi - c->s_hi1, c->rcv_r);
-    }
-    case 3: {   // boundary planes -> neighbours' ghost planes (appended, flagged in phase 4)
-      if (!c->slab_rebuild) {   // reuse step: refresh the ghost values y_n in place
-        const int y = c->cur;
-        post_slice(c, L, true, y, c->s_lo, c->s_lo1, false);
-        post_slice(c, R, true, y, c->s_hi1, c->s_hi, false);
-        post_slice(c, L, false, y, c->s_lom1, c->s_lo, false);
-        post_slice(c, R, false, y, c->s_hi, c->s_hip1, false);
-        return CRM_OK;
+      if ((int64_t)nl + el + gl + er + gr > c->ncap) return fail(c, CRM_E_CAPACITY, "slab capacity exceeded (immigrants + ghosts)");
+      const int y = c->cur;
+      for (int d = 0; d < 2; ++d) {   // sends: E then G of each side (the receiver posts in the same order)
+        const int peer = d == 0 ? L : R;
+        const uint32_t ne = c->pk_n[2 * d], ng = c->pk_n[2 * d + 1], g0 = c->pk.cap_e;
+        post(c, peer, true, c->pk.P[d], ne * 16); post(c, peer, true, c->pk.L[d], ne * 16);
+        post(c, peer, true, c->pk.U[d], ne * 16); post(c, peer, true, c->pk.S1[d], ne * 16);
+        post(c, peer, true, c->pk.S2[d], ne * 8); post(c, peer, true, c->pk.id[d], ne * 4);
+        post(c, peer, true, c->pk.P[d] + g0, ng * 16); post(c, peer, true, c->pk.L[d] + g0, ng * 16);
+        post(c, peer, true, c->pk.U[d] + g0, ng * 16); post(c, peer, true, c->pk.S1[d] + g0, ng * 16);
+        post(c, peer, true, c->pk.S2[d] + g0, ng * 8); post(c, peer, true, c->pk.id[d] + g0, ng * 4);
       }
-      uint32_t la, lb, ra, rb;
-      if (int r = read_counts(c, &la, &lb, &ra, &rb)) return r;
-      c->gh_l = la + lb;
-      c->gh_r = ra + rb;
-      if ((int64_t)c->n_app + c->gh_l + c->gh_r > c->ncap) return fail(c, CRM_E_CAPACITY, "slab capacity exceeded (ghosts)");
-      const int y = c->cur;
-      const uint32_t nl = (uint32_t)c->nl;
-      post_slice(c, L, true, y, c->s_lo, c->s_lo1, true);
-      post_slice(c, L, true, y, nl, nl + c->rcv_l, true);
-      post_slice(c, R, true, y, c->s_hi1, c->s_hi, true);
-      post_slice(c, R, true, y, nl + c->rcv_l, nl + c->rcv_l + c->rcv_r, true);
-      const uint32_t a0 = c->n_app, a1 = a0 + la, a2 = a1 + lb, a3 = a2 + ra, a4 = a3 + rb;
+      // receives, appended behind the local particles: [E left][G left][E right][G right]
+      const uint32_t a0 = nl, a1 = a0 + el, a2 = a1 + gl, a3 = a2 + er, a4 = a3 + gr;
       post_slice(c, L, false, y, a0, a1, true);
       post_slice(c, L, false, y, a1, a2, true);
       post_slice(c, R, false, y, a2, a3, true);
       post_slice(c, R, false, y, a3, a4, true);
       return CRM_OK;
     }
+    case 2: {   // rebuild: immigrants checked to sit in the boundary plane; ghosts flagged
+      if (!c->slab_rebuild) return CRM_OK;
+      const int y = c->cur;
+      const uint32_t nl = (uint32_t)c->nl;
+      const uint32_t a0 = nl, a1 = a0 + c->rv_n[0], a2 = a1 + c->rv_n[1], a3 = a2 + c->rv_n[2], a4 = a3 + c->rv_n[3];
+      if (a1 > a0)
+        launch(c, KID_SLAB, k_check_plane, dim3(blocks(a1 - a0, 256)), dim3(256), (const float4*)c->P[y],
+               (const uint32_t*)c->ids[y], a0, a1, c->grid, c->x_lo, c->d_err, step);
+      if (a3 > a2)
+        launch(c, KID_SLAB, k_check_plane, dim3(blocks(a3 - a2, 256)), dim3(256), (const float4*)c->P[y],
+               (const uint32_t*)c->ids[y], a2, a3, c->grid, c->x_hi - 1, c->d_err, step);
+      if (a2 > a1) launch(c, KID_SLAB, k_or_tag, dim3(blocks(a2 - a1, 256)), dim3(256), c->U[y], a1, a2, TAG_GHOST);
+      if (a4 > a3) launch(c, KID_SLAB, k_or_tag, dim3(blocks(a4 - a3, 256)), dim3(256), c->U[y], a3, a4, TAG_GHOST);
+      c->nl = a4;
+      return CRM_OK;
+    }
+    case 3: {   // Alg. 2 reuse step: refresh the ghost values y_n in place
+      if (c->slab_rebuild) return CRM_OK;
+      const int y = c->cur;
+      post_slice(c, L, true, y, c->s_lo, c->s_lo1, false);
+      post_slice(c, R, true, y, c->s_hi1, c->s_hi, false);
+      post_slice(c, L, false, y, c->s_lom1, c->s_lo, false);
+      post_slice(c, R, false, y, c->s_hi, c->s_hip1, false);
+      return CRM_OK;
+    }
     case 4: {   // ghosts flagged, local sort, BCE at y_n; boundary planes -> ghosts
-      if (c->slab_rebuild) {
-        const int y0 = c->cur;
-        const uint32_t ng = c->gh_l + c->gh_r;
-        if (ng) launch(c, KID_SLAB, k_or_tag, dim3(blocks(ng, 256)), dim3(256), c->U[y0], c->n_app, c->n_app + ng, TAG_GHOST);
-        c->nl = c->n_app + ng;
+      if (c->slab_rebuild) {   // the one sort of the rebuild: old ghosts out, emigrants kept as ghosts
         issue_sort(c, step, TAG_DROP);
         const int ps[7] = {c->x_lo - 1, c->x_lo, c->x_lo + 1, c->x_hi - 1, c->x_hi, c->x_hi + 1, c->grid.dims[0]};
         uint32_t st[7];

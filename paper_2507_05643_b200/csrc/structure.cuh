@@ -161,6 +161,72 @@ __global__ void k_check_plane(const float4* __restrict__ P, const uint32_t* __re
   if (!(f == (float)plane)) latch_error(err, -2 /*CRM_E_DOMAIN*/, (long long)ids[s], step, 1);
 }
 
+// Slab rebuild, one pass over the local particles (replaces a first sort): last step's ghosts are
+// marked dropped; an owned particle now in the neighbour's first plane is an emigrant — its state goes
+// to that neighbour (segment E of the pack buffer of that side) and this rank keeps it as a ghost;
+// an owned particle in this slab's first / last plane is copied to the left / right pack buffer
+// (segment G: the neighbour's ghost plane).  Order inside a segment is arbitrary: the receiver sorts
+// by (cell, id).  A particle that crossed more than one plane latches CRM_E_DOMAIN (aux 1).
+struct SlabPack {
+  float4 *P[2], *L[2], *U[2], *S1[2];
+  float2* S2[2];
+  uint32_t* id[2];
+  uint32_t* cnt;      // [E_left, G_left, E_right, G_right]
+  uint32_t cap_e, cap_g;
+};
+__device__ __forceinline__ void slab_put(const SlabPack& pk, int d, uint32_t slot, const float4& p, const float4& l,
+                                         const float4& u, const float4& s1, const float2& s2, uint32_t id) {
+  pk.P[d][slot] = p; pk.L[d][slot] = l; pk.U[d][slot] = u; pk.S1[d][slot] = s1; pk.S2[d][slot] = s2;
+  pk.id[d][slot] = id;
+}
+__global__ void k_slab_pack(int n, const float4* __restrict__ P, const float4* __restrict__ L, float4* __restrict__ U,
+                            const float4* __restrict__ S1, const float2* __restrict__ S2,
+                            const uint32_t* __restrict__ ids, Grid g, int x_lo, int x_hi, int has_l, int has_r,
+                            SlabPack pk, ErrLatch* err, long long step) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float4 u = U[i];
+  const uint32_t tag = tag_of(u.w);
+  if (tag & TAG_GHOST) {   // last step's ghost: leaves at this rebuild
+    U[i].w = __uint_as_float(tag | TAG_DROP);
+    return;
+  }
+  const float4 p = P[i];
+  const int pl = (int)b1_floor(p.x, g.lo[0], g.s);
+  const bool emi_l = pl < x_lo, emi_r = pl >= x_hi;
+  if ((emi_l && (pl != x_lo - 1 || !has_l)) || (emi_r && (pl != x_hi || !has_r))) {
+    latch_error(err, -2 /*CRM_E_DOMAIN*/, (long long)ids[i], step, 1);
+    return;
+  }
+  const bool g_l = has_l && pl == x_lo, g_r = has_r && pl == x_hi - 1;
+  if (!(emi_l || emi_r || g_l || g_r)) return;
+  const float4 l = L[i], s1 = S1[i];
+  const float2 s2 = S2[i];
+  const uint32_t id = ids[i];
+  if (emi_l || emi_r) {
+    const int d = emi_l ? 0 : 1;
+    const uint32_t k = atomicAdd(&pk.cnt[2 * d], 1u);
+    if (k < pk.cap_e) slab_put(pk, d, k, p, l, u, s1, s2, id);   // (overflow: the host checks the count)
+    U[i].w = __uint_as_float(tag | TAG_GHOST);   // kept here as a ghost of the neighbour's first plane
+    return;
+  }
+  if (g_l) {
+    const uint32_t k = atomicAdd(&pk.cnt[1], 1u);
+    if (k < pk.cap_g) slab_put(pk, 0, pk.cap_e + k, p, l, u, s1, s2, id);
+  }
+  if (g_r) {
+    const uint32_t k = atomicAdd(&pk.cnt[3], 1u);
+    if (k < pk.cap_g) slab_put(pk, 1, pk.cap_e + k, p, l, u, s1, s2, id);
+  }
+}
+
+// slot_of_id entries of the particles of the old sorted set: invalid before the reorder writes the new
+// set (O(local) instead of a fill over every id of the global input)
+__global__ void k_clear_slots(int n, const uint32_t* __restrict__ ids, uint32_t* __restrict__ slot_of_id) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) slot_of_id[ids[i]] = 0xffffffffu;
+}
+
 // sum of |P(i)| over owned fluid particles (the directed pairs of the rates loops)
 __global__ void k_pair_count(int n, const float4* __restrict__ U, const uint32_t* __restrict__ count_all,
                              unsigned long long* __restrict__ out) {
