@@ -295,7 +295,13 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    nccl_log = None
     if world > 1:
+        # NCCL's INFO lines (communicator size, transports, NVLS) go to a per-rank file: rank 0 reports
+        # its communicator lines in the JSON so the scaling run can be checked against the rank count
+        nccl_log = f"/tmp/crm_nccl.{rank}.{os.getpid()}.log"
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_FILE", nccl_log)
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl")
@@ -509,6 +515,10 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = oracle_rate(args.config, 12)
 
+    nccl_info = None
+    if nccl_log and os.path.exists(nccl_log):
+        keys = ("nRanks", "nranks", "Init COMPLETE", "NVLS", "Channel 00")
+        nccl_info = [ln.strip()[:200] for ln in open(nccl_log, errors="replace") if any(k in ln for k in keys)][:8]
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
@@ -521,7 +531,7 @@ def main():
                            "parallelism": f"x-slabs x{world}, NCCL ghost planes" if world > 1 else "single GPU"},
                 "roofline": roof, "hbm_roofline": hbm, "alu_roofline_step": alu_step, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clocks, "next_alg2": nxt, "next_active": nxt_active,
-                "next_cone": nxt_cone}
+                "next_cone": nxt_cone, "nccl_info": nccl_info}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()

@@ -397,6 +397,30 @@ def test_alg2_ps10_trajectory_and_rates(crm):
     assert np.abs(xg - xo).max() < 1e-3 * sc.params["d0"]
 
 
+def test_alg2_reuse_step_rates_match_oracle_at_1e4(crm):
+    """Alg. 2 at the 1e-4 rate bar: both sides rebuild at t = 10 from the GPU's state y_10
+    (identical lists), then at t = 11 — a reuse step on the stale t = 10 lists — the oracle gets the
+    GPU's u, rho, sigma of y_11 (positions kept: setting them would rebuild its lists), so both evaluate
+    the same stale pair set on the same fields."""
+    sc = workloads.rate_state_S0(workloads.block_settle())
+    sc.params["ps_freq"] = 10
+    g, o = both(crm, sc)
+    g.step(sc.dt, 10)
+    o.step(sc.dt, 10)                       # (its own trajectory; only the step counter matters)
+    o.set_state(0, *g.get_state())          # y_10 of the GPU; the oracle's lists are dropped
+    nf = sc.n_fluid
+    g.debug_arm(True)
+    for t in (10, 11):
+        if t == 11:
+            _, vel, rho, sig = g.get_state()
+            o.set_state(0, None, vel, rho, sig)
+        g.step(sc.dt, 1)                    # t = 10: rebuild, t = 11: reuse
+        o.step(sc.dt, 1)
+        for stage in (0, 1):
+            for a, b in zip(g.last_rates(stage), o.last_rates(stage)):
+                assert rel_linf(a[:nf], b[:nf]) <= 1e-4, (t, stage, rel_linf(a[:nf], b[:nf]))
+
+
 def test_cuda_graph_replay_bit_identical(crm):
     # the captured step (default) equals the kernel-by-kernel step, also across Alg. 2 rebuilds
     for ps in (1, 3):
