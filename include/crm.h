@@ -126,7 +126,9 @@ void crm_destroy(crm_t* ctx);
  * rho starts at rho0.  *first_id receives the id of the first one.  CRM_E_STATE after a step. */
 int  crm_add_fluid(crm_t* ctx, int64_t n, const double* pos, const double* vel, const double* sig6,
                    int64_t* first_id);
-/* Add a rigid body (returns its index in *body_id; body 0 exists already). */
+/* Add a rigid body (returns its index in *body_id; body 0 exists already).  At most 126 bodies besides
+   the walls (the body index shares the marker tag word with the position's compensation term);
+   more return CRM_E_INVALID. */
 int  crm_add_body(crm_t* ctx, const crm_body_t* body, int32_t* body_id);
 /* Append n BCE markers attached to `body`, given in world coordinates at the body's initial pose. */
 int  crm_add_bce(crm_t* ctx, int32_t body, int64_t n, const double* pos_world, int64_t* first_id);

@@ -15,23 +15,49 @@ namespace crmk {
 
 // tag word stored in U.w (bit pattern, not a float value)
 //   bit 0      : 1 = BCE marker, 0 = fluid
-//   bits 1..15 : body index (0 = static walls)
-//   bit 16     : 1 = the body moves (FREE or PRESCRIBED)
+//   bits 1..7  : body index (0 = static walls; at most 127 bodies)
+//   bit 8      : 1 = the body moves (FREE or PRESCRIBED)
 __host__ __device__ __forceinline__ uint32_t make_tag(uint32_t kind, uint32_t body, uint32_t moving) {
-  return (kind & 1u) | ((body & 0x7fffu) << 1) | ((moving & 1u) << 16);
+  return (kind & 1u) | ((body & 0x7fu) << 1) | ((moving & 1u) << 8);
 }
-//   bit 17     : ghost copy of a neighbour slab's particle (multi-GPU)
-//   bit 18     : dropped at the next sort (migrated to a neighbour slab)
-//   bit 19     : Extended-Active particle of Alg. 3 (reading A31): a neighbour only, state frozen
-constexpr uint32_t TAG_GHOST = 1u << 17;
-constexpr uint32_t TAG_DROP = 1u << 18;
-constexpr uint32_t TAG_FROZEN = 1u << 19;
+//   bit 9      : ghost copy of a neighbour slab's particle (multi-GPU)
+//   bit 10     : dropped at the next sort (migrated to a neighbour slab)
+//   bit 11     : Extended-Active particle of Alg. 3 (reading A31): a neighbour only, state frozen
+//   bits 12..29: the position's compensation term lo (x = hi + lo) quantised to 6
+//                signed bits per axis in units of |hi| 2^-29 (|lo| <= ulp(hi)/2 <= |hi| 2^-24, so
+//                the code spans it; resolution <= ulp(hi)/32).  The pair and BCE kernels read it from
+//                the staged window (no global lo loads); the integrator keeps the exact lo in L.
+//   bits 30,31 : 0 (the word is a finite float bit pattern)
+constexpr uint32_t TAG_GHOST = 1u << 9;
+constexpr uint32_t TAG_DROP = 1u << 10;
+constexpr uint32_t TAG_FROZEN = 1u << 11;
+constexpr uint32_t TAG_FLAGS = 0xfffu;   // everything but the quantised lo
 __device__ __forceinline__ uint32_t tag_of(float w) { return __float_as_uint(w); }
 __device__ __forceinline__ bool tag_is_bce(uint32_t t) { return t & 1u; }
-__device__ __forceinline__ uint32_t tag_body(uint32_t t) { return (t >> 1) & 0x7fffu; }
-__device__ __forceinline__ bool tag_moving(uint32_t t) { return (t >> 16) & 1u; }
+__device__ __forceinline__ uint32_t tag_body(uint32_t t) { return (t >> 1) & 0x7fu; }
+__device__ __forceinline__ bool tag_moving(uint32_t t) { return (t >> 8) & 1u; }
 __device__ __forceinline__ bool tag_ghost(uint32_t t) { return (t & TAG_GHOST) != 0u; }
 __device__ __forceinline__ bool tag_frozen(uint32_t t) { return (t & TAG_FROZEN) != 0u; }
+
+// quantised lo of one axis: 6-bit two's complement code of lo / (|hi| 2^-29)
+__host__ __device__ __forceinline__ uint32_t loq_code(float hi, float lo) {
+  const float unit = fabsf(hi) * 1.86264514923095703125e-9f;   // |hi| 2^-29
+#ifdef __CUDA_ARCH__
+  float q = unit > 0.f ? rintf(__fdividef(lo, unit)) : 0.f;   // (an encoding: the approximate quotient is fine)
+#else
+  float q = unit > 0.f ? rintf(lo / unit) : 0.f;
+#endif
+  q = fminf(fmaxf(q, -32.f), 31.f);
+  return (uint32_t)((int)q) & 63u;
+}
+__host__ __device__ __forceinline__ uint32_t tag_with_lo(uint32_t tag, float hx, float hy, float hz, float lx, float ly,
+                                                         float lz) {
+  return (tag & TAG_FLAGS) | (loq_code(hx, lx) << 12) | (loq_code(hy, ly) << 18) | (loq_code(hz, lz) << 24);
+}
+__device__ __forceinline__ float loq_value(uint32_t tag, int axis, float hi) {
+  const int q = ((int)(tag << (14 - 6 * axis))) >> 26;   // sign-extended bits 12 + 6 axis .. + 5
+  return (float)q * (fabsf(hi) * 1.86264514923095703125e-9f);
+}
 
 // fixed grid (reading A19); cells of size s = support*h
 struct Grid {

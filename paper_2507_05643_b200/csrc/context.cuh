@@ -238,6 +238,11 @@ inline float u2f(uint32_t u) {
   std::memcpy(&f, &u, 4);
   return f;
 }
+inline uint32_t f2u(float f) {
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  return u;
+}
 
 inline unsigned blocks(long long n, int bs) { return (unsigned)((n + bs - 1) / bs); }
 

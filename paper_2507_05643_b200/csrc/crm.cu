@@ -458,7 +458,7 @@ void issue_body_finish(crm_t* c) {
   if (c->n_moving_markers)
     launch(c, KID_MARKERS, k_markers_place, dim3(blocks(c->n_moving_markers, 128)), dim3(128), c->n_moving_markers,
            (const uint32_t*)c->d_moving_ids, (const float4*)c->d_xlocal, (const uint32_t*)c->slot_of_id,
-           (const Pose*)c->d_pose0, c->P[y], c->L[y], (const float4*)c->U[y]);
+           (const Pose*)c->d_pose0, c->P[y], c->L[y], c->U[y]);
 }
 
 int issue_step(crm_t* c, float dt, long long step) {
@@ -478,7 +478,7 @@ int issue_step(crm_t* c, float dt, long long step) {
   if (c->n_moving_markers)
     launch(c, KID_MARKERS, k_markers_place, dim3(blocks(c->n_moving_markers, 128)), dim3(128), c->n_moving_markers,
            (const uint32_t*)c->d_moving_ids, (const float4*)c->d_xlocal, (const uint32_t*)c->slot_of_id,
-           (const Pose*)c->d_posem, c->Pm, c->Lm, (const float4*)c->Um);
+           (const Pose*)c->d_posem, c->Pm, c->Lm, c->Um);
   issue_bce(c, 1, dt, step, 0);
   issue_rates(c, 1, dt, step);
   if (c->n_moving_bodies) {
@@ -796,8 +796,10 @@ int crm_add_fluid(crm_t* c, int64_t n, const double* pos, const double* vel, con
   for (int64_t k = 0; k < n; ++k) {
     c->hP.push_back(make_float4((float)pos[3 * k], (float)pos[3 * k + 1], (float)pos[3 * k + 2], (float)c->mat.rho0));
     c->hL.push_back(host_lo(pos + 3 * k));
-    c->hU.push_back(vel ?make_float4((float)vel[3 * k], (float)vel[3 * k + 1], (float)vel[3 * k + 2], tag)
-                        : make_float4(0.f, 0.f, 0.f, tag));
+    const float4 hp = c->hP.back(), hl = c->hL.back();
+    const float tg = u2f(tag_with_lo(f2u(tag), hp.x, hp.y, hp.z, hl.x, hl.y, hl.z));
+    c->hU.push_back(vel ? make_float4((float)vel[3 * k], (float)vel[3 * k + 1], (float)vel[3 * k + 2], tg)
+                        : make_float4(0.f, 0.f, 0.f, tg));
     if (sig6) {
       c->hS1.push_back(make_float4((float)sig6[6 * k], (float)sig6[6 * k + 1], (float)sig6[6 * k + 2], (float)sig6[6 * k + 3]));
       c->hS2.push_back(make_float2((float)sig6[6 * k + 4], (float)sig6[6 * k + 5]));
@@ -815,7 +817,7 @@ int crm_add_fluid(crm_t* c, int64_t n, const double* pos, const double* vel, con
 int crm_add_body(crm_t* c, const crm_body_t* b, int32_t* body_id) {
   if (!c || !b) return CRM_E_INVALID;
   if (c->committed) return fail(c, CRM_E_STATE, "crm_add_body after the state went to the device");
-  if (c->bodies.size() >= 0x7fff) return fail(c, CRM_E_INVALID, "too many bodies");
+  if (c->bodies.size() >= 0x7f) return fail(c, CRM_E_INVALID, "too many bodies (at most 126 besides the walls)");
   if (b->motion < 0 || b->motion > 2) return fail(c, CRM_E_INVALID, "bad motion");
   if (b->motion == CRM_BODY_FREE && !(b->mass > 0)) return fail(c, CRM_E_INVALID, "free body needs mass > 0");
   const double qn = std::sqrt(b->quat[0] * b->quat[0] + b->quat[1] * b->quat[1] + b->quat[2] * b->quat[2] + b->quat[3] * b->quat[3]);
@@ -844,7 +846,8 @@ int crm_add_bce(crm_t* c, int32_t body, int64_t n, const double* pos, int64_t* f
   for (int64_t k = 0; k < n; ++k) {
     c->hP.push_back(make_float4((float)pos[3 * k], (float)pos[3 * k + 1], (float)pos[3 * k + 2], (float)c->mat.rho0));
     c->hL.push_back(host_lo(pos + 3 * k));
-    c->hU.push_back(make_float4(0.f, 0.f, 0.f, tag));
+    const float4 hp = c->hP.back(), hl = c->hL.back();
+    c->hU.push_back(make_float4(0.f, 0.f, 0.f, u2f(tag_with_lo(f2u(tag), hp.x, hp.y, hp.z, hl.x, hl.y, hl.z))));
     c->hS1.push_back(make_float4(0.f, 0.f, 0.f, 0.f));
     c->hS2.push_back(make_float2(0.f, 0.f));
     c->hBody.push_back(body);

@@ -363,7 +363,7 @@ int slab_phase(crm_t* c, int k, float dt, long long step) {
           if (c->n_moving_markers)   // moving markers at the mid-step pose, before the y_mid halo
             launch(c, KID_MARKERS, k_markers_place, dim3(blocks(c->n_moving_markers, 128)), dim3(128),
                    c->n_moving_markers, (const uint32_t*)c->d_moving_ids, (const float4*)c->d_xlocal,
-                   (const uint32_t*)c->slot_of_id, (const Pose*)c->d_posem, c->Pm, c->Lm, (const float4*)c->Um);
+                   (const uint32_t*)c->slot_of_id, (const Pose*)c->d_posem, c->Pm, c->Lm, c->Um);
         }
       } else if (k == 6) {
         if (split) issue_rates_range(c, 0, dt, step, per_x, (ntx - 2) * per_x);

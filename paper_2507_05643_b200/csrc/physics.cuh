@@ -222,8 +222,10 @@ __global__ void k_set_state(long long first, long long count, const uint32_t* __
   if (tag_ghost(tag_of(u.w))) return;
   if (has_pos) {   // hi = fp32 rounding of x (what rules B1/B2 see), lo = the remainder
     p.x = (float)pos[3 * k]; p.y = (float)pos[3 * k + 1]; p.z = (float)pos[3 * k + 2];
-    L[s] = make_float4((float)(pos[3 * k] - (double)p.x), (float)(pos[3 * k + 1] - (double)p.y),
-                       (float)(pos[3 * k + 2] - (double)p.z), 0.f);
+    const float4 l = make_float4((float)(pos[3 * k] - (double)p.x), (float)(pos[3 * k + 1] - (double)p.y),
+                                 (float)(pos[3 * k + 2] - (double)p.z), 0.f);
+    L[s] = l;
+    u.w = __uint_as_float(tag_with_lo(tag_of(u.w), p.x, p.y, p.z, l.x, l.y, l.z));
   }
   if (has_rho && !tag_is_bce(tag_of(u.w))) p.w = (float)rho[k];
   if (has_vel) { u.x = (float)vel[3 * k]; u.y = (float)vel[3 * k + 1]; u.z = (float)vel[3 * k + 2]; }

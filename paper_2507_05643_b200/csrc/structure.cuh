@@ -33,7 +33,7 @@ __device__ __forceinline__ bool b2_pred(float xi, float yi, float zi, float xj, 
 __global__ void k_markers_place(int nm, const uint32_t* __restrict__ moving_ids,
                                 const float4* __restrict__ xlocal, const uint32_t* __restrict__ slot_of_id,
                                 const Pose* __restrict__ pose, float4* __restrict__ P, float4* __restrict__ L,
-                                const float4* __restrict__ U) {
+                                float4* __restrict__ U) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= nm) return;
   const uint32_t id = moving_ids[k];
@@ -48,6 +48,7 @@ __global__ void k_markers_place(int nm, const uint32_t* __restrict__ moving_ids,
   p.z = q.pos[2] + q.R[6] * xl.x + q.R[7] * xl.y + q.R[8] * xl.z;
   P[s] = p;
   L[s] = make_float4(0.f, 0.f, 0.f, 0.f);   // placed from the pose: no compensation term
+  U[s].w = __uint_as_float(tag_of(U[s].w) & TAG_FLAGS);
 }
 
 // hash + per-cell count; the error latch reports particles outside the grid.

@@ -32,7 +32,7 @@ __device__ __forceinline__ void load_all(const TileSmem& sm, const float4* __res
     p = win_P(sm, e); u = win_U(sm, e); s1 = win_S1(sm, e); s2 = win_S2(sm, e);
   } else {
     const uint32_t g = window_to_global(sm, e);
-    p = rel_pos(P[g], L[g], sm); u = U[g]; s1 = S1[g]; s2 = S2[g];
+    u = U[g]; p = rel_pos_q(P[g], tag_of(u.w), sm); s1 = S1[g]; s2 = S2[g];
   }
 }
 
@@ -46,7 +46,7 @@ __device__ __forceinline__ void load_rates(const TileSmem& sm, const float4* __r
     p = win_P(sm, e); u = win_U(sm, e); s1 = win_S1(sm, e); s2 = win_S2(sm, e);
   } else {
     const uint32_t g = window_to_global(sm, e);
-    p = rel_pos(P[g], L[g], sm); u = U[g]; s1 = S1[g]; s2 = S2[g];
+    u = U[g]; p = rel_pos_q(P[g], tag_of(u.w), sm); s1 = S1[g]; s2 = S2[g];
     p.w = signed_volume(p.w, u.w, m);
   }
 }
@@ -74,7 +74,7 @@ __device__ __forceinline__ void bce_tile(const Phys& ph, TileSmem& sm, const flo
       continue;
     }
     const float4 pabs = P[i];
-    const float4 pa = rel_pos(pabs, L[i], sm);
+    const float4 pa = rel_pos_q(pabs, tag, sm);
     const uint32_t nl = nlist[i];
     float ub[3] = {0.f, 0.f, 0.f}, ab[3] = {0.f, 0.f, 0.f};
     if (tag_moving(tag)) body_kinematics(pose[tag_body(tag)], pabs.x, pabs.y, pabs.z, ub, ab);
@@ -162,7 +162,7 @@ __global__ void TILE_BOUNDS
     tile_stage_cells(P, U, S1, S2, sm, klo, khi);
     tile_stage_wait();
     __syncthreads();
-    tile_relativize_cells(L, sm, klo, khi);
+    tile_relativize_cells(sm, klo, khi);
     __syncthreads();
     if (sm.staged) bce_tile<STAGE, KER, true>(ph, sm, P, L, U, S1, S2, list, nlist, pose, ls, dbg, dbg_on);
     else bce_tile<STAGE, KER, false>(ph, sm, P, L, U, S1, S2, list, nlist, pose, ls, dbg, dbg_on);
@@ -284,7 +284,7 @@ __device__ __forceinline__ void rates_tile(const Phys& ph, float dt, TileSmem& s
       }
       continue;
     }
-    const float4 pi = first ? rel_pos(pre.p, pre.l, sm) : rel_pos(P[i], L[i], sm);
+    const float4 pi = rel_pos_q(first ? pre.p : P[i], tag, sm);
     const uint32_t nl = first ? pre.nl : nlist[i];
     const uint4 c0 = first ? pre.c0 : reinterpret_cast<const uint4*>(list)[i];
     PairAcc A;
@@ -307,8 +307,8 @@ __device__ __forceinline__ void rates_tile(const Phys& ph, float dt, TileSmem& s
     }
     pair_loop<KER, STAGED>(A, ph, sm, P, L, U, S1, S2, list, i, ls, nl, c0, pi, ui, true, false);
     // own state for the epilogue, (re)loaded after the loop to keep registers free inside it
-    const float4 phi = P[i];
-    const float4 pli = L[i];
+    const float4 phi = first ? pre.p : P[i];
+    const float4 pli = first ? pre.l : L[i];
     const float4 si1 = S1[i];
     const float2 si2 = S2[i];
     const float rinv_i = 1.0f / pi.w;
@@ -355,7 +355,8 @@ __device__ __forceinline__ void rates_tile(const Phys& ph, float dt, TileSmem& s
       comp_add(hz, lz, hd * ui.z);
       YP[i] = make_float4(hx, hy, hz, phi.w + hd * drho);
       YL[i] = make_float4(lx, ly, lz, 0.f);
-      YU[i] = make_float4(ui.x + hd * a[0], ui.y + hd * a[1], ui.z + hd * a[2], ui.w);
+      YU[i] = make_float4(ui.x + hd * a[0], ui.y + hd * a[1], ui.z + hd * a[2],
+                          __uint_as_float(tag_with_lo(tag, hx, hy, hz, lx, ly, lz)));
       YS1[i] = make_float4(si1.x + hd * ds[0], si1.y + hd * ds[1], si1.z + hd * ds[2], si1.w + hd * ds[3]);
       YS2[i] = make_float2(si2.x + hd * ds[4], si2.y + hd * ds[5]);
     } else {
@@ -373,7 +374,8 @@ __device__ __forceinline__ void rates_tile(const Phys& ph, float dt, TileSmem& s
       comp_add(hy, ly, dt * ui.y);
       comp_add(hz, lz, dt * ui.z);
       const float4 pn = make_float4(hx, hy, hz, p0.w + dt * drho);
-      const float4 un = make_float4(u0.x + dt * a[0], u0.y + dt * a[1], u0.z + dt * a[2], u0.w);
+      const float4 un = make_float4(u0.x + dt * a[0], u0.y + dt * a[1], u0.z + dt * a[2],
+                                    __uint_as_float(tag_with_lo(tag_of(u0.w), hx, hy, hz, lx, ly, lz)));
       YP[i] = pn;
       YL[i] = make_float4(lx, ly, lz, 0.f);
       YU[i] = un;
@@ -423,15 +425,26 @@ __global__ void TILE_BOUNDS
   //  mbarrier byte count, ran 1.5 % slower — here and in round 1: the window's arrival rate, not the
   //  copy instructions, bounds the prologue)
   tile_stage(P, U, S1, S2, sm);
-  RelPre rp;
-  relativize_load(L, sm, rp);
+#ifndef CRM_LISTPF
+#define CRM_LISTPF 12
+#endif
+  // stage A reads lists the filter has just written (the filter's 6 GB of lists have left L2): chunks
+  // 1 .. CRM_LISTPF-1 of each thread's first particle are prefetched to L2 with the window copy
+  // (measured: k_rates_A 12.28 -> 11.79 ms with 11 chunks; 4: 12.11, 16: 11.85; stage B gains nothing)
+  if (STAGE == 0 && CRM_LISTPF > 1 && threadIdx.x < n_i) {
+    int q;
+    const uint32_t i0 = tile_particle(sm, threadIdx.x, q);
+#pragma unroll
+    for (int cc = 1; cc < CRM_LISTPF; ++cc)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const uint4*>(list) + (size_t)cc * ls.stride + i0));
+  }
   Prefetch pre;
   if (threadIdx.x < n_i) {
     int q;
     pre.i = tile_particle(sm, threadIdx.x, q);
     pre.u = U[pre.i];
     pre.p = P[pre.i];
-    pre.l = L[pre.i];
+    pre.l = L[pre.i];   // (for the epilogue's integrator: requested early, its latency hides in the prologue)
     pre.nl = nlist[pre.i];
     pre.c0 = reinterpret_cast<const uint4*>(list)[pre.i];
   }
@@ -463,7 +476,7 @@ __global__ void TILE_BOUNDS
   if (!any) return;
   __syncthreads();
   EXP_T(3)
-  relativize_apply<true>(sm, rp, ph.m);
+  relativize_apply<true>(sm, ph.m);
   __syncthreads();
   EXP_T(4)
   if (sm.staged)

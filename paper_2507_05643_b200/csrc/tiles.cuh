@@ -229,6 +229,12 @@ __device__ __forceinline__ void tile_stage_wait() { __pipeline_wait_prior(0); }
 __device__ __forceinline__ float4 rel_pos(const float4& hi, const float4& lo, const TileHead& sm) {
   return make_float4((hi.x - sm.ox) + lo.x, (hi.y - sm.oy) + lo.y, (hi.z - sm.oz) + lo.z, hi.w);
 }
+// the same with lo decoded from the quantised copy in the tag word (common.cuh): what the pair and
+// BCE kernels use, from the staged window, with no global lo loads
+__device__ __forceinline__ float4 rel_pos_q(const float4& hi, uint32_t tag, const TileHead& sm) {
+  return make_float4((hi.x - sm.ox) + loq_value(tag, 0, hi.x), (hi.y - sm.oy) + loq_value(tag, 1, hi.y),
+                     (hi.z - sm.oz) + loq_value(tag, 2, hi.z), hi.w);
+}
 
 // signed neighbour volume carried in the .w slot of a rates window: +m/rho for fluid, -m/rho for
 // markers (A7, A8: markers are ordinary neighbours with V = m/rho0; the sign lets the marker-load
@@ -238,68 +244,45 @@ __device__ __forceinline__ float signed_volume(float rho, float tagw, float m) {
   return tag_is_bce(tag_of(tagw)) ? -V : V;
 }
 
-// convert the staged window from absolute hi to relative compensated positions;
-// TO_V: the rates kernels also replace rho_j by the signed volume V_j (one division per staged
-// particle instead of one reciprocal per pair).  Split in two: relativize_load requests the lo parts
-// of the thread's window slots (registers) BEFORE the staging wait, relativize_apply converts after
-// it, so the global latency of lo hides behind the staging.
+#ifndef CRM_RELK_UNROLL
+#define CRM_RELK_UNROLL 1
+#endif
+// convert the staged window from absolute hi to relative compensated positions (lo from the staged
+// tag words: no global loads; measured: the per-slot lo loads of the previous design held every tile's
+// prologue ~1.2 ms per step); TO_V: the rates kernels also replace rho_j by the signed volume V_j (one
+// division per staged particle instead of one reciprocal per pair)
 constexpr int RELK = (WMAX + TILE_THREADS - 1) / TILE_THREADS;   // window slots per thread (blockDim == TILE_THREADS)
-struct RelPre {
-  float4 l[RELK];
-};
-__device__ __forceinline__ void relativize_load(const float4* __restrict__ L, const TileSmem& sm, RelPre& rp) {
-  if (!sm.staged) return;
-  const uint32_t W = sm.run_base[WR];
-#pragma unroll
-  for (int k = 0; k < RELK; ++k) {
-    const uint32_t idx = threadIdx.x + (uint32_t)k * blockDim.x;
-    if (idx < W) {
-      int r = 0;
-#pragma unroll
-      for (int step = WR / 2; step > 0; step >>= 1) r += (sm.run_base[r + step] <= idx) ? step : 0;
-      rp.l[k] = L[sm.run_start[r] + (idx - sm.run_base[r])];
-    }
-  }
-}
 template <bool TO_V>
-__device__ __forceinline__ void relativize_apply(TileSmem& sm, const RelPre& rp, float m) {
+__device__ __forceinline__ void relativize_apply(TileSmem& sm, float m) {
   if (!sm.staged) return;
   const uint32_t W = sm.run_base[WR];
+#if CRM_RELK_UNROLL
 #pragma unroll
   for (int k = 0; k < RELK; ++k) {
     const uint32_t idx = threadIdx.x + (uint32_t)k * blockDim.x;
     if (idx < W) {
-      float4 p = rel_pos(sm.P[idx], rp.l[k], sm);
-      if (TO_V) p.w = signed_volume(p.w, sm.U[idx].w, m);
+#else
+  for (uint32_t idx = threadIdx.x; idx < W; idx += blockDim.x) {
+    {
+#endif
+      const float tw = sm.U[idx].w;
+      float4 p = rel_pos_q(sm.P[idx], tag_of(tw), sm);
+      if (TO_V) p.w = signed_volume(p.w, tw, m);
       sm.P[idx] = p;
     }
   }
 }
 // the BCE kernels' variant (densities kept: the Adami stress needs rho_f) over the staged cells
 // klo..khi-1 of every run, one warp per run
-__device__ __forceinline__ void tile_relativize_cells(const float4* __restrict__ L, TileSmem& sm, int klo, int khi) {
+__device__ __forceinline__ void tile_relativize_cells(TileSmem& sm, int klo, int khi) {
   if (!sm.staged) return;
   const uint32_t lane = threadIdx.x & 31u, nw = blockDim.x >> 5;
   for (uint32_t r = threadIdx.x >> 5; r < (uint32_t)WR; r += nw) {
     const uint32_t rs = sm.run_start[r], rb = sm.run_base[r];
     const uint32_t b = rb + (sm.wcs[r][klo] - rs), e = rb + (sm.wcs[r][khi] - rs);
-    for (uint32_t idx = b + lane; idx < e; idx += 32) sm.P[idx] = rel_pos(sm.P[idx], L[rs + (idx - rb)], sm);
+    for (uint32_t idx = b + lane; idx < e; idx += 32) sm.P[idx] = rel_pos_q(sm.P[idx], tag_of(sm.U[idx].w), sm);
   }
 }
-// (whole-window single pass)
-__device__ __forceinline__ void tile_relativize(const float4* __restrict__ L, TileSmem& sm) {
-  if (!sm.staged) return;
-  // a flat element loop (balanced over the threads, unlike one warp per run); the run of an
-  // element by binary search over the 16 run bases
-  const uint32_t W = sm.run_base[WR];
-  for (uint32_t idx = threadIdx.x; idx < W; idx += blockDim.x) {
-    int r = 0;
-#pragma unroll
-    for (int step = WR / 2; step > 0; step >>= 1) r += (sm.run_base[r + step] <= idx) ? step : 0;
-    sm.P[idx] = rel_pos(sm.P[idx], L[sm.run_start[r] + (idx - sm.run_base[r])], sm);
-  }
-}
-
 // staged window entries by list entry (byte offset of the float4 slot)
 __device__ __forceinline__ float4 win_P(const TileSmem& sm, uint32_t e) {
   return *reinterpret_cast<const float4*>(reinterpret_cast<const char*>(sm.P) + e);
