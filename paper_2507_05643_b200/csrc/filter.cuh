@@ -428,9 +428,21 @@ __device__ __forceinline__ int filter_tile(const Grid& g, FilterSmem& sm, const 
     const uint32_t i = tile_particle(sm, t, q);
     const int r_self = (1 + q / TY) * WRY + (1 + q % TY);
     const uint32_t self = sm.run_base[r_self] + (i - sm.run_start[r_self]);
-    const int cz = (int)(cell_of[i] % (uint32_t)g.dims[2]);
+    // the particle's cell row and kind from the tile geometry and the staged window (no global
+    // loads on the per-particle path when staged): cz = the cell of the own run holding slot i
+    int cz;
+    bool bce;
+    if (STAGED) {
+      int k = 0;
+#pragma unroll
+      for (int kk = 1; kk < TZ + 2; ++kk) k += (kk <= sm.zhi - sm.zlo && sm.wcs[r_self][kk] <= i) ? 1 : 0;
+      cz = sm.zlo + k;
+      bce = sm.bce[self] != 0;
+    } else {
+      cz = (int)(cell_of[i] % (uint32_t)g.dims[2]);
+      bce = tag_is_bce(tag_of(U[i].w));
+    }
     const float4 pi = STAGED ? make_float4(sm.X[self], sm.Y[self], sm.Z[self], 0.f) : P[i];
-    const bool bce = tag_is_bce(tag_of(U[i].w));
     has_marker |= bce ? 1 : 0;
     if (bce) {
       atomicMin(const_cast<int*>(&sm.mzmin), cz);
