@@ -152,6 +152,26 @@ def test_more_than_64_bodies_are_posed(crm):
     assert np.abs(x - expect).max() < 1e-6
 
 
+def test_body_count_limit(crm):
+    """The body index has 7 bits of the marker tag (the rest holds the flags and the quantised
+    position compensation): 126 bodies besides the walls are accepted, the next one is
+    refused with CRM_E_INVALID; the last body's markers follow it."""
+    p = _params((0.0, 0.0, 0.0), (1.0, 1.0, 0.2), gravity=(0.0, 0.0, 0.0))
+    g = crm.Crm(p)
+    g.add_fluid(np.array([[0.9, 0.9, 0.1]]))
+    for b in range(126):
+        x0 = (0.02 + 0.006 * b, 0.05, 0.1)
+        bid = g.add_body(Body(mass=1.0, inertia=(1, 1, 1), pos=x0, vel=(0.0, 0.01, 0.0), motion=BODY_PRESCRIBED))
+        assert bid == b + 1
+    g.add_bce(126, np.array([[0.02 + 0.006 * 125, 0.05, 0.12]]))
+    with pytest.raises(crm.CrmError) as e:
+        g.add_body(Body(mass=1.0, inertia=(1, 1, 1), pos=(0.5, 0.5, 0.1), motion=BODY_PRESCRIBED))
+    assert e.value.code == crm.CRM_E_INVALID
+    g.step(1e-3, 10)
+    x = g.get_state()[0][1]
+    assert np.abs(x - np.array([0.02 + 0.006 * 125, 0.05 + 10 * 1e-3 * 0.01, 0.12])).max() < 1e-6
+
+
 def test_error_latch_names_the_failing_step_and_stops(crm):
     """S:147 / S:318: a particle leaving the grid box is reported with the step in which it left,
     also from a replayed CUDA graph, and the later steps of the call compute nothing."""
