@@ -112,16 +112,16 @@ __device__ __forceinline__ float kernel_W(float r, const Phys& ph) {
   }
 }
 
-// W'(r)/r of the selected kernel, 0 < r < 2h; rinv = 1/r
+// W'(r)/r of the selected kernel, r > 0 (0 from 2h on); rinv = 1/r
 template <int KER>
 __device__ __forceinline__ float kernel_F(float r, float rinv, const Phys& ph) {
   if (KER == KER_WENDLAND) {
-    const float t = fmaf(-0.5f * ph.hinv, r, 1.0f);
+    const float t = fmaxf(fmaf(-0.5f * ph.hinv, r, 1.0f), 0.0f);   // 0 beyond 2h (A17)
     return ph.wd_f * t * t * t;
   } else {
     // cubic spline (A1): kin_a r + kin_b for r < h, kout (2 - r/h)^2 / r otherwise; both pieces
     // are evaluated and selected (no branch: the pair loops stay straight-line code)
-    const float t = fmaf(-ph.hinv, r, 2.0f);
+    const float t = fmaxf(fmaf(-ph.hinv, r, 2.0f), 0.0f);   // 0 beyond 2h (A17)
     const float f_in = fmaf(ph.kin_a, r, ph.kin_b);
     const float f_out = (ph.kout * rinv) * (t * t);
     return (r < ph.h) ? f_in : f_out;

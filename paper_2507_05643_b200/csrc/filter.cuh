@@ -36,7 +36,8 @@ struct FilterSmem : TileHead {
   float Z[WMAX + 40];
   alignas(4) uint8_t bce[WMAX + 40];    // 1 = BCE marker
   // each thread's hit masks (word-major: thread t's word w at [w][t], bank = t) and the window
-  // offset of each mask's bit 0; drained into the list once the particle's sweep is complete
+  // offset of each mask's bit 0 (group-major path: its byte offset, 16 x the slot, as the list entry
+  // needs it); drained into the list once the particle's sweep is complete
   uint32_t mw[FMW][FILTER_THREADS];
   uint16_t wb[FMW][FILTER_THREADS];
   uint2 pmask[33];   // group-major path: gm_prefix_mask(x) for x = 0..32
@@ -234,7 +235,7 @@ __device__ __forceinline__ void gm_drain(FilterSmem& sm, GmState& st, uint32_t g
     W = adv ? Wn : W;
     const uint32_t q = (__ffs(W) - 1) & 31u;   // bit q: chunk 8 wd + (q >> 2), candidate 8 (q & 3) + g of it
     W &= W - 1;
-    return (sm.wb[8 * wd + (q >> 2)][t] + 8u * (q & 3u) + g) << 4;
+    return sm.wb[8 * wd + (q >> 2)][t] + ((q & 3u) << 7) + (g << 4);   // wb holds 16 x the chunk base
   };
   if (final && w.k == 0 && (int)st.nent <= w.cap) {
     // the whole list at once (no early drain): whole chunks of 8 entries, one 16-B store each, the
@@ -242,7 +243,17 @@ __device__ __forceinline__ void gm_drain(FilterSmem& sm, GmState& st, uint32_t g
     // warp, so the chunk's register positions are compile-time
     uint4* row = reinterpret_cast<uint4*>(w.cur);
     const uint32_t nchk = max(1u, (st.nent + 7u) >> 3);
-    for (uint32_t c = 0; c < nchk; ++c) {
+    // whole chunks without the tail select, then the last (padded) chunk (with the pre-scaled chunk
+    // bases: k_filter 13.15 -> 12.74 ms)
+    for (uint32_t c = 0; c + 1 < nchk; ++c) {
+      uint32_t v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = next();
+      row[(size_t)c * w.stride] = make_uint4(v[0] | (v[1] << 16), v[2] | (v[3] << 16), v[4] | (v[5] << 16),
+                                             v[6] | (v[7] << 16));
+    }
+    {
+      const uint32_t c = nchk - 1;
       uint32_t v[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
@@ -266,7 +277,7 @@ __device__ __forceinline__ void gm_store_chunk(FilterSmem& sm, GmState& st, uint
                                                uint32_t g0, ListWriter& w) {
   if (st.nch == FMW) gm_drain(sm, st, g0, w, 0u, false);   // all mask slots used: append what they hold now
   const uint32_t t = threadIdx.x;
-  sm.wb[st.nch][t] = (uint16_t)base;
+  sm.wb[st.nch][t] = (uint16_t)(base << 4);   // staged windows: base < 4096
   st.nent += __popc(a) + __popc(b);
   if (st.nch & 1) {
     const int p = st.nch >> 1;

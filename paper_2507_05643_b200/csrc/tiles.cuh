@@ -70,9 +70,10 @@ __device__ __forceinline__ uint32_t cell_id(const Grid& g, int cx, int cy, int c
 __device__ __forceinline__ TileGeom tile_geom(const Grid& g, long long t) {
   const int ntz = tiles_z(g), nty = tiles_y(g);
   TileGeom G;
-  const int tz = (int)(t % ntz);
-  const int ty = (int)((t / ntz) % nty);
-  const int tx = (int)(t / ((long long)ntz * nty));
+  const uint32_t t32 = (uint32_t)t, tq = t32 / (uint32_t)ntz;   // tile indices < 2^32
+  const int tz = (int)(t32 - tq * (uint32_t)ntz);
+  const int tx = (int)(tq / (uint32_t)nty);
+  const int ty = (int)(tq - (uint32_t)tx * (uint32_t)nty);
   G.X0 = tx * TX;
   G.Y0 = ty * TY;
   G.z0 = tz * TZ;
