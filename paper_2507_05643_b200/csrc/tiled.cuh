@@ -185,9 +185,9 @@ struct Prefetch {
 // One directed pair (i, j).  pj.w = signed V_j (+ fluid, - marker).  Branch-free, no mask: beyond 2h
 // (A17) kernel_F is 0 (clamped), so w = 0; at r = 0 (the self padding, A18) r is lifted to 1e-15 and
 // every term carries x_ij = 0; a marker when only fluid counts gets w = 0 — a zero contribution to
-// every sum.  The AV term reuses V_j grad W (Pi += c (v.r)/den g).  Two MUFU per pair (rsqrt, one
-// reciprocal for the AV).  (measured: the mask compares, the AV product and 64-bit tile divisions
-// removed, k_rates_A/B 11.79/11.42 -> 11.60/11.20 ms)
+// every sum.  The AV term reuses V_j grad W (Pi += (v.r)/den g; the constant c_av multiplies the
+// sum in the epilogue).  Two MUFU per pair (rsqrt, one reciprocal for the AV).  (measured: the mask
+// compares, the AV products and 64-bit tile divisions removed, k_rates_A/B 11.79/11.42 -> 11.51/11.14 ms)
 template <int KER>
 __device__ __forceinline__ void pair_terms(PairAcc& A, const Phys& ph, const float4& pi, const float4& ui,
                                            const float4& pj, const float4& uj, const float4& sj1, const float2& sj2,
@@ -218,7 +218,7 @@ __device__ __forceinline__ void pair_terms(PairAcc& A, const Phys& ph, const flo
   // and rho_j = m / V_j:  m / rho_bar = 2 m V_j / (rho_i V_j + m)  (c_av holds 2 m gamma_a h c_s)
   const float vr = -fmaf(duz, dz, fmaf(duy, dy, dux * dx));
   const float den = fmaf(pi.w, Vj, ph.m) * (r2 + ph.xi2);
-  const float cv = (ph.c_av * vr) * rcp_approx(den);
+  const float cv = vr * rcp_approx(den);   // c_av applied once in the epilogue
   const float coef = (!ph.unilateral || vr < 0.f) ? cv : 0.f;
   A.Pi[0] = fmaf(coef, gx, A.Pi[0]); A.Pi[1] = fmaf(coef, gy, A.Pi[1]); A.Pi[2] = fmaf(coef, gz, A.Pi[2]);
 }
@@ -303,9 +303,9 @@ __device__ __forceinline__ void rates_tile(const Phys& ph, float dt, TileSmem& s
       const float2 si2 = S2[i];
       const float rinv_i = 1.0f / pi.w;
       float a[3];
-      a[0] = (si1.x * A.Gs[0] + si1.w * A.Gs[1] + si2.x * A.Gs[2] + A.Ms[0]) * rinv_i + A.Pi[0];
-      a[1] = (si1.w * A.Gs[0] + si1.y * A.Gs[1] + si2.y * A.Gs[2] + A.Ms[1]) * rinv_i + A.Pi[1];
-      a[2] = (si2.x * A.Gs[0] + si2.y * A.Gs[1] + si1.z * A.Gs[2] + A.Ms[2]) * rinv_i + A.Pi[2];
+      a[0] = (si1.x * A.Gs[0] + si1.w * A.Gs[1] + si2.x * A.Gs[2] + A.Ms[0]) * rinv_i + ph.c_av * A.Pi[0];
+      a[1] = (si1.w * A.Gs[0] + si1.y * A.Gs[1] + si2.y * A.Gs[2] + A.Ms[1]) * rinv_i + ph.c_av * A.Pi[1];
+      a[2] = (si2.x * A.Gs[0] + si2.y * A.Gs[1] + si1.z * A.Gs[2] + A.Ms[2]) * rinv_i + ph.c_av * A.Pi[2];
       macc[i] = make_float4(ph.m * a[0], ph.m * a[1], ph.m * a[2], 0.f);
       if (dbg_on) dbg.acc[1][i] = make_float4(a[0], a[1], a[2], 0.f);
       continue;
@@ -318,9 +318,9 @@ __device__ __forceinline__ void rates_tile(const Phys& ph, float dt, TileSmem& s
     const float2 si2 = S2[i];
     const float rinv_i = 1.0f / pi.w;
     float a[3];
-    a[0] = (si1.x * A.Gs[0] + si1.w * A.Gs[1] + si2.x * A.Gs[2] + A.Ms[0]) * rinv_i + A.Pi[0] + ph.g[0];
-    a[1] = (si1.w * A.Gs[0] + si1.y * A.Gs[1] + si2.y * A.Gs[2] + A.Ms[1]) * rinv_i + A.Pi[1] + ph.g[1];
-    a[2] = (si2.x * A.Gs[0] + si2.y * A.Gs[1] + si1.z * A.Gs[2] + A.Ms[2]) * rinv_i + A.Pi[2] + ph.g[2];
+    a[0] = (si1.x * A.Gs[0] + si1.w * A.Gs[1] + si2.x * A.Gs[2] + A.Ms[0]) * rinv_i + ph.c_av * A.Pi[0] + ph.g[0];
+    a[1] = (si1.w * A.Gs[0] + si1.y * A.Gs[1] + si2.y * A.Gs[2] + A.Ms[1]) * rinv_i + ph.c_av * A.Pi[1] + ph.g[1];
+    a[2] = (si2.x * A.Gs[0] + si2.y * A.Gs[1] + si1.z * A.Gs[2] + A.Ms[2]) * rinv_i + ph.c_av * A.Pi[2] + ph.g[2];
     // continuity (Eq. continuity_dis): drho = -rho_i sum (u_j - u_i) . gradW V_j = -rho_i tr L
     const float drho = -pi.w * (A.L[0] + A.L[4] + A.L[8]);
     // Jaumann stress rate (Eq. stress_rate with Eq. 3; readings A4–A6)
