@@ -65,6 +65,7 @@ extern "C" {
 #define CRM_BCE               1
 #define CRM_ALL               2
 #define CRM_OWNED             3
+#define CRM_GRAPH_REPLAYS     4   /* crm_count: steps of this context replayed from a captured CUDA graph */
 
 typedef struct crm crm_t;   /* opaque; owned by the library */
 
@@ -196,7 +197,7 @@ int  crm_set_state(crm_t* ctx, int64_t first_id, int64_t count, const double* po
                    const double* rho, const double* sig6);
 /* Body pose/velocity and the force/torque of the last step (about the centre of mass). */
 int  crm_get_body(crm_t* ctx, int32_t body, crm_body_t* state, double force[3], double torque[3]);
-int64_t crm_count(const crm_t* ctx, int which /* CRM_FLUID | CRM_BCE | CRM_ALL | CRM_OWNED */);
+int64_t crm_count(const crm_t* ctx, int which /* CRM_FLUID | CRM_BCE | CRM_ALL | CRM_OWNED | CRM_GRAPH_REPLAYS */);
 const char* crm_last_error(const crm_t* ctx);
 const char* crm_strerror(int code);
 

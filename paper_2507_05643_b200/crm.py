@@ -17,7 +17,7 @@ LIB_PATH = os.environ.get("CRM_LIB") or os.path.join(_HERE, "libcrm.so")
 
 CRM_OK, CRM_E_INVALID, CRM_E_DOMAIN, CRM_E_NONFINITE, CRM_E_UNSUPPORTED = 0, -1, -2, -3, -4
 CRM_E_STATE, CRM_E_OOM, CRM_E_CUDA, CRM_E_COMM, CRM_E_CAPACITY = -5, -6, -7, -8, -9
-CRM_FLUID, CRM_BCE, CRM_ALL, CRM_OWNED = 0, 1, 2, 3
+CRM_FLUID, CRM_BCE, CRM_ALL, CRM_OWNED, CRM_GRAPH_REPLAYS = 0, 1, 2, 3, 4
 
 # every symbol include/crm.h declares (checked by tests/test_abi.py)
 EXPORTS = [

@@ -30,7 +30,8 @@ __global__ void k_activity(int n, const float4* __restrict__ P, const float4* __
                            float4* __restrict__ U, const uint32_t* __restrict__ ids,
                            const BodyState* __restrict__ bodies, const ActiveBox* __restrict__ boxes, int nbox,
                            double radius, uint8_t* __restrict__ act_slot, uint8_t* __restrict__ act_id,
-                           unsigned long long* __restrict__ counts) {
+                           unsigned long long* __restrict__ counts, const uint32_t* __restrict__ dn) {
+  if (dn) n = (int)*dn;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   int f = 3;   // no particle (tail lanes)
   if (i < n) {

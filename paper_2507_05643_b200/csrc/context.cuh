@@ -117,6 +117,10 @@ struct crm {
   double dt_d = 0.0;                    // the step of the current crm_step call (fp64: body updates)
   int gcur_after[2][2] = {{0, 0}, {0, 0}};
   int64_t gkernels[2][2] = {{0, 0}, {0, 0}};
+  cudaGraphExec_t ggroup[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};   // rank 0 of an in-process slab group
+  std::vector<crm_t*> gmembers;         // the contexts the group graphs were captured with
+  bool slab_graph_off = false;
+  int64_t graph_replays = 0;            // steps replayed from a captured graph (crm_count CRM_GRAPH_REPLAYS)          // a slab-step capture failed once: eager launches from then on
   int ps_freq = 1;                      // Alg. 2: lists rebuilt when step % ps_freq == 0
   bool lists_valid = false;             // the stored lists/sort match the current slots
   int list_order = 1;                   // stored list order: 1 bank-group-major (filter.cuh), 0 candidate order
@@ -137,7 +141,9 @@ struct crm {
   uint32_t s_lom1 = 0, s_hip1 = 0;                     // starts of planes x_lo-1 and x_hi+1 (ghost ranges)
   uint32_t pk_n[4] = {0, 0, 0, 0};     // packed at this rebuild: E_left, G_left, E_right, G_right
   uint32_t rv_n[4] = {0, 0, 0, 0};     // received: E / G from the left, E / G from the right
-  SlabPack pk{};                       // pack buffers of the slab rebuild (structure.cuh k_slab_pack)
+  SlabPack pk{};                       // pack buffers of the slab rebuild (structure.cuh k_slab_pack) and halos
+  SlabPack rv{};                       // receive buffers (the neighbours' pk, whole: fixed-capacity transfers)
+  uint32_t* d_slab = nullptr;          // device: [0] local count, [1..4] appended segment starts, [5..8] their sizes
 
   // active domains (Alg. 3): boxes per body, the active-set capacity of
   // the arrays indexed by sorted slot (lists, mid state, marker loads) and its ManageArrayMemory policy

@@ -111,14 +111,24 @@ int commit(crm_t* c) {
       for (int64_t i = 0; i < c->n; ++i) cnt[host_plane(c->grid, c->hP[i].x)]++;
       for (int64_t v : cnt) maxp = std::max(maxp, v);
     }
-    c->pk.cap_e = (uint32_t)(maxp + 1024);
-    c->pk.cap_g = (uint32_t)(2 * maxp + 1024);
+    // (fixed-size transfers: the emigrants of one rebuild are a fraction of a plane; the boundary plane
+    //  may densify by a quarter before CRM_E_CAPACITY is latched)
+    c->pk.cap_e = (uint32_t)(maxp / 2 + 1024);
+    c->pk.cap_g = (uint32_t)(maxp + maxp / 4 + 1024);
     const size_t pc = (size_t)c->pk.cap_e + c->pk.cap_g;
     for (int d = 0; d < 2; ++d) {
       r |= dalloc(c, &c->pk.P[d], pc); r |= dalloc(c, &c->pk.L[d], pc); r |= dalloc(c, &c->pk.U[d], pc);
       r |= dalloc(c, &c->pk.S1[d], pc); r |= dalloc(c, &c->pk.S2[d], pc); r |= dalloc(c, &c->pk.id[d], pc);
     }
     r |= dalloc(c, &c->pk.cnt, 4);
+    c->rv.cap_e = c->pk.cap_e;
+    c->rv.cap_g = c->pk.cap_g;
+    for (int d = 0; d < 2; ++d) {
+      r |= dalloc(c, &c->rv.P[d], pc); r |= dalloc(c, &c->rv.L[d], pc); r |= dalloc(c, &c->rv.U[d], pc);
+      r |= dalloc(c, &c->rv.S1[d], pc); r |= dalloc(c, &c->rv.S2[d], pc); r |= dalloc(c, &c->rv.id[d], pc);
+    }
+    r |= dalloc(c, &c->rv.cnt, 4);
+    r |= dalloc(c, &c->d_slab, 16);
   }
   c->acap = (int64_t)n;
   if (!c->boxes.empty()) {   // active domains (Alg. 3)
@@ -214,6 +224,8 @@ int commit(crm_t* c) {
     for (size_t k = 0; k < nl; ++k) slots[owned[k]] = (uint32_t)k;
     CK(cudaMemcpyAsync(c->slot_of_id, slots.data(), (size_t)c->n * 4, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->ids[0], idv.data(), nl * 4, cudaMemcpyHostToDevice, c->stream));
+    c->h_pin[40] = (uint32_t)nl;   // the device's local count (the slab step keeps it on the device)
+    CK(cudaMemcpyAsync(c->d_slab, c->h_pin + 40, 4, cudaMemcpyHostToDevice, c->stream));
     CK(cudaStreamSynchronize(c->stream));
   } else {
     for (size_t i = 0; i < nl; ++i) idv[i] = (uint32_t)i;
@@ -259,7 +271,9 @@ namespace {
 // matches drop_mask leave the local set.  With active domains (Alg. 3) past t_delay, UpdateActivity
 // runs first and Inactive particles go behind the active set, frozen.
 void issue_sort(crm_t* c, long long step, uint32_t drop_mask) {
-  const int n = (int)c->nl;
+  // slabs: the local count is the device word d_slab[0] (kernels read it; grids span the capacity)
+  const uint32_t* dn = c->slab ? (const uint32_t*)c->d_slab : nullptr;
+  const int n = (int)(c->slab ? c->ncap : c->nl);
   const int a = c->cur, b = 1 - c->cur;
   const bool act = !c->boxes.empty() && c->t_now > c->t_delay;   // Alg. 3: "if t > t_delay"
   c->active_on = act;
@@ -269,11 +283,11 @@ void issue_sort(crm_t* c, long long step, uint32_t drop_mask) {
     launch(c, KID_ACTIVITY, k_activity, dim3(blocks(n, 256)), dim3(256), n, (const float4*)c->P[a],
            (const float4*)c->L[a], c->U[a], (const uint32_t*)c->ids[a], (const BodyState*)c->d_bodies,
            (const ActiveBox*)c->d_boxes, (int)c->boxes.size(), c->support * (double)c->ker.h, c->d_act, c->d_act_id,
-           c->d_actcnt);
+           c->d_actcnt, dn);
   }
   launch(c, KID_BIN, k_bin, dim3(blocks(n, 256)), dim3(256), n, (const float4*)c->P[a], (const float4*)c->U[a],
          (const uint32_t*)c->ids[a], c->grid, drop_mask, (const uint8_t*)(act ? c->d_act : nullptr), c->key,
-         c->arrival, c->cell_count, c->d_err, step);
+         c->arrival, c->cell_count, c->d_err, step, dn);
   scan_u32(c, c->cell_count, c->cell_start, (long long)c->grid.M + 1, 0);
   if (act) {   // the tiles the step's kernels run on, and the counts the host sizes arrays from
     cudaMemsetAsync(c->d_tile_cnt, 0, 4, c->stream);
@@ -284,14 +298,14 @@ void issue_sort(crm_t* c, long long step, uint32_t drop_mask) {
     cudaMemcpyAsync(c->h_pin + 8, c->d_actcnt, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream);
   }
   launch(c, KID_SCATTER, k_scatter, dim3(blocks(n, 256)), dim3(256), n, (const uint32_t*)c->key,
-         (const uint32_t*)c->arrival, (const uint32_t*)c->cell_start, (const uint32_t*)c->ids[a], c->tmp_src, c->tmp_id);
+         (const uint32_t*)c->arrival, (const uint32_t*)c->cell_start, (const uint32_t*)c->ids[a], c->tmp_src, c->tmp_id, dn);
   if (c->slab && n)
-    launch(c, KID_SLAB, k_clear_slots, dim3(blocks(n, 256)), dim3(256), n, (const uint32_t*)c->ids[a], c->slot_of_id);
+    launch(c, KID_SLAB, k_clear_slots, dim3(blocks(n, 256)), dim3(256), n, (const uint32_t*)c->ids[a], c->slot_of_id, dn);
   launch(c, KID_REORDER, k_reorder, dim3(blocks(n, 256)), dim3(256), n, (const uint32_t*)c->tmp_src,
          (const uint32_t*)c->tmp_id, (const uint32_t*)c->key, (const uint32_t*)c->cell_start,
          (const float4*)c->P[a], (const float4*)c->L[a], (const float4*)c->U[a], (const float4*)c->S1[a],
          (const float2*)c->S2[a], c->P[b], c->L[b], c->U[b], c->S1[b], c->S2[b], c->ids[b], c->cell_of, c->slot_of_id,
-         c->grid.M, act ? 1 : 0);
+         c->grid.M, act ? 1 : 0, dn);
   c->cur = b;
 }
 
@@ -520,9 +534,133 @@ int run_step(crm_t* c, float dt, long long step) {
     c->lists_valid = valid0;
   }
   CK(cudaGraphLaunch(c->gexec[p][q], c->stream));
+  c->graph_replays++;
   c->launches += c->gkernels[p][q];
   c->cur = c->gcur_after[p][q];
   c->lists_valid = true;
+  return CRM_OK;
+}
+
+// One slab step (NCCL transport), replayed from a CUDA graph like run_step: the phases launch a
+// fixed sequence per (buffer parity, rebuild) with fixed-size transfers (dist.cuh), so NCCL's
+// point-to-point calls are captured with the kernels and the comm-stream fork/join of the overlapped
+// halo.  A capture that fails (a transport that cannot be captured) falls back to eager launches.
+int slab_step_eager(crm_t* c, float dt, long long step) {
+  for (int k = 0; k < kSlabPhases; ++k) {
+    if (int r = slab_phase(c, k, dt, step)) return r;
+    if (int r = nccl_flush(c)) return r;
+  }
+  return CRM_OK;
+}
+int run_slab_step(crm_t* c, float dt, long long step) {
+  const bool rebuild = !c->lists_valid || (step % c->ps_freq) == 0;
+  if (!c->graphs || c->prof || c->dbg_on || c->slab_graph_off) return slab_step_eager(c, dt, step);
+  const int p = c->cur, q = rebuild ? 1 : 0;
+  if (!c->gexec[p][q] || c->gdt[p][q] != c->dt_d) {
+    if (c->gexec[p][q]) cudaGraphExecDestroy(c->gexec[p][q]);
+    c->gexec[p][q] = nullptr;
+    const int64_t l0 = c->launches;
+    const bool valid0 = c->lists_valid;
+    c->lists_valid = !rebuild;
+    cudaGraph_t graph = nullptr;
+    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    const int rs = slab_step_eager(c, dt, -1);
+    const cudaError_t ec = cudaStreamEndCapture(c->stream, &graph);
+    cudaError_t ei = cudaErrorUnknown;
+    if (!rs && ec == cudaSuccess) ei = cudaGraphInstantiate(&c->gexec[p][q], graph, 0);
+    if (graph) cudaGraphDestroy(graph);
+    c->gkernels[p][q] = c->launches - l0;
+    c->gcur_after[p][q] = c->cur;
+    c->launches = l0;
+    c->cur = p;
+    c->lists_valid = valid0;
+    c->posts.clear();
+    c->comm_pending = false;
+    c->halo_async = false;
+    if (rs || ec != cudaSuccess || ei != cudaSuccess) {   // not capturable here: eager from now on
+      cudaGetLastError();
+      c->gexec[p][q] = nullptr;
+      c->slab_graph_off = true;
+      return slab_step_eager(c, dt, step);
+    }
+    c->gdt[p][q] = c->dt_d;
+  }
+  CK(cudaGraphLaunch(c->gexec[p][q], c->stream));
+  c->graph_replays++;
+  c->launches += c->gkernels[p][q];
+  c->cur = c->gcur_after[p][q];
+  c->lists_valid = true;
+  return CRM_OK;
+}
+
+// One step of in-process slab contexts on one stream (loopback transport), every phase on every
+// rank then the matched copies — replayed from one CUDA graph per (buffer parity, rebuild), kept on
+// rank 0 (the test bed of the capturable slab step on one GPU).
+int group_slab_eager(crm_t** cs, int world, float dt, long long step) {
+  for (int k = 0; k < kSlabPhases; ++k) {
+    for (int a = 0; a < world; ++a)   // (the ranks step in lockstep: one step number)
+      if (int r = slab_phase(cs[a], k, dt, step)) return r;
+    if (int r = loopback_flush(cs, world)) return r;
+  }
+  return CRM_OK;
+}
+int group_slab_step(crm_t** cs, int world, float dt, long long step) {
+  crm_t* c0 = cs[0];
+  crm_t* c = c0;   // (error reports of the CK checks)
+  const bool rebuild = !c0->lists_valid || (step % c0->ps_freq) == 0;
+  bool eager = c0->slab_graph_off;
+  for (int a = 0; a < world; ++a) eager = eager || !cs[a]->graphs || cs[a]->prof || cs[a]->dbg_on;
+  if (eager) return group_slab_eager(cs, world, dt, step);
+  const int p = c0->cur, q = rebuild ? 1 : 0;
+  const std::vector<crm_t*> members(cs, cs + world);
+  if (members != c0->gmembers) {   // another group of contexts: the captured graphs point at other buffers
+    for (int b = 0; b < 2; ++b)
+      for (int k = 0; k < 2; ++k) {
+        if (c0->ggroup[b][k]) cudaGraphExecDestroy(c0->ggroup[b][k]);
+        c0->ggroup[b][k] = nullptr;
+      }
+    c0->gmembers = members;
+  }
+  if (!c0->ggroup[p][q] || c0->gdt[p][q] != c0->dt_d) {
+    if (c0->ggroup[p][q]) cudaGraphExecDestroy(c0->ggroup[p][q]);
+    c0->ggroup[p][q] = nullptr;
+    std::vector<int64_t> l0(world);
+    std::vector<bool> v0(world);
+    for (int a = 0; a < world; ++a) {
+      l0[a] = cs[a]->launches;
+      v0[a] = cs[a]->lists_valid;
+      cs[a]->lists_valid = !rebuild;
+    }
+    cudaGraph_t graph = nullptr;
+    CK(cudaStreamBeginCapture(c0->stream, cudaStreamCaptureModeThreadLocal));
+    const int rs = group_slab_eager(cs, world, dt, -1);
+    const cudaError_t ec = cudaStreamEndCapture(c0->stream, &graph);
+    cudaError_t ei = cudaErrorUnknown;
+    if (!rs && ec == cudaSuccess) ei = cudaGraphInstantiate(&c0->ggroup[p][q], graph, 0);
+    if (graph) cudaGraphDestroy(graph);
+    for (int a = 0; a < world; ++a) {
+      cs[a]->gkernels[p][q] = cs[a]->launches - l0[a];
+      cs[a]->gcur_after[p][q] = cs[a]->cur;
+      cs[a]->launches = l0[a];
+      cs[a]->cur = p;
+      cs[a]->lists_valid = v0[a];
+      cs[a]->posts.clear();
+    }
+    if (rs || ec != cudaSuccess || ei != cudaSuccess) {
+      cudaGetLastError();
+      c0->ggroup[p][q] = nullptr;
+      c0->slab_graph_off = true;
+      return group_slab_eager(cs, world, dt, step);
+    }
+    c0->gdt[p][q] = c0->dt_d;
+  }
+  CK(cudaGraphLaunch(c0->ggroup[p][q], c0->stream));
+  for (int a = 0; a < world; ++a) {
+    cs[a]->launches += cs[a]->gkernels[p][q];
+    cs[a]->graph_replays++;
+    cs[a]->cur = cs[a]->gcur_after[p][q];
+    cs[a]->lists_valid = true;
+  }
   return CRM_OK;
 }
 
@@ -583,7 +721,16 @@ int end_steps(crm_t* c, int64_t nsteps) {
   if (e != cudaSuccess) return fail(c, CRM_E_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
   c->steps_done += nsteps;
   c->dbg_valid = c->dbg_on;
+  if (c->slab) {   // the host copies of the slab's counts, once per call (the steps never read them)
+    cudaMemcpyAsync(c->h_pin + 41, c->d_slab, 4, cudaMemcpyDeviceToHost, c->stream);
+    cudaMemcpyAsync(c->h_pin + 42, c->cell_start + plane_start_index(c, c->x_lo), 4, cudaMemcpyDeviceToHost, c->stream);
+    cudaMemcpyAsync(c->h_pin + 43, c->cell_start + plane_start_index(c, c->x_hi), 4, cudaMemcpyDeviceToHost, c->stream);
+  }
   int r = read_latch(c);
+  if (c->slab && nsteps > 0) {
+    c->nl = c->h_pin[41];
+    c->n_owned = (int64_t)c->h_pin[43] - (int64_t)c->h_pin[42];
+  }
   e = cudaGetLastError();
   if (e != cudaSuccess) return fail(c, CRM_E_CUDA, std::string("step: ") + cudaGetErrorString(e));
   return r;
@@ -762,6 +909,8 @@ void crm_destroy(crm_t* c) {
     cudaFree(c->P[b]); cudaFree(c->L[b]); cudaFree(c->U[b]); cudaFree(c->S1[b]); cudaFree(c->S2[b]); cudaFree(c->ids[b]);
     for (int q = 0; q < 2; ++q)
       if (c->gexec[b][q]) cudaGraphExecDestroy(c->gexec[b][q]);
+    for (int q = 0; q < 2; ++q)
+      if (c->ggroup[b][q]) cudaGraphExecDestroy(c->ggroup[b][q]);
     cudaFree(c->dbg.drho[b]); cudaFree(c->dbg.acc[b]); cudaFree(c->dbg.ds1[b]); cudaFree(c->dbg.ds2[b]);
     cudaFree(c->dbg.bu[b]); cudaFree(c->dbg.bs1[b]); cudaFree(c->dbg.bs2[b]);
   }
@@ -780,6 +929,11 @@ void crm_destroy(crm_t* c) {
     cudaFree(c->pk.id[d]);
   }
   cudaFree(c->pk.cnt);
+  for (int d = 0; d < 2; ++d) {
+    cudaFree(c->rv.P[d]); cudaFree(c->rv.L[d]); cudaFree(c->rv.U[d]); cudaFree(c->rv.S1[d]); cudaFree(c->rv.S2[d]);
+    cudaFree(c->rv.id[d]);
+  }
+  cudaFree(c->rv.cnt); cudaFree(c->d_slab);
   cudaFree(c->macc); cudaFree(c->d_bpart); cudaFree(c->d_err); cudaFree(c->d_xcount); cudaFree(c->dbg_ids); cudaFree(c->d_stage);
   if (c->h_err) cudaFreeHost(c->h_err);
   if (c->h_pin) cudaFreeHost(c->h_pin);
@@ -863,6 +1017,7 @@ int64_t crm_count(const crm_t* c, int which) {
     case CRM_FLUID: return c->n_fluid;
     case CRM_BCE: return c->n_bce;
     case CRM_OWNED: return c->committed ? c->n_owned : (c->slab ? 0 : c->n);
+    case CRM_GRAPH_REPLAYS: return c->graph_replays;
     default: return c->n;
   }
 }
@@ -930,10 +1085,7 @@ int crm_step(crm_t* c, double dt, int64_t nsteps) {
       c->t_now += dt;
       continue;
     }
-    for (int k = 0; k < kSlabPhases; ++k) {
-      if ((r = slab_phase(c, k, (float)dt, step))) return r;
-      if ((r = nccl_flush(c))) return r;
-    }
+    if ((r = run_slab_step(c, (float)dt, step))) return r;
   }
   return end_steps(c, nsteps);
 }
@@ -951,16 +1103,11 @@ int crm_group_step(crm_t** cs, int world, double dt, int64_t nsteps) {
   for (int a = 0; a < world; ++a)
     if ((r = begin_steps(cs[a], dt))) return r;
   for (int64_t s = 0; s < nsteps; ++s) {
-    for (int k = 0; k < kSlabPhases; ++k) {
-      for (int a = 0; a < world; ++a) {
-        const long long step = (long long)(cs[a]->steps_done + s);
-        if (world == 1) {
-          if (k == 0 && (r = issue_step(cs[a], (float)dt, step))) return r;
-          continue;
-        }
-        if ((r = slab_phase(cs[a], k, (float)dt, step))) return r;
-      }
-      if (world > 1 && (r = loopback_flush(cs, world))) return r;
+    const long long step0 = (long long)(cs[0]->steps_done + s);
+    if (world == 1) {
+      if ((r = issue_step(cs[0], (float)dt, step0))) return r;
+    } else if ((r = group_slab_step(cs, world, (float)dt, step0))) {
+      return r;
     }
     for (int a = 0; a < world; ++a) cs[a]->t_now += dt;
   }

@@ -71,28 +71,6 @@ void post(crm_t* c, int peer, bool send, const void* ptr, size_t bytes) {
   c->posts.push_back({peer, send, const_cast<void*>(ptr), bytes});
 }
 
-// state slice [b, e) of buffer set `y` (ids included when with_ids)
-void post_slice(crm_t* c, int peer, bool send, int y, uint32_t b, uint32_t e, bool with_ids) {
-  if (e <= b) return;
-  const size_t k = e - b;
-  post(c, peer, send, c->P[y] + b, k * 16);
-  post(c, peer, send, c->L[y] + b, k * 16);
-  post(c, peer, send, c->U[y] + b, k * 16);
-  post(c, peer, send, c->S1[y] + b, k * 16);
-  post(c, peer, send, c->S2[y] + b, k * 8);
-  if (with_ids) post(c, peer, send, c->ids[y] + b, k * 4);
-}
-
-void post_mid_slice(crm_t* c, int peer, bool send, uint32_t b, uint32_t e) {
-  if (e <= b) return;
-  const size_t k = e - b;
-  post(c, peer, send, c->Pm + b, k * 16);
-  post(c, peer, send, c->Lm + b, k * 16);
-  post(c, peer, send, c->Um + b, k * 16);
-  post(c, peer, send, c->S1m + b, k * 16);
-  post(c, peer, send, c->S2m + b, k * 8);
-}
-
 // the compute stream waits for an asynchronous halo (phase 5's) before touching ghost slots
 void wait_comm(crm_t* c) {
   if (!c->comm_pending) return;
@@ -193,36 +171,46 @@ uint32_t plane_start_index(const crm_t* c, int p) {   // cell index of the first
   return (uint32_t)(p * NyNz);
 }
 
-// read cellStart at the first cell of planes ps[0..k) (k <= 8) into out
-int read_plane_starts(crm_t* c, const int* ps, int k, uint32_t* out) {
-  for (int j = 0; j < k; ++j)
-    CK(cudaMemcpyAsync(c->h_pin + j, c->cell_start + plane_start_index(c, ps[j]), 4, cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
-  for (int j = 0; j < k; ++j) out[j] = c->h_pin[j];
-  return CRM_OK;
+// the whole of side d of a pack / receive buffer set (fixed capacity: entries [0, count))
+void post_buf(crm_t* c, int peer, bool send, const SlabPack& b, int d, size_t count, bool with_ids) {
+  post(c, peer, send, b.P[d], count * 16);
+  post(c, peer, send, b.L[d], count * 16);
+  post(c, peer, send, b.U[d], count * 16);
+  post(c, peer, send, b.S1[d], count * 16);
+  post(c, peer, send, b.S2[d], count * 8);
+  if (with_ids) post(c, peer, send, b.id[d], count * 4);
 }
 
-// count exchange: two words per direction (d_xcount: send L[2], send R[2], recv L[2], recv R[2])
-int read_counts(crm_t* c, uint32_t* l0, uint32_t* l1, uint32_t* r0, uint32_t* r1) {
-  CK(cudaMemcpyAsync(c->h_pin + 16, c->d_xcount + 4, 16, cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
-  const bool hl = c->rank > 0, hr = c->rank < c->world - 1;
-  *l0 = hl ? c->h_pin[16] : 0;
-  if (l1) *l1 = hl ? c->h_pin[17] : 0;
-  *r0 = hr ? c->h_pin[18] : 0;
-  if (r1) *r1 = hr ? c->h_pin[19] : 0;
-  return CRM_OK;
+// cell ranges of the slab's two boundary planes (ghost = false: the owned first / last plane, sent)
+// or of its two ghost planes (ghost = true: received)
+HaloSide halo_side(const crm_t* c, bool ghost) {
+  HaloSide hs{};
+  const int pl[2] = {ghost ? c->x_lo - 1 : c->x_lo, ghost ? c->x_hi : c->x_hi - 1};
+  for (int d = 0; d < 2; ++d) {
+    hs.on[d] = d == 0 ? (c->rank > 0) : (c->rank < c->world - 1);
+    hs.c0[d] = hs.on[d] ? plane_start_index(c, pl[d]) : 0u;
+    hs.c1[d] = hs.on[d] ? plane_start_index(c, pl[d] + 1) : 0u;
+  }
+  return hs;
 }
 
-int post_counts(crm_t* c, uint32_t l0, uint32_t l1, uint32_t r0, uint32_t r1) {
-  c->h_pin[24] = l0; c->h_pin[25] = l1; c->h_pin[26] = r0; c->h_pin[27] = r1;
-  CK(cudaMemcpyAsync(c->d_xcount, c->h_pin + 24, 16, cudaMemcpyHostToDevice, c->stream));
-  CK(cudaMemsetAsync(c->d_xcount + 4, 0, 16, c->stream));
-  post(c, c->rank - 1, true, c->d_xcount + 0, 8);
-  post(c, c->rank + 1, true, c->d_xcount + 2, 8);
-  post(c, c->rank - 1, false, c->d_xcount + 4, 8);
-  post(c, c->rank + 1, false, c->d_xcount + 6, 8);
-  return CRM_OK;
+// halo, sender side: the boundary planes of (P, L, U, S1, S2) packed and posted, each side's count
+// beside it (d_xcount[0..1] out, [2..3] in); halo_unpack (after the flush) fills the ghost planes
+void halo_pack(crm_t* c, const float4* P, const float4* L, const float4* U, const float4* S1, const float2* S2,
+               long long step) {
+  launch(c, KID_SLAB, k_halo_pack, dim3(2 * c->num_sms, 2), dim3(256), (const uint32_t*)c->cell_start,
+         halo_side(c, false), P, L, U, S1, S2, c->pk, c->d_xcount, c->d_err, step);
+  for (int d = 0; d < 2; ++d) {
+    const int peer = d == 0 ? c->rank - 1 : c->rank + 1;
+    post_buf(c, peer, true, c->pk, d, c->pk.cap_g, false);
+    post(c, peer, true, c->d_xcount + d, 4);
+    post_buf(c, peer, false, c->rv, d, c->rv.cap_g, false);
+    post(c, peer, false, c->d_xcount + 2 + d, 4);
+  }
+}
+void halo_unpack(crm_t* c, float4* P, float4* L, float4* U, float4* S1, float2* S2, long long step) {
+  launch(c, KID_SLAB, k_halo_unpack, dim3(2 * c->num_sms, 2), dim3(256), (const uint32_t*)c->cell_start,
+         halo_side(c, true), c->rv, (const uint32_t*)(c->d_xcount + 2), P, L, U, S1, S2, c->d_err, step);
 }
 
 void issue_sort(crm_t* c, long long step, uint32_t drop_mask);
@@ -233,106 +221,67 @@ void issue_body_partial(crm_t* c);
 void issue_body_finish(crm_t* c);
 
 // ---------------------------------------------------------------------------------------
-// the phases of one slab step (each ends with posts; the transport flushes between phases)
+// The phases of one slab step (each ends with posts; the transport flushes between phases).  No
+// phase reads the device: the local count is the device word d_slab[0], slot ranges of planes come
+// from cellStart inside the kernels, and every transfer has a fixed size (the pack buffers whole),
+// so a slab step is one fixed launch sequence per (buffer parity, rebuild) and is replayed from a
+// CUDA graph (run_slab_step / crm_group_step).
 int slab_phase(crm_t* c, int k, float dt, long long step) {
-  const int L = c->rank - 1, R = c->rank + 1;
   switch (k) {
     case 0: {   // rebuild: one pass packs emigrants and boundary planes per side (no sort here)
       // Alg. 2: between rebuilds the slots, ghost sets and lists stay; only values move (phase 3)
-      c->slab_rebuild = !c->lists_valid || (step % c->ps_freq) == 0;
+      c->slab_rebuild = !c->lists_valid || (step >= 0 && (step % c->ps_freq) == 0);
       launch(c, KID_STEP, k_step_begin, dim3(1), dim3(1), c->d_err, step);
       if (!c->slab_rebuild) return CRM_OK;
       const int y = c->cur;
       CK(cudaMemsetAsync(c->pk.cnt, 0, 16, c->stream));
-      if (c->nl)
-        launch(c, KID_SLAB, k_slab_pack, dim3(blocks(c->nl, 256)), dim3(256), (int)c->nl, (const float4*)c->P[y],
-               (const float4*)c->L[y], c->U[y], (const float4*)c->S1[y], (const float2*)c->S2[y],
-               (const uint32_t*)c->ids[y], c->grid, c->x_lo, c->x_hi, c->rank > 0 ? 1 : 0,
-               c->rank < c->world - 1 ? 1 : 0, c->pk, c->d_err, step);
-      CK(cudaMemcpyAsync(c->h_pin + 32, c->pk.cnt, 16, cudaMemcpyDeviceToHost, c->stream));
-      CK(cudaStreamSynchronize(c->stream));
-      for (int k = 0; k < 4; ++k) c->pk_n[k] = c->h_pin[32 + k];
-      if (c->pk_n[0] > c->pk.cap_e || c->pk_n[2] > c->pk.cap_e || c->pk_n[1] > c->pk.cap_g || c->pk_n[3] > c->pk.cap_g)
-        return fail(c, CRM_E_CAPACITY, "slab pack buffers exceeded (emigrants or boundary plane)");
-      return post_counts(c, c->pk_n[0], c->pk_n[1], c->pk_n[2], c->pk_n[3]);
-    }
-    case 1: {   // rebuild: payloads — emigrants (owned there) and boundary planes (ghosts there), appended
-      if (!c->slab_rebuild) return CRM_OK;
-      uint32_t el, gl, er, gr;
-      if (int r = read_counts(c, &el, &gl, &er, &gr)) return r;
-      c->rv_n[0] = el; c->rv_n[1] = gl; c->rv_n[2] = er; c->rv_n[3] = gr;
-      const uint32_t nl = (uint32_t)c->nl;
-      if ((int64_t)nl + el + gl + er + gr > c->ncap) return fail(c, CRM_E_CAPACITY, "slab capacity exceeded (immigrants + ghosts)");
-      const int y = c->cur;
-      for (int d = 0; d < 2; ++d) {   // sends: E then G of each side (the receiver posts in the same order)
-        const int peer = d == 0 ? L : R;
-        const uint32_t ne = c->pk_n[2 * d], ng = c->pk_n[2 * d + 1], g0 = c->pk.cap_e;
-        post(c, peer, true, c->pk.P[d], ne * 16); post(c, peer, true, c->pk.L[d], ne * 16);
-        post(c, peer, true, c->pk.U[d], ne * 16); post(c, peer, true, c->pk.S1[d], ne * 16);
-        post(c, peer, true, c->pk.S2[d], ne * 8); post(c, peer, true, c->pk.id[d], ne * 4);
-        post(c, peer, true, c->pk.P[d] + g0, ng * 16); post(c, peer, true, c->pk.L[d] + g0, ng * 16);
-        post(c, peer, true, c->pk.U[d] + g0, ng * 16); post(c, peer, true, c->pk.S1[d] + g0, ng * 16);
-        post(c, peer, true, c->pk.S2[d] + g0, ng * 8); post(c, peer, true, c->pk.id[d] + g0, ng * 4);
+      launch(c, KID_SLAB, k_slab_pack, dim3(8 * c->num_sms), dim3(256), (int)c->ncap, (const float4*)c->P[y],
+             (const float4*)c->L[y], c->U[y], (const float4*)c->S1[y], (const float2*)c->S2[y],
+             (const uint32_t*)c->ids[y], c->grid, c->x_lo, c->x_hi, c->rank > 0 ? 1 : 0,
+             c->rank < c->world - 1 ? 1 : 0, c->pk, c->d_err, step, (const uint32_t*)c->d_slab);
+      // counts and the whole pack buffers (E then G of each side): the receiver places them by count
+      const size_t pc = (size_t)c->pk.cap_e + c->pk.cap_g;
+      for (int d = 0; d < 2; ++d) {
+        const int peer = d == 0 ? c->rank - 1 : c->rank + 1;
+        post(c, peer, true, c->pk.cnt + 2 * d, 8);
+        post_buf(c, peer, true, c->pk, d, pc, true);
+        post(c, peer, false, c->rv.cnt + 2 * d, 8);
+        post_buf(c, peer, false, c->rv, d, pc, true);
       }
-      // receives, appended behind the local particles: [E left][G left][E right][G right]
-      const uint32_t a0 = nl, a1 = a0 + el, a2 = a1 + gl, a3 = a2 + er, a4 = a3 + gr;
-      post_slice(c, L, false, y, a0, a1, true);
-      post_slice(c, L, false, y, a1, a2, true);
-      post_slice(c, R, false, y, a2, a3, true);
-      post_slice(c, R, false, y, a3, a4, true);
       return CRM_OK;
     }
-    case 2: {   // rebuild: immigrants checked to sit in the boundary plane; ghosts flagged
+    case 1: {   // rebuild: immigrants (checked to sit in the boundary plane) and ghosts appended
       if (!c->slab_rebuild) return CRM_OK;
       const int y = c->cur;
-      const uint32_t nl = (uint32_t)c->nl;
-      const uint32_t a0 = nl, a1 = a0 + c->rv_n[0], a2 = a1 + c->rv_n[1], a3 = a2 + c->rv_n[2], a4 = a3 + c->rv_n[3];
-      if (a1 > a0)
-        launch(c, KID_SLAB, k_check_plane, dim3(blocks(a1 - a0, 256)), dim3(256), (const float4*)c->P[y],
-               (const uint32_t*)c->ids[y], a0, a1, c->grid, c->x_lo, c->d_err, step);
-      if (a3 > a2)
-        launch(c, KID_SLAB, k_check_plane, dim3(blocks(a3 - a2, 256)), dim3(256), (const float4*)c->P[y],
-               (const uint32_t*)c->ids[y], a2, a3, c->grid, c->x_hi - 1, c->d_err, step);
-      if (a2 > a1) launch(c, KID_SLAB, k_or_tag, dim3(blocks(a2 - a1, 256)), dim3(256), c->U[y], a1, a2, TAG_GHOST);
-      if (a4 > a3) launch(c, KID_SLAB, k_or_tag, dim3(blocks(a4 - a3, 256)), dim3(256), c->U[y], a3, a4, TAG_GHOST);
-      c->nl = a4;
+      launch(c, KID_SLAB, k_slab_counts, dim3(1), dim3(1), c->d_slab, (const uint32_t*)c->rv.cnt, c->rank > 0 ? 1 : 0,
+             c->rank < c->world - 1 ? 1 : 0, c->pk.cap_e, c->pk.cap_g, (uint32_t)c->ncap, c->d_err, step);
+      launch(c, KID_SLAB, k_slab_append, dim3(2 * c->num_sms, 2), dim3(256),
+             (const uint32_t*)c->d_slab, c->rv, c->P[y], c->L[y], c->U[y], c->S1[y], c->S2[y], c->ids[y], c->grid,
+             c->x_lo, c->x_hi, c->d_err, step);
       return CRM_OK;
     }
-    case 3: {   // Alg. 2 reuse step: refresh the ghost values y_n in place
+    case 2:
+      return CRM_OK;
+    case 3: {   // Alg. 2 reuse step: the ghost planes' y_n refreshed in place
       if (c->slab_rebuild) return CRM_OK;
       const int y = c->cur;
-      post_slice(c, L, true, y, c->s_lo, c->s_lo1, false);
-      post_slice(c, R, true, y, c->s_hi1, c->s_hi, false);
-      post_slice(c, L, false, y, c->s_lom1, c->s_lo, false);
-      post_slice(c, R, false, y, c->s_hi, c->s_hip1, false);
+      halo_pack(c, c->P[y], c->L[y], c->U[y], c->S1[y], c->S2[y], step);
       return CRM_OK;
     }
-    case 4: {   // ghosts flagged, local sort, BCE at y_n; boundary planes -> ghosts
-      if (c->slab_rebuild) {   // the one sort of the rebuild: old ghosts out, emigrants kept as ghosts
+    case 4: {   // the one sort of a rebuild (ghosts in, emigrants and old ghosts out); BCE at y_n; E4
+      if (c->slab_rebuild) {
         issue_sort(c, step, TAG_DROP);
-        const int ps[7] = {c->x_lo - 1, c->x_lo, c->x_lo + 1, c->x_hi - 1, c->x_hi, c->x_hi + 1, c->grid.dims[0]};
-        uint32_t st[7];
-        if (int r = read_plane_starts(c, ps, 7, st)) return r;
-        c->nl = st[6];
-        c->s_lom1 = c->rank > 0 ? st[0] : st[1];
-        c->s_lo = st[1]; c->s_lo1 = st[2]; c->s_hi1 = st[3]; c->s_hi = st[4];
-        c->s_hip1 = c->rank < c->world - 1 ? st[5] : st[4];
-        c->n_owned = c->s_hi - c->s_lo;
-      } else {   // the refreshed ghost values carried the owners' tags
+        // the new local count: the dropped particles sorted behind cell M
+        launch(c, KID_SLAB, k_copy_u32, dim3(1), dim3(1), c->d_slab, (const uint32_t*)(c->cell_start + c->grid.M));
+      } else {
         const int y0 = c->cur;
-        if (c->s_lo > c->s_lom1)
-          launch(c, KID_SLAB, k_or_tag, dim3(blocks(c->s_lo - c->s_lom1, 256)), dim3(256), c->U[y0], c->s_lom1, c->s_lo, TAG_GHOST);
-        if (c->s_hip1 > c->s_hi)
-          launch(c, KID_SLAB, k_or_tag, dim3(blocks(c->s_hip1 - c->s_hi, 256)), dim3(256), c->U[y0], c->s_hi, c->s_hip1, TAG_GHOST);
+        halo_unpack(c, c->P[y0], c->L[y0], c->U[y0], c->S1[y0], c->S2[y0], step);
       }
       c->ph.build_lists = c->slab_rebuild ? 1 : 0;
       c->lists_valid = true;
       issue_bce(c, 0, dt, step, 0);
       const int y = c->cur;
-      post_slice(c, L, true, y, c->s_lo, c->s_lo1, false);
-      post_slice(c, R, true, y, c->s_hi1, c->s_hi, false);
-      post_slice(c, L, false, y, c->s_lom1, c->s_lo, false);
-      post_slice(c, R, false, y, c->s_hi, c->s_hip1, false);
+      halo_pack(c, c->P[y], c->L[y], c->U[y], c->S1[y], c->S2[y], step);
       return CRM_OK;
     }
     case 5:   // rates + half step on the boundary tile columns (all tiles with moving bodies); y_mid halo
@@ -348,12 +297,8 @@ int slab_phase(crm_t* c, int k, float dt, long long step) {
       const long long ntx = per_x ? c->ntiles / per_x : 0;
       const bool split = c->n_moving_markers == 0 && c->boxes.empty() && ntx > 2;
       if (k == 5) {
-        // the copies of E4 carried the owners' tags: mark the ghost planes as ghosts again
         const int y = c->cur;
-        if (c->s_lo > c->s_lom1)
-          launch(c, KID_SLAB, k_or_tag, dim3(blocks(c->s_lo - c->s_lom1, 256)), dim3(256), c->U[y], c->s_lom1, c->s_lo, TAG_GHOST);
-        if (c->s_hip1 > c->s_hi)
-          launch(c, KID_SLAB, k_or_tag, dim3(blocks(c->s_hip1 - c->s_hi, 256)), dim3(256), c->U[y], c->s_hi, c->s_hip1, TAG_GHOST);
+        halo_unpack(c, c->P[y], c->L[y], c->U[y], c->S1[y], c->S2[y], step);   // E4 -> ghost planes
         if (split) {
           issue_rates_range(c, 0, dt, step, 0, per_x);                    // first tile column
           issue_rates_range(c, 0, dt, step, (ntx - 1) * per_x, per_x);    // last tile column
@@ -370,16 +315,15 @@ int slab_phase(crm_t* c, int k, float dt, long long step) {
         return CRM_OK;
       } else {
         wait_comm(c);
+        halo_unpack(c, c->Pm, c->Lm, c->Um, c->S1m, c->S2m, step);   // E5 -> ghost planes of y_mid
         issue_bce(c, 1, dt, step, 0);
       }
-      post_mid_slice(c, L, true, c->s_lo, c->s_lo1);
-      post_mid_slice(c, R, true, c->s_hi1, c->s_hi);
-      post_mid_slice(c, L, false, c->s_lom1, c->s_lo);
-      post_mid_slice(c, R, false, c->s_hi, c->s_hip1);
+      halo_pack(c, c->Pm, c->Lm, c->Um, c->S1m, c->S2m, step);
       return CRM_OK;
     }
     case 8:   // rates + full step; moving bodies: this slab's partial loads to every other slab
       wait_comm(c);
+      halo_unpack(c, c->Pm, c->Lm, c->Um, c->S1m, c->S2m, step);   // E7 -> ghost planes of y_mid
       issue_rates(c, 1, dt, step);
       if (c->n_moving_bodies) {
         issue_body_partial(c);

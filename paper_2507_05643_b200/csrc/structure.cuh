@@ -59,7 +59,8 @@ __global__ void k_markers_place(int nm, const uint32_t* __restrict__ moving_ids,
 __global__ void k_bin(int n, const float4* __restrict__ P, const float4* __restrict__ U,
                       const uint32_t* __restrict__ ids, Grid g, uint32_t drop_mask, const uint8_t* __restrict__ act,
                       uint32_t* __restrict__ key, uint32_t* __restrict__ arrival, uint32_t* __restrict__ cell_count,
-                      ErrLatch* err, long long step) {
+                      ErrLatch* err, long long step, const uint32_t* __restrict__ dn) {
+  if (dn) n = (int)*dn;   // slabs: the local count lives on the device (grid over the capacity)
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const bool valid = i < n;
   uint32_t c = g.M;
@@ -180,12 +181,24 @@ __device__ __forceinline__ void slab_put(const SlabPack& pk, int d, uint32_t slo
   pk.P[d][slot] = p; pk.L[d][slot] = l; pk.U[d][slot] = u; pk.S1[d][slot] = s1; pk.S2[d][slot] = s2;
   pk.id[d][slot] = id;
 }
+__device__ __forceinline__ void slab_pack_one(int i, const float4* __restrict__ P, const float4* __restrict__ L,
+                                              float4* __restrict__ U, const float4* __restrict__ S1,
+                                              const float2* __restrict__ S2, const uint32_t* __restrict__ ids,
+                                              const Grid& g, int x_lo, int x_hi, int has_l, int has_r,
+                                              const SlabPack& pk, ErrLatch* err, long long step);
 __global__ void k_slab_pack(int n, const float4* __restrict__ P, const float4* __restrict__ L, float4* __restrict__ U,
                             const float4* __restrict__ S1, const float2* __restrict__ S2,
                             const uint32_t* __restrict__ ids, Grid g, int x_lo, int x_hi, int has_l, int has_r,
-                            SlabPack pk, ErrLatch* err, long long step) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+                            SlabPack pk, ErrLatch* err, long long step, const uint32_t* __restrict__ dn) {
+  n = (int)*dn;   // the local count (device word: the slab step has no host reads)
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    slab_pack_one(i, P, L, U, S1, S2, ids, g, x_lo, x_hi, has_l, has_r, pk, err, step);
+}
+__device__ __forceinline__ void slab_pack_one(int i, const float4* __restrict__ P, const float4* __restrict__ L,
+                                              float4* __restrict__ U, const float4* __restrict__ S1,
+                                              const float2* __restrict__ S2, const uint32_t* __restrict__ ids,
+                                              const Grid& g, int x_lo, int x_hi, int has_l, int has_r,
+                                              const SlabPack& pk, ErrLatch* err, long long step) {
   const float4 u = U[i];
   const uint32_t tag = tag_of(u.w);
   if (tag & TAG_GHOST) {   // last step's ghost: leaves at this rebuild
@@ -207,23 +220,117 @@ __global__ void k_slab_pack(int n, const float4* __restrict__ P, const float4* _
   if (emi_l || emi_r) {
     const int d = emi_l ? 0 : 1;
     const uint32_t k = atomicAdd(&pk.cnt[2 * d], 1u);
-    if (k < pk.cap_e) slab_put(pk, d, k, p, l, u, s1, s2, id);   // (overflow: the host checks the count)
+    if (k < pk.cap_e) slab_put(pk, d, k, p, l, u, s1, s2, id);
+    else latch_error(err, -9 /*CRM_E_CAPACITY*/, (long long)id, step, 2);
     U[i].w = __uint_as_float(tag | TAG_GHOST);   // kept here as a ghost of the neighbour's first plane
     return;
   }
   if (g_l) {
     const uint32_t k = atomicAdd(&pk.cnt[1], 1u);
     if (k < pk.cap_g) slab_put(pk, 0, pk.cap_e + k, p, l, u, s1, s2, id);
+    else latch_error(err, -9 /*CRM_E_CAPACITY*/, (long long)id, step, 2);
   }
   if (g_r) {
     const uint32_t k = atomicAdd(&pk.cnt[3], 1u);
     if (k < pk.cap_g) slab_put(pk, 1, pk.cap_e + k, p, l, u, s1, s2, id);
+    else latch_error(err, -9 /*CRM_E_CAPACITY*/, (long long)id, step, 2);
+  }
+}
+
+// Slab rebuild, receiver side.  The neighbours' pack buffers arrive whole (fixed capacity: the
+// transfer sizes do not depend on device counts, so the step needs no host read and can be
+// captured in a CUDA graph) with their counts in rv.cnt = [E, G from the left, E, G from the right].
+// k_slab_counts (one thread) places the four segments behind the n local particles (d_slab[0] = n;
+// d_slab[1..4] = segment starts; d_slab[0] becomes the new count) or latches CRM_E_CAPACITY;
+// k_slab_append (gridDim.y = side) copies them: immigrants (E) must sit in this slab's boundary
+// plane (a particle crosses at most one 2h plane per step), ghosts (G) get TAG_GHOST.
+__global__ void k_slab_counts(uint32_t* __restrict__ d_slab, const uint32_t* __restrict__ rcnt, int has_l, int has_r,
+                              uint32_t cap_e, uint32_t cap_g, uint32_t ncap, ErrLatch* err, long long step) {
+  const uint32_t n = d_slab[0];
+  const uint32_t el = has_l ? rcnt[0] : 0u, gl = has_l ? rcnt[1] : 0u;
+  const uint32_t er = has_r ? rcnt[2] : 0u, gr = has_r ? rcnt[3] : 0u;
+  if (el > cap_e || er > cap_e || gl > cap_g || gr > cap_g || (unsigned long long)n + el + gl + er + gr > ncap) {
+    latch_error(err, -9 /*CRM_E_CAPACITY*/, -1, step, 3);
+    d_slab[1] = d_slab[2] = d_slab[3] = d_slab[4] = n;   // nothing appended
+    d_slab[5] = d_slab[6] = d_slab[7] = d_slab[8] = 0;
+    return;
+  }
+  d_slab[1] = n; d_slab[2] = n + el; d_slab[3] = n + el + gl; d_slab[4] = n + el + gl + er;
+  d_slab[5] = el; d_slab[6] = gl; d_slab[7] = er; d_slab[8] = gr;
+  d_slab[0] = n + el + gl + er + gr;
+}
+__global__ void k_slab_append(const uint32_t* __restrict__ d_slab, SlabPack rv, float4* __restrict__ P,
+                              float4* __restrict__ L, float4* __restrict__ U, float4* __restrict__ S1,
+                              float2* __restrict__ S2, uint32_t* __restrict__ ids, Grid g, int x_lo, int x_hi,
+                              ErrLatch* err, long long step) {
+  if (latched(err)) return;
+  const int d = blockIdx.y;   // 0: from the left neighbour, 1: from the right
+  const uint32_t ne = d_slab[5 + 2 * d], ng = d_slab[6 + 2 * d];
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < ne + ng; j += gridDim.x * blockDim.x) {
+    const bool emi = j < ne;
+    const uint32_t k = emi ? j : rv.cap_e + (j - ne);                          // source slot
+    const uint32_t dst = emi ? d_slab[1 + 2 * d] + j : d_slab[2 + 2 * d] + (j - ne);
+    const float4 p = rv.P[d][k];
+    float4 u = rv.U[d][k];
+    const uint32_t id = rv.id[d][k];
+    if (emi) {
+      const float f = b1_floor(p.x, g.lo[0], g.s);
+      if (!(f == (float)(d == 0 ? x_lo : x_hi - 1))) latch_error(err, -2 /*CRM_E_DOMAIN*/, (long long)id, step, 1);
+    } else {
+      u.w = __uint_as_float(tag_of(u.w) | TAG_GHOST);
+    }
+    P[dst] = p; L[dst] = rv.L[d][k]; U[dst] = u; S1[dst] = rv.S1[d][k]; S2[dst] = rv.S2[d][k];
+    ids[dst] = id;
+  }
+}
+
+// Per-stage halo of the slabs, fixed-capacity (graph-capturable): k_halo_pack copies this slab's
+// boundary plane of side d = blockIdx.y (the cells [c0[d], c1[d]) — slots from cellStart) into the
+// pack buffer of that side and its count into cnt[d]; k_halo_unpack copies the neighbour's plane
+// into the ghost plane of side d (cells [c0[d], c1[d])), flags it TAG_GHOST and checks the counts
+// agree (both sides hold the same particles in the same (cell, id) order).
+struct HaloSide {
+  uint32_t c0[2], c1[2];   // cell range per side
+  int on[2];               // side has a neighbour
+};
+__global__ void k_halo_pack(const uint32_t* __restrict__ cell_start, HaloSide hs, const float4* __restrict__ P,
+                            const float4* __restrict__ L, const float4* __restrict__ U, const float4* __restrict__ S1,
+                            const float2* __restrict__ S2, SlabPack pk, uint32_t* __restrict__ cnt, ErrLatch* err,
+                            long long step) {
+  if (latched(err)) return;
+  const int d = blockIdx.y;
+  if (!hs.on[d]) return;
+  const uint32_t b = cell_start[hs.c0[d]], n = cell_start[hs.c1[d]] - b;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    cnt[d] = n;
+    if (n > pk.cap_g) latch_error(err, -9 /*CRM_E_CAPACITY*/, -1, step, 4);
+  }
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < min(n, pk.cap_g); k += gridDim.x * blockDim.x) {
+    pk.P[d][k] = P[b + k]; pk.L[d][k] = L[b + k]; pk.U[d][k] = U[b + k]; pk.S1[d][k] = S1[b + k];
+    pk.S2[d][k] = S2[b + k];
+  }
+}
+__global__ void k_halo_unpack(const uint32_t* __restrict__ cell_start, HaloSide hs, SlabPack rv,
+                              const uint32_t* __restrict__ cnt, float4* __restrict__ P, float4* __restrict__ L,
+                              float4* __restrict__ U, float4* __restrict__ S1, float2* __restrict__ S2, ErrLatch* err,
+                              long long step) {
+  if (latched(err)) return;
+  const int d = blockIdx.y;
+  if (!hs.on[d]) return;
+  const uint32_t b = cell_start[hs.c0[d]], n = cell_start[hs.c1[d]] - b;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && cnt[d] != n) latch_error(err, -8 /*CRM_E_COMM*/, -1, step, (long long)cnt[d]);
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < min(n, rv.cap_g); k += gridDim.x * blockDim.x) {
+    float4 u = rv.U[d][k];
+    u.w = __uint_as_float(tag_of(u.w) | TAG_GHOST);
+    P[b + k] = rv.P[d][k]; L[b + k] = rv.L[d][k]; U[b + k] = u; S1[b + k] = rv.S1[d][k]; S2[b + k] = rv.S2[d][k];
   }
 }
 
 // slot_of_id entries of the particles of the old sorted set: invalid before the reorder writes the new
 // set (O(local) instead of a fill over every id of the global input)
-__global__ void k_clear_slots(int n, const uint32_t* __restrict__ ids, uint32_t* __restrict__ slot_of_id) {
+__global__ void k_clear_slots(int n, const uint32_t* __restrict__ ids, uint32_t* __restrict__ slot_of_id,
+                              const uint32_t* __restrict__ dn) {
+  if (dn) n = (int)*dn;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) slot_of_id[ids[i]] = 0xffffffffu;
 }
@@ -284,7 +391,8 @@ __global__ void k_fill_u32(uint32_t* __restrict__ p, long long n, uint32_t v) {
 // ---------------------------------------------------------------------------------------
 __global__ void k_scatter(int n, const uint32_t* __restrict__ key, const uint32_t* __restrict__ arrival,
                           const uint32_t* __restrict__ cell_start, const uint32_t* __restrict__ ids,
-                          uint32_t* __restrict__ tmp_src, uint32_t* __restrict__ tmp_id) {
+                          uint32_t* __restrict__ tmp_src, uint32_t* __restrict__ tmp_id, const uint32_t* __restrict__ dn) {
+  if (dn) n = (int)*dn;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const uint32_t slot = cell_start[key[i]] + arrival[i];
@@ -300,7 +408,8 @@ __global__ void k_reorder(int n, const uint32_t* __restrict__ tmp_src, const uin
                           const float2* __restrict__ S2, float4* __restrict__ Pn, float4* __restrict__ Ln,
                           float4* __restrict__ Un, float4* __restrict__ S1n, float2* __restrict__ S2n,
                           uint32_t* __restrict__ ids_n, uint32_t* __restrict__ cell_of,
-                          uint32_t* __restrict__ slot_of_id, uint32_t M, int keep_tail) {
+                          uint32_t* __restrict__ slot_of_id, uint32_t M, int keep_tail, const uint32_t* __restrict__ dn) {
+  if (dn) n = (int)*dn;
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n) return;
   const uint32_t i = tmp_src[s];

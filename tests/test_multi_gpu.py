@@ -93,3 +93,28 @@ def test_moving_body_across_slabs(crm):
     x_ref = ref.get_state()[0]
     assert not np.isnan(got[0]).any()
     assert np.abs(got[0] - x_ref).max() < 1e-5 * sc.params["d0"]
+
+
+def test_slab_step_graph_replay_equals_eager(crm):
+    """The slab step reads no device value on the host (device-resident counts, fixed-size
+    transfers: DESIGN §7), so it is captured once per (buffer parity, rebuild) and replayed; the
+    replay must give the eager launches' state bit for bit, across several calls, with migration
+    and Alg. 2 reuse steps."""
+    from paper_2507_05643_b200 import dist
+    sc = workloads.block_settle()
+    sc.params["ps_freq"] = 3
+    sc.fluid_vel = np.zeros_like(sc.fluid_pos)
+    sc.fluid_vel[:, 0] = 1.0
+    out = []
+    for graphs in (False, True):
+        c0 = crm.load_scenario(sc, rank=0, world=3)
+        ctxs = [c0] + [crm.load_scenario(sc, rank=r, world=3, stream=c0.stream()) for r in range(1, 3)]
+        for c in ctxs:
+            c.set_graphs(graphs)
+        for _ in range(4):
+            crm.group_step(ctxs, sc.dt, 7)
+        assert [c.count(crm.CRM_GRAPH_REPLAYS) for c in ctxs] == [28 if graphs else 0] * 3
+        out.append(dist.merge_owned([c.get_state() for c in ctxs]))
+    for a, b in zip(*out):
+        assert not np.isnan(a).any()
+        assert np.array_equal(a, b)
