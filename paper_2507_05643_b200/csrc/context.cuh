@@ -88,7 +88,7 @@ struct crm {
   uint32_t *key = nullptr, *arrival = nullptr, *cell_count = nullptr, *cell_start = nullptr;
   uint32_t *tmp_src = nullptr, *tmp_id = nullptr, *cell_of = nullptr, *slot_of_id = nullptr;
   uint16_t* list = nullptr;             // hot-path lists: window offsets, cap per particle
-  uint32_t *nlist = nullptr, *count_all = nullptr;
+  uint32_t* nlist = nullptr;            // stored entries per slot (|P(i)| for fluid; all with store_all)
   uint32_t* list32 = nullptr;           // debug only: global indices, ELL k-major
   long long ntiles = 0, tile_base = 0;
   bool attrs_set = false;

@@ -100,7 +100,7 @@ int commit(crm_t* c) {
   r |= dalloc(c, &c->cell_count, (size_t)c->grid.M + 1); r |= dalloc(c, &c->cell_start, (size_t)c->grid.M + 2);
   r |= dalloc(c, &c->tmp_src, n); r |= dalloc(c, &c->tmp_id, n); r |= dalloc(c, &c->cell_of, n);
   r |= dalloc(c, &c->slot_of_id, (size_t)c->n);
-  r |= dalloc(c, &c->list, n * (size_t)c->cap); r |= dalloc(c, &c->nlist, n); r |= dalloc(c, &c->count_all, n);
+  r |= dalloc(c, &c->list, n * (size_t)c->cap); r |= dalloc(c, &c->nlist, n);
   r |= dalloc(c, &c->d_err, 1);
   r |= dalloc(c, &c->d_mtiles, (size_t)std::max<long long>(num_tiles(c->grid), 1)); r |= dalloc(c, &c->d_mtile_cnt, 1);
   r |= dalloc(c, &c->d_xcount, 8);
@@ -325,7 +325,7 @@ int aalloc(crm_t* c, T** p, size_t n) {
 int alloc_active_arrays(crm_t* c, int64_t cap) {
   const size_t n = (size_t)std::max<int64_t>(cap, 1);
   int r = 0;
-  r |= aalloc(c, &c->list, n * (size_t)c->cap); r |= aalloc(c, &c->nlist, n); r |= aalloc(c, &c->count_all, n);
+  r |= aalloc(c, &c->list, n * (size_t)c->cap); r |= aalloc(c, &c->nlist, n);
   r |= aalloc(c, &c->Pm, n); r |= aalloc(c, &c->Lm, n); r |= aalloc(c, &c->Um, n); r |= aalloc(c, &c->S1m, n);
   r |= aalloc(c, &c->S2m, n);
   if (c->n_moving_markers) {
@@ -399,7 +399,7 @@ void issue_filter(crm_t* c, long long step, int store_all) {
   if (tile_grid(c) == 0) return;
   launch_smem(c, KID_FILTER, k_filter_t, dim3((unsigned)tile_grid(c)), dim3(FILTER_THREADS), sizeof(FilterSmem),
               c->grid, (const uint32_t*)c->cell_start, (const float4*)c->P[y], (const float4*)c->U[y], c->list,
-              c->nlist, c->count_all, (const uint32_t*)c->cell_of, list_shape(c), store_all, c->d_err,
+              c->nlist, (const uint32_t*)c->cell_of, list_shape(c), store_all, c->d_err,
               (const uint32_t*)c->ids[y], step, c->tile_base, tile_list(c), c->d_mtiles, c->d_mtile_cnt,
               c->list_order);
 }
@@ -919,7 +919,7 @@ void crm_destroy(crm_t* c) {
   cudaFree(c->d_tile_list); cudaFree(c->d_tile_cnt); cudaFree(c->d_mtiles); cudaFree(c->d_mtile_cnt);
   cudaFree(c->key); cudaFree(c->arrival); cudaFree(c->cell_count); cudaFree(c->cell_start);
   cudaFree(c->tmp_src); cudaFree(c->tmp_id); cudaFree(c->cell_of); cudaFree(c->slot_of_id);
-  cudaFree(c->list); cudaFree(c->nlist); cudaFree(c->count_all); cudaFree(c->list32);
+  cudaFree(c->list); cudaFree(c->nlist); cudaFree(c->list32);
   for (auto p : c->scan_sums) cudaFree(p);
   for (auto p : c->scan_sums_x) cudaFree(p);
   cudaFree(c->d_bodies); cudaFree(c->d_pose0); cudaFree(c->d_posem);
@@ -1135,7 +1135,7 @@ int crm_pair_count(crm_t* c, int64_t* fluid_pairs) {
   const int n = (int)(c->boxes.empty() ? c->nl : c->n_ae);   // slots that have lists
   if (n > 0)
     launch(c, KID_SLAB, k_pair_count, dim3(blocks(n, 256)), dim3(256), n, (const float4*)c->U[c->cur],
-           (const uint32_t*)c->count_all, d);
+           (const uint32_t*)c->nlist, d);
   unsigned long long h = 0;
   CK(cudaMemcpyAsync(&h, d, 8, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
@@ -1312,7 +1312,7 @@ int crm_debug_structure(crm_t* c, uint32_t* cell_by_id, int64_t* sorted_ids, uin
   if ((r = issue_rebuild_sort(c, c->steps_done))) return r;
   c->ph.build_lists = 1;
   c->lists_valid = true;
-  issue_bce(c, 0, 0.0f, c->steps_done, 0);
+  issue_bce(c, 0, 0.0f, c->steps_done, 1);   // store_all: every list holds all neighbours, |P(i)|
   issue_rates(c, 0, 0.0f, c->steps_done);
   r = read_latch(c);
   if (r) return r;
@@ -1322,7 +1322,7 @@ int crm_debug_structure(crm_t* c, uint32_t* cell_by_id, int64_t* sorted_ids, uin
   std::vector<uint32_t> ids(n), cell(n), cnt(n, 0u);
   CK(cudaMemcpy(ids.data(), c->ids[c->cur], n * 4, cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(cell.data(), c->cell_of, n * 4, cudaMemcpyDeviceToHost));
-  if (nv) CK(cudaMemcpy(cnt.data(), c->count_all, nv * 4, cudaMemcpyDeviceToHost));
+  if (nv) CK(cudaMemcpy(cnt.data(), c->nlist, nv * 4, cudaMemcpyDeviceToHost));
   for (size_t s = 0; s < n; ++s) {
     if (cell_by_id) cell_by_id[ids[s]] = cell[s];
     if (sorted_ids) sorted_ids[s] = ids[s];

@@ -6,7 +6,7 @@
 //               instead of inside the register- and shared-memory-limited pair kernels.  Every
 //               particle of the tile gets its list: fluid particles all neighbours, markers their
 //               fluid neighbours (Adami sums run over fluid only), or all with store_all
-//               (debug export).  count_all = |P(i)| for the structure checks.  The tiles that hold
+//               (debug export; nlist = |P(i)| for the structure checks).  The tiles that hold
 //               markers are appended to `mtiles` for the BCE kernels.
 // Runs only at rebuild steps of Alg. 2 (t mod ps_freq == 0); the tile kernels read the lists.
 // The predicate is rule B2 on the absolute fp32 positions; the candidate order (runs in (da, db)
@@ -296,7 +296,7 @@ __device__ __forceinline__ void gm_store_chunk(FilterSmem& sm, GmState& st, uint
 // the two paths of a divergent warp)
 template <int MODE>
 __device__ __forceinline__ void filter_range_gm(float R2, FilterSmem& sm, uint32_t ob, uint32_t oe, uint32_t self,
-                                                const float4& pi, uint32_t& cnt, GmState& st, uint32_t g0,
+                                                const float4& pi, GmState& st, uint32_t g0,
                                                 ListWriter& w, bool fonly) {
   constexpr bool STORE_BCE = MODE == 0;
   const unsigned long long xi2 = f2_splat(pi.x), yi2 = f2_splat(pi.y), zi2 = f2_splat(pi.z);
@@ -328,7 +328,6 @@ __device__ __forceinline__ void filter_range_gm(float R2, FilterSmem& sm, uint32
     }
     a &= va;
     b &= vb;
-    cnt += __popc(a) + __popc(b);
     if (MODE == 1 || (MODE == 2 && fonly)) {
       a = fa & va;
       b = fb & vb;
@@ -346,7 +345,7 @@ __device__ __forceinline__ void filter_range_gm(float R2, FilterSmem& sm, uint32
 template <bool STAGED, bool STORE_BCE>
 __device__ __forceinline__ void filter_range(float R2, FilterSmem& sm, const float4* __restrict__ P,
                                              const float4* __restrict__ U, uint32_t ob, uint32_t oe, uint32_t self,
-                                             uint32_t gshift, const float4& pi, uint32_t& cnt, int& nw,
+                                             uint32_t gshift, const float4& pi, int& nw,
                                              uint32_t& nent, ListWriter& w) {
   const unsigned long long xi2 = f2_splat(pi.x), yi2 = f2_splat(pi.y), zi2 = f2_splat(pi.z);
   // staged: chunks start on an aligned slot (vector loads); the slots before ob are masked off
@@ -382,7 +381,6 @@ __device__ __forceinline__ void filter_range(float R2, FilterSmem& sm, const flo
     if (base < ob) valid &= ~((1u << (ob - base)) - 1u);   // the aligned chunk's slots before ob
     if (self - base < nc) valid &= ~(1u << (self - base));
     m &= valid;
-    cnt += __popc(m);
     const uint32_t s = STORE_BCE ? m : (mf & valid);
     if (s) {
       if (nw == FMW) {   // this thread's mask slots are full: append what they hold now
@@ -400,7 +398,7 @@ __device__ __forceinline__ void filter_range(float R2, FilterSmem& sm, const flo
 
 // the 9 candidate runs of particle i (window offset self, column q, cell z = cz); returns |P(i)|
 template <bool STAGED, bool STORE_BCE, int MODE = STORE_BCE ? 0 : 1>
-__device__ __forceinline__ uint32_t filter_particle(float R2, FilterSmem& sm, const float4* __restrict__ P,
+__device__ __forceinline__ void filter_particle(float R2, FilterSmem& sm, const float4* __restrict__ P,
                                                     const float4* __restrict__ U, int q, int cz, uint32_t self,
                                                     float4 pi, ListWriter& w, bool gmaj, uint32_t g0,
                                                     bool fonly = false) {
@@ -410,7 +408,6 @@ __device__ __forceinline__ uint32_t filter_particle(float R2, FilterSmem& sm, co
   if (STAGED && gmaj) gm_reset(st);
   // (measured: pruning neighbour cells by their box distance removes ~24 % of the candidates
   //  but costs more in divergence than it saves; the full 27-cell stencil is kept)
-  uint32_t cnt = 0;
 #pragma unroll 1
   for (int da = -1; da <= 1; ++da) {
 #pragma unroll 1
@@ -421,19 +418,18 @@ __device__ __forceinline__ uint32_t filter_particle(float R2, FilterSmem& sm, co
       const uint32_t gshift = sm.run_start[r] - sm.run_base[r];
       // the own run holds i itself: its bit is masked off (j != i, A18)
       const uint32_t sf = (da == 0 && db == 0) ? self : ~0u;
-      if (STAGED && gmaj) filter_range_gm<MODE>(R2, sm, ob, oe, sf, pi, cnt, st, g0, w, fonly);
-      else filter_range<STAGED, STORE_BCE>(R2, sm, P, U, ob, oe, sf, gshift, pi, cnt, nw, nent, w);
+      if (STAGED && gmaj) filter_range_gm<MODE>(R2, sm, ob, oe, sf, pi, st, g0, w, fonly);
+      else filter_range<STAGED, STORE_BCE>(R2, sm, P, U, ob, oe, sf, gshift, pi, nw, nent, w);
     }
   }
   if (STAGED && gmaj) gm_drain(sm, st, g0, w, self << 4, true);
   else drain_masks<STAGED>(sm, nw, nent, w);
-  return cnt;
 }
 
 template <bool STAGED>
 __device__ __forceinline__ int filter_tile(const Grid& g, FilterSmem& sm, const float4* __restrict__ P,
                                             const float4* __restrict__ U, uint16_t* __restrict__ list,
-                                            uint32_t* __restrict__ nlist, uint32_t* __restrict__ count_all,
+                                            uint32_t* __restrict__ nlist,
                                             const uint32_t* __restrict__ cell_of, ListShape ls, int store_all,
                                             ErrLatch* err, const uint32_t* __restrict__ ids, long long step,
                                             bool gmaj) {
@@ -471,15 +467,14 @@ __device__ __forceinline__ int filter_tile(const Grid& g, FilterSmem& sm, const 
     // a divergent warp would run both sweeps; measured k_filter 12.71 -> 12.05 ms on the C5 bed)
     const unsigned am = __activemask();
     const bool any_f = __any_sync(am, fluid_only), all_f = __all_sync(am, fluid_only);
-    uint32_t cnt;
     if (STAGED && gmaj && any_f && !all_f)
-      cnt = filter_particle<STAGED, false, 2>(g.R2, sm, P, U, q, cz, self, pi, w, gmaj, t & 7u, fluid_only);
+      filter_particle<STAGED, false, 2>(g.R2, sm, P, U, q, cz, self, pi, w, gmaj, t & 7u, fluid_only);
+    else if (fluid_only)
+      filter_particle<STAGED, false>(g.R2, sm, P, U, q, cz, self, pi, w, gmaj, t & 7u);
     else
-      cnt = fluid_only ? filter_particle<STAGED, false>(g.R2, sm, P, U, q, cz, self, pi, w, gmaj, t & 7u)
-                       : filter_particle<STAGED, true>(g.R2, sm, P, U, q, cz, self, pi, w, gmaj, t & 7u);
+      filter_particle<STAGED, true>(g.R2, sm, P, U, q, cz, self, pi, w, gmaj, t & 7u);
     w.flush(STAGED ? self << 4 : self);
     nlist[i] = (uint32_t)min(w.k, ls.cap);
-    count_all[i] = cnt;
     if (w.k > ls.cap) latch_error(err, -9 /*CRM_E_CAPACITY*/, (long long)ids[i], step, (long long)w.k);
   }
   return has_marker;
@@ -489,7 +484,7 @@ __device__ __forceinline__ int filter_tile(const Grid& g, FilterSmem& sm, const 
 __global__ void __launch_bounds__(FILTER_THREADS, CRM_FILTER_MINB)
     k_filter_t(Grid g, const uint32_t* __restrict__ cell_start, const float4* __restrict__ P,
                const float4* __restrict__ U, uint16_t* __restrict__ list, uint32_t* __restrict__ nlist,
-               uint32_t* __restrict__ count_all, const uint32_t* __restrict__ cell_of, ListShape ls, int store_all,
+               const uint32_t* __restrict__ cell_of, ListShape ls, int store_all,
                ErrLatch* err, const uint32_t* __restrict__ ids, long long step, long long tile_base,
                const uint32_t* __restrict__ tile_list, uint32_t* __restrict__ mtiles, uint32_t* __restrict__ mcount,
                int order) {
@@ -513,8 +508,8 @@ __global__ void __launch_bounds__(FILTER_THREADS, CRM_FILTER_MINB)
   tile_stage_wait();
   __syncthreads();
   const bool gmaj = order == 1;
-  const int has = sm.staged ? filter_tile<true>(g, sm, P, U, list, nlist, count_all, cell_of, ls, store_all, err, ids, step, gmaj)
-                            : filter_tile<false>(g, sm, P, U, list, nlist, count_all, cell_of, ls, store_all, err, ids, step, gmaj);
+  const int has = sm.staged ? filter_tile<true>(g, sm, P, U, list, nlist, cell_of, ls, store_all, err, ids, step, gmaj)
+                            : filter_tile<false>(g, sm, P, U, list, nlist, cell_of, ls, store_all, err, ids, step, gmaj);
   // the tiles holding markers: the BCE kernels run over these only (any order: tiles are independent)
   // with the rows z0 + zl .. z0 + zh (0 <= zl <= zh < TZ) that hold them in bits 28-31 (tiles < 2^28)
   if (__syncthreads_or(has) && threadIdx.x == 0) {

@@ -336,13 +336,13 @@ __global__ void k_clear_slots(int n, const uint32_t* __restrict__ ids, uint32_t*
 }
 
 // sum of |P(i)| over owned fluid particles (the directed pairs of the rates loops)
-__global__ void k_pair_count(int n, const float4* __restrict__ U, const uint32_t* __restrict__ count_all,
+__global__ void k_pair_count(int n, const float4* __restrict__ U, const uint32_t* __restrict__ nlist,
                              unsigned long long* __restrict__ out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long v = 0;
   if (i < n) {
     const uint32_t t = tag_of(U[i].w);
-    if (!tag_is_bce(t) && !tag_ghost(t)) v = count_all[i];
+    if (!tag_is_bce(t) && !tag_ghost(t)) v = nlist[i];   // a fluid list holds all of P(i)
   }
   for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
   if ((threadIdx.x & 31) == 0 && v) atomicAdd(out, v);
