@@ -244,6 +244,10 @@ __device__ __forceinline__ void pair_loop(PairAcc& A, const Phys& ph, const Tile
     const uint4 v = vn;
     vn = vn2;
     vn2 = seg[(size_t)min(c + 2, nch - 1) * ls_stride];
+    // chunk c + 4 to L2 (no register): the LDG two chunks ahead then hits L2 (measured: k_rates_B
+    // 11.14 -> 11.05 ms; 3 or 5 ahead the same)
+    if (c + 4 < nch)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(seg + (size_t)(c + 4) * ls_stride));
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       float4 pj, uj, s1;
@@ -291,7 +295,9 @@ __device__ __forceinline__ void rates_tile(const Phys& ph, float dt, TileSmem& s
     }
     const float4 pi = rel_pos_q(first ? pre.p : P[i], tag, sm);
     const uint32_t nl = first ? pre.nl : nlist[i];
-    const uint4 c0 = first ? pre.c0 : reinterpret_cast<const uint4*>(list)[i];
+    // stage A: chunk 0 was prefetched to L2 with the others (held in a register across the prologue
+    // it was spilled, and the spill waited for the load: k_rates_A 11.49 -> 11.01 ms); stage B keeps it
+    const uint4 c0 = (STAGE == 1 && first) ? pre.c0 : reinterpret_cast<const uint4*>(list)[i];
     PairAcc A;
 #pragma unroll
     for (int k = 0; k < 9; ++k) A.L[k] = 0.f;
@@ -433,14 +439,15 @@ __global__ void TILE_BOUNDS
 #ifndef CRM_LISTPF
 #define CRM_LISTPF 12
 #endif
+
   // stage A reads lists the filter has just written (the filter's 6 GB of lists have left L2): chunks
-  // 1 .. CRM_LISTPF-1 of each thread's first particle are prefetched to L2 with the window copy
+  // 0 .. CRM_LISTPF-1 of each thread's first particle are prefetched to L2 with the window copy
   // (measured: k_rates_A 12.28 -> 11.79 ms with 11 chunks; 4: 12.11, 16: 11.85; stage B gains nothing)
   if (STAGE == 0 && CRM_LISTPF > 1 && threadIdx.x < n_i) {
     int q;
     const uint32_t i0 = tile_particle(sm, threadIdx.x, q);
 #pragma unroll
-    for (int cc = 1; cc < CRM_LISTPF; ++cc)
+    for (int cc = 0; cc < CRM_LISTPF; ++cc)
       asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const uint4*>(list) + (size_t)cc * ls.stride + i0));
   }
   Prefetch pre;
@@ -451,7 +458,7 @@ __global__ void TILE_BOUNDS
     pre.p = P[pre.i];
     pre.l = L[pre.i];   // (for the epilogue's integrator: requested early, its latency hides in the prologue)
     pre.nl = nlist[pre.i];
-    pre.c0 = reinterpret_cast<const uint4*>(list)[pre.i];
+    if (STAGE == 1) pre.c0 = reinterpret_cast<const uint4*>(list)[pre.i];
   }
   // marker bookkeeping that needs no window; detect whether the tile has pair work
   int work = 0;
