@@ -178,7 +178,7 @@ struct PairAcc {
 // latency overlaps the staging and the relativize pass instead of following them
 struct Prefetch {
   uint32_t i, nl;
-  float4 u, p, l;
+  float4 u, p;
   uint4 c0;
 };
 
@@ -319,7 +319,7 @@ __device__ __forceinline__ void rates_tile(const Phys& ph, float dt, TileSmem& s
     pair_loop<KER, STAGED>(A, ph, sm, P, L, U, S1, S2, list, i, ls, nl, c0, pi, ui, true, false);
     // own state for the epilogue, (re)loaded after the loop to keep registers free inside it
     const float4 phi = first ? pre.p : P[i];
-    const float4 pli = first ? pre.l : L[i];
+    const float4 pli = L[i];   // (held across the prologue it was spilled: k_rates_A 11.02 -> 10.72 ms)
     const float4 si1 = S1[i];
     const float2 si2 = S2[i];
     const float rinv_i = 1.0f / pi.w;
@@ -456,7 +456,6 @@ __global__ void TILE_BOUNDS
     pre.i = tile_particle(sm, threadIdx.x, q);
     pre.u = U[pre.i];
     pre.p = P[pre.i];
-    pre.l = L[pre.i];   // (for the epilogue's integrator: requested early, its latency hides in the prologue)
     pre.nl = nlist[pre.i];
     if (STAGE == 1) pre.c0 = reinterpret_cast<const uint4*>(list)[pre.i];
   }
