@@ -198,11 +198,6 @@ __device__ __forceinline__ void bytes4x4(uint32_t& r0, uint32_t& r1, uint32_t& r
 __device__ __forceinline__ void gm_drain(FilterSmem& sm, GmState& st, uint32_t g0, ListWriter& w, uint32_t fill,
                                          bool final) {
   const uint32_t t = threadIdx.x;
-  if (st.nch & 1) {   // a half-filled byte position
-    const int p = st.nch >> 1;
-    sm.mw[2 * p][t] = st.A;
-    sm.mw[2 * p + 1][t] = st.B;
-  }
   const int nb = (st.nch + 1) >> 1;   // byte positions
   uint32_t NZ = 0;                    // bit 4 g + wd: group g's word wd holds entries
   for (int wd = 0; 4 * wd < nb; ++wd) {
@@ -282,13 +277,14 @@ __device__ __forceinline__ void gm_store_chunk(FilterSmem& sm, GmState& st, uint
   const uint32_t t = threadIdx.x;
   sm.wb[st.nch][t] = (uint16_t)(base << 4);   // staged windows: base < 4096
   st.nent += __popc(a) + __popc(b);
-  if (st.nch & 1) {
+  {   // branch-free: the open byte position is stored with every chunk (the odd one completes it;
+      // measured against a store per completed pair: k_filter 11.75 -> 11.45 ms)
+    const bool odd = (st.nch & 1) != 0;
     const int p = st.nch >> 1;
-    sm.mw[2 * p][t] = st.A | (a << 4);
-    sm.mw[2 * p + 1][t] = st.B | (b << 4);
-  } else {
-    st.A = a;
-    st.B = b;
+    st.A = odd ? (st.A | (a << 4)) : a;
+    st.B = odd ? (st.B | (b << 4)) : b;
+    sm.mw[2 * p][t] = st.A;
+    sm.mw[2 * p + 1][t] = st.B;
   }
   ++st.nch;
 }
