@@ -331,7 +331,7 @@ __device__ __forceinline__ void filter_range_gm(float R2, FilterSmem& sm, uint32
       a = fa & va;
       b = fb & vb;
     }
-    if (a | b) gm_store_chunk(sm, st, a, b, base, g0, w);
+    gm_store_chunk(sm, st, a, b, base, g0, w);   // empty chunks too (no divergent store: -0.12 ms)
   }
 }
 
