@@ -376,7 +376,7 @@ void issue_bce_k(crm_t* c, int stage, long long step) {
   const int dbg = c->dbg_on ? 1 : 0;
   if (tile_grid(c) == 0) return;
   // persistent: two resident CTAs per SM walk the marker tiles listed by k_filter_t
-  const dim3 tg((unsigned)std::min<long long>(tile_grid(c), 2LL * c->num_sms)), tb(TILE_THREADS);
+  const dim3 tg((unsigned)std::min<long long>(tile_grid(c), 2LL * c->num_sms)), tb(BCE_THREADS);
   const size_t sm = sizeof(TileSmem);
   const int y = c->cur;
   if (stage == 0)

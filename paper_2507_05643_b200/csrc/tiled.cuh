@@ -135,7 +135,7 @@ __device__ __forceinline__ void bce_tile(const Phys& ph, TileSmem& sm, const flo
 // of fluid only has nothing to extrapolate, and a CTA per tile of the whole grid would cost more
 // in setup than the markers' work.
 template <int STAGE, int KER>
-__global__ void TILE_BOUNDS
+__global__ void BCE_BOUNDS
     k_bce_t(Grid g, Phys ph, const uint32_t* __restrict__ cell_start, const float4* __restrict__ P,
             const float4* __restrict__ L, float4* __restrict__ U, float4* __restrict__ S1, float2* __restrict__ S2,
             const uint16_t* __restrict__ list, const uint32_t* __restrict__ nlist, const Pose* __restrict__ pose,

@@ -29,6 +29,13 @@ constexpr int TILE_THREADS = CRM_TILE_THREADS;
 // 288 threads a quarter of the tiles ran a second round for a few particles and took twice as long
 // (measured: 288 -> 384 threads, rates kernels -14 %; 448 threads spill and are slower)
 #define TILE_BOUNDS __launch_bounds__(TILE_THREADS, 2)
+#ifndef CRM_BCE_THREADS
+#define CRM_BCE_THREADS 320
+#endif
+// the BCE kernels' CTAs (2 per SM: the same window); 320 threads leave 96 registers and no spills
+// (measured: k_bce_A/B 0.75 -> 0.70 ms against 384; 256: 0.73, 192: 0.90)
+constexpr int BCE_THREADS = CRM_BCE_THREADS;
+#define BCE_BOUNDS __launch_bounds__(BCE_THREADS, 2)
 #ifndef CRM_WMAX
 #define CRM_WMAX 1968
 #endif
