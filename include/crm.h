@@ -49,8 +49,9 @@ extern "C" {
 #define CRM_E_STATE       -5   /* crm_add_* after the first step, debug data not available */
 #define CRM_E_OOM         -6   /* device or host allocation failed */
 #define CRM_E_CUDA        -7   /* CUDA runtime error, or no sm_100 device */
-#define CRM_E_COMM        -8   /* NCCL error (multi-GPU) */
-#define CRM_E_CAPACITY    -9   /* a particle has more neighbours than crm_kernel_t.max_neighbors */
+#define CRM_E_COMM        -8   /* NCCL error, or a received halo plane whose count differs from the ghost plane's (multi-GPU) */
+#define CRM_E_CAPACITY    -9   /* a particle has more neighbours than crm_kernel_t.max_neighbors, or (slabs) the
+                                   fixed-capacity emigrant / boundary-plane / slab buffers overflowed */
 
 #define CRM_KERNEL_CUBIC      0   /* Monaghan (1985) M4 cubic spline, support 2h (A1) */
 #define CRM_KERNEL_WENDLAND   1   /* quintic Wendland (Wendland 1995, A28): a (1 - q/2)^4 (2q + 1), support 2h */
@@ -139,7 +140,10 @@ int  crm_add_bce(crm_t* ctx, int32_t body, int64_t n, const double* pos_world, i
  * which it occurred in crm_last_error (a device step counter, also inside replayed CUDA graphs).
  * The steps after the failing one compute nothing: the state is the one the failing step left,
  * and the call returns after nsteps launches with that first error.  With world > 1 and an NCCL id, every rank calls crm_step with the same
- * arguments; ghost planes are exchanged with NCCL point-to-point transfers (CRM_E_COMM). */
+ * arguments; ghost planes are exchanged with NCCL point-to-point transfers (CRM_E_COMM).  A step
+ * reads nothing back on the host (slabs too: device-resident counts, fixed-size transfers), so
+ * with graphs on (the default, crm_set_graphs) each step after the first of its kind is replayed
+ * from a captured CUDA graph; crm_count(ctx, CRM_GRAPH_REPLAYS) counts the replayed steps. */
 int  crm_step(crm_t* ctx, double dt, int64_t nsteps);
 
 /* ---- multi-GPU slab decomposition along x ----
@@ -152,7 +156,8 @@ int  crm_step(crm_t* ctx, double dt, int64_t nsteps);
  * exchanged and added in rank order, so every rank integrates the same body state. */
 /* Step `world` contexts of ranks 0..world-1 living in one process on one device and stream
  * (nccl_id NULL): exchanges become device copies ("loopback"); used to test the decomposition
- * on one GPU.  Owned particles follow bit-identical trajectories to a one-context run. */
+ * on one GPU.  Owned particles follow bit-identical trajectories to a one-context run.  The ranks'
+ * steps (all phases and copies) are captured together as one CUDA graph, kept by ctxs[0]. */
 int  crm_group_step(crm_t** ctxs, int world, double dt, int64_t nsteps);
 /* 128-byte ncclUniqueId for crm_dist_t.nccl_id (call on one rank, broadcast to the others). */
 int  crm_nccl_unique_id(void* out128);
