@@ -676,8 +676,17 @@ int read_latch(crm_t* c) {
       snprintf(buf, sizeof buf, "particle id %lld outside the grid box at step %lld", e.id, e.step);
     else if (e.code == CRM_E_NONFINITE)
       snprintf(buf, sizeof buf, "non-finite state at particle id %lld after step %lld", e.id, e.step);
+    else if (e.code == CRM_E_CAPACITY && e.aux == 2)
+      snprintf(buf, sizeof buf, "slab pack buffer full (emigrants or boundary plane) at particle id %lld, step %lld",
+               e.id, e.step);
+    else if (e.code == CRM_E_CAPACITY && e.aux == 3)
+      snprintf(buf, sizeof buf, "slab capacity exceeded by the immigrants and ghosts received at step %lld", e.step);
+    else if (e.code == CRM_E_CAPACITY && e.aux == 4)
+      snprintf(buf, sizeof buf, "slab boundary plane larger than the halo buffer at step %lld", e.step);
     else if (e.code == CRM_E_CAPACITY && e.id < 0)
       snprintf(buf, sizeof buf, "tile window of %lld particles exceeds 16-bit offsets at step %lld", e.aux, e.step);
+    else if (e.code == CRM_E_COMM)
+      snprintf(buf, sizeof buf, "halo of %lld particles does not match the ghost plane at step %lld", e.aux, e.step);
     else if (e.code == CRM_E_CAPACITY)
       snprintf(buf, sizeof buf, "particle id %lld has %lld neighbours > max_neighbors %d at step %lld", e.id, e.aux,
                c->cap, e.step);
