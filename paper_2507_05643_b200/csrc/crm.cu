@@ -115,6 +115,7 @@ int commit(crm_t* c) {
     //  may densify by a quarter before CRM_E_CAPACITY is latched)
     c->pk.cap_e = (uint32_t)(maxp / 2 + 1024);
     c->pk.cap_g = (uint32_t)(maxp + maxp / 4 + 1024);
+    if (const char* v = std::getenv("CRM_SLAB_CAP_G")) c->pk.cap_g = (uint32_t)std::max(1, std::atoi(v));   // (tests)
     const size_t pc = (size_t)c->pk.cap_e + c->pk.cap_g;
     for (int d = 0; d < 2; ++d) {
       r |= dalloc(c, &c->pk.P[d], pc); r |= dalloc(c, &c->pk.L[d], pc); r |= dalloc(c, &c->pk.U[d], pc);

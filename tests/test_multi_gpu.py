@@ -118,3 +118,16 @@ def test_slab_step_graph_replay_equals_eager(crm):
     for a, b in zip(*out):
         assert not np.isnan(a).any()
         assert np.array_equal(a, b)
+
+
+def test_slab_halo_overflow_is_latched(crm, monkeypatch):
+    """A boundary plane larger than the fixed-capacity halo buffer (forced small here) is a
+    CRM_E_CAPACITY error latched on the device and reported by the step, with its message."""
+    monkeypatch.setenv("CRM_SLAB_CAP_G", "16")
+    sc = workloads.block_settle()
+    c0 = crm.load_scenario(sc, rank=0, world=2)
+    ctxs = [c0, crm.load_scenario(sc, rank=1, world=2, stream=c0.stream())]
+    with pytest.raises(crm.CrmError) as ei:
+        crm.group_step(ctxs, sc.dt, 3)
+    assert ei.value.code == -9
+    assert "halo buffer" in str(ei.value) or "pack buffer" in str(ei.value)
