@@ -282,7 +282,7 @@ def main():
     ap.add_argument("--config", default="bed32M")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=2)
-    ap.add_argument("--repeats", type=int, default=3, help="timed K-step regions; the median is reported")
+    ap.add_argument("--repeats", type=int, default=5, help="timed K-step regions; the median is reported (SURVEY D6: median of 5)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-next", action="store_true", help="skip the ps_freq = 10 (Alg. 2) measurement")
