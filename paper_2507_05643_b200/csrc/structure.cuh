@@ -147,22 +147,6 @@ __global__ void k_scan_add(uint32_t* __restrict__ out, const uint32_t* __restric
 __global__ void k_copy_u32(uint32_t* dst, const uint32_t* src) { *dst = *src; }
 
 // ---------------------------------------------------------------------------------------
-// multi-GPU helpers: OR bits into the tags of slots [b, e); check that particles of slots [b, e)
-// lie in x-plane `plane` (immigrants may cross at most one cell plane per step)
-__global__ void k_or_tag(float4* __restrict__ U, uint32_t b, uint32_t e, uint32_t bits) {
-  const uint32_t s = b + blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= e) return;
-  U[s].w = __uint_as_float(tag_of(U[s].w) | bits);
-}
-
-__global__ void k_check_plane(const float4* __restrict__ P, const uint32_t* __restrict__ ids, uint32_t b, uint32_t e,
-                              Grid g, int plane, ErrLatch* err, long long step) {
-  const uint32_t s = b + blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= e) return;
-  const float f = b1_floor(P[s].x, g.lo[0], g.s);
-  if (!(f == (float)plane)) latch_error(err, -2 /*CRM_E_DOMAIN*/, (long long)ids[s], step, 1);
-}
-
 // Slab rebuild, one pass over the local particles (replaces a first sort): last step's ghosts are
 // marked dropped; an owned particle now in the neighbour's first plane is an emigrant — its state goes
 // to that neighbour (segment E of the pack buffer of that side) and this rank keeps it as a ghost;
