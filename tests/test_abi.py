@@ -127,3 +127,15 @@ def test_active_box_validation(lib):
     c.set_active_box(0, (0.1, 0.1, 0.1))
     c.set_active_policy(0.01)
     c.close()
+
+
+def test_binding_constants_match_the_header():
+    """The Python binding's CRM_* constants are the header's #defines (marshalling only: one source)."""
+    from paper_2507_05643_b200 import crm
+    src = open(os.path.join(ROOT, "include", "crm.h")).read()
+    defs = {k: int(v) for k, v in re.findall(r"#define\s+(CRM_[A-Z0-9_]+)\s+(-?\d+)\b", src)}
+    shared = [k for k in dir(crm) if k.startswith("CRM_") and isinstance(getattr(crm, k), int)]
+    assert {"CRM_OWNED", "CRM_GRAPH_REPLAYS", "CRM_E_CAPACITY"} <= set(shared)
+    for k in shared:
+        assert k in defs, k
+        assert getattr(crm, k) == defs[k], k
