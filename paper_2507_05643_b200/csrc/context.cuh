@@ -1,6 +1,7 @@
 // context.cuh — the opaque crm_t of include/crm.h and host-side helpers (launch, alloc, errors).
 #pragma once
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -17,6 +18,15 @@
 #include "tiled.cuh"
 #include "filter.cuh"
 #include "active.cuh"
+
+// NVTX range of the host-side launch sequence (an nsys / ncu timeline shows the step's phases; a
+// no-op without a tool attached; not recorded by replayed graphs, whose kernels show by name)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 using namespace crmk;
 

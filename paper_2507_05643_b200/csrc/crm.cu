@@ -480,15 +480,21 @@ int issue_step(crm_t* c, float dt, long long step) {
   // Alg. 2: rebuild (sort + filtered lists) when t mod ps_freq == 0; otherwise the particles keep
   // their slots and the stored lists are reused without a distance re-check (A17)
   const bool rebuild = !c->lists_valid || (step % c->ps_freq) == 0;
+  NvtxRange step_range(rebuild ? "crm step (rebuild)" : "crm step (reuse lists)");
   launch(c, KID_STEP, k_step_begin, dim3(1), dim3(1), c->d_err, step);
   if (rebuild) {
+    NvtxRange r_sort("sort (A1-A3)");
     const int r = issue_rebuild_sort(c, step);
     if (r) return r;
   }
   c->ph.build_lists = rebuild ? 1 : 0;
   c->lists_valid = true;
-  issue_bce(c, 0, dt, step, 0);
-  issue_rates(c, 0, dt, step);
+  {
+    NvtxRange r_a("filter + BCE + rates, stage A (A4-A7)");
+    issue_bce(c, 0, dt, step, 0);
+    issue_rates(c, 0, dt, step);
+  }
+  NvtxRange r_b("BCE + rates + return map, stage B (A5-A9)");
   const int y = c->cur;
   if (c->n_moving_markers)
     launch(c, KID_MARKERS, k_markers_place, dim3(blocks(c->n_moving_markers, 128)), dim3(128), c->n_moving_markers,
@@ -1085,6 +1091,7 @@ int crm_step(crm_t* c, double dt, int64_t nsteps) {
   if (!c) return CRM_E_INVALID;
   if (!(dt > 0) || nsteps < 0) return fail(c, CRM_E_INVALID, "dt must be > 0 and nsteps >= 0");
   if (c->slab && !c->has_nccl_id) return fail(c, CRM_E_STATE, "in-process slab contexts step with crm_group_step");
+  NvtxRange range("crm_step");
   int r = begin_steps(c, dt);
   if (r) return r;
   if (nsteps == 0) return CRM_OK;
@@ -1102,6 +1109,7 @@ int crm_step(crm_t* c, double dt, int64_t nsteps) {
 
 int crm_group_step(crm_t** cs, int world, double dt, int64_t nsteps) {
   if (!cs || world < 1) return CRM_E_INVALID;
+  NvtxRange range("crm_group_step");
   for (int a = 0; a < world; ++a) {
     if (!cs[a] || cs[a]->world != world || cs[a]->rank != a || cs[a]->has_nccl_id)
       return fail(cs[a], CRM_E_INVALID, "crm_group_step: contexts must be ranks 0..world-1 without an NCCL id");

@@ -227,6 +227,10 @@ void issue_body_finish(crm_t* c);
 // so a slab step is one fixed launch sequence per (buffer parity, rebuild) and is replayed from a
 // CUDA graph (run_slab_step / crm_group_step).
 int slab_phase(crm_t* c, int k, float dt, long long step) {
+  static const char* kNames[10] = {"slab P0 pack", "slab P1 append", "slab P2", "slab P3 reuse halo",
+                                   "slab P4 sort + BCE(y_n)", "slab P5 rates A boundary", "slab P6 rates A interior",
+                                   "slab P7 BCE(y_mid)", "slab P8 rates B", "slab P9 bodies"};
+  NvtxRange range(kNames[k < 10 ? k : 9]);
   switch (k) {
     case 0: {   // rebuild: one pass packs emigrants and boundary planes per side (no sort here)
       // Alg. 2: between rebuilds the slots, ghost sets and lists stay; only values move (phase 3)
