@@ -2,20 +2,25 @@
 //
 // Each rank owns the cell planes [x_lo, x_hi) (boundaries from a prefix sum of per-plane particle
 // counts, aligned to the tile width) and keeps one ghost plane (one 2h cell) on each interior
-// face.  With the B3 cell order a plane is one contiguous index range of the sorted state, so
-// every exchange is a handful of contiguous slices.  Per step:
+// face.  With the B3 cell order a plane is one contiguous index range of the sorted state.  No
+// phase reads the device on the host: the local count lives in d_slab[0], plane ranges are read
+// from cellStart inside the kernels, and every transfer has a fixed size.  Per step:
 //   P0  one pass over the local particles (k_slab_pack): last step's ghosts dropped; owned particles
 //       now in a neighbour's first plane packed as emigrants (kept here as ghosts); owned particles of
-//       the first / last plane packed as the neighbours' ghost planes;      E0  counts
-//   P1  E1  payloads (id + 72-B state), appended: immigrants, then ghosts
-//   P2  immigrants checked to sit in the boundary plane, received ghosts flagged
+//       the first / last plane packed as the neighbours' ghost planes;
+//       E0  the counts and the whole pack buffers (fixed capacity) to both neighbours
+//   P1  received immigrants and ghosts appended by count (k_slab_counts, k_slab_append: immigrants
+//       checked to sit in the boundary plane, ghosts flagged)
 //   P4  the one sort of the step (ghosts in, emigrants and old ghosts out), BCE at y_n on owned tiles
-//   E4  boundary planes (markers now extrapolated) -> ghosts
+//   E4  boundary planes (markers now extrapolated) packed and sent (k_halo_pack), unpacked into the
+//       ghost planes at the start of P5 (k_halo_unpack)
 //   P5  rates + half step, boundary tile columns     E5  y_mid boundary planes -> ghosts
 //   P6  rates + half step, interior columns (overlaps E5 on the NCCL transport)
 //   P7  BCE extrapolation at y_mid                   E7  y_mid boundary planes -> ghosts
 //   P8  rates + full step + return map on owned tiles
-// (Alg. 2 reuse steps skip P0-P2 and the sort and refresh the ghost values in P3.)
+// (Alg. 2 reuse steps skip P0-P1 and the sort and refresh the ghost values of y_n in P3/P4.)  The
+// launch sequence is fixed per (buffer parity, rebuild), so the step is captured once as a CUDA
+// graph and replayed (crm.cu run_slab_step, group_slab_step).
 // Neighbour iteration order is the global (cell, id) order restricted to the local planes, so
 // owned particles follow bit-identical trajectories to a one-GPU run.
 // Transports: NCCL point-to-point (ncclSend/ncclRecv in a group, on the context stream; NCCL is
