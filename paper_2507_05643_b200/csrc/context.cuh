@@ -130,6 +130,7 @@ struct crm {
   cudaGraphExec_t ggroup[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};   // rank 0 of an in-process slab group
   std::vector<crm_t*> gmembers;         // the contexts the group graphs were captured with
   bool slab_graph_off = false;
+  int slab_eager_steps = 0;             // NCCL slab steps run eagerly before the first capture
   int64_t graph_replays = 0;            // steps replayed from a captured graph (crm_count CRM_GRAPH_REPLAYS)          // a slab-step capture failed once: eager launches from then on
   int ps_freq = 1;                      // Alg. 2: lists rebuilt when step % ps_freq == 0
   bool lists_valid = false;             // the stored lists/sort match the current slots

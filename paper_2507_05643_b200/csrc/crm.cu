@@ -561,6 +561,12 @@ int slab_step_eager(crm_t* c, float dt, long long step) {
 }
 int run_slab_step(crm_t* c, float dt, long long step) {
   const bool rebuild = !c->lists_valid || (step % c->ps_freq) == 0;
+  // the first steps run eagerly: NCCL connects its point-to-point channels lazily, at the first
+  // transfer to a peer, and that setup (allocations, proxy handshakes) is not a stream operation
+  if (c->slab_eager_steps < 2) {
+    ++c->slab_eager_steps;
+    return slab_step_eager(c, dt, step);
+  }
   if (!c->graphs || c->prof || c->dbg_on || c->slab_graph_off) return slab_step_eager(c, dt, step);
   const int p = c->cur, q = rebuild ? 1 : 0;
   if (!c->gexec[p][q] || c->gdt[p][q] != c->dt_d) {
