@@ -143,7 +143,8 @@ int  crm_add_bce(crm_t* ctx, int32_t body, int64_t n, const double* pos_world, i
  * arguments; ghost planes are exchanged with NCCL point-to-point transfers (CRM_E_COMM).  A step
  * reads nothing back on the host (slabs too: device-resident counts, fixed-size transfers), so
  * with graphs on (the default, crm_set_graphs) each step after the first of its kind is replayed
- * from a captured CUDA graph; crm_count(ctx, CRM_GRAPH_REPLAYS) counts the replayed steps. */
+ * from a captured CUDA graph (slab contexts over NCCL: captured from the third step on, after NCCL
+ * has connected its channels); crm_count(ctx, CRM_GRAPH_REPLAYS) counts the replayed steps. */
 int  crm_step(crm_t* ctx, double dt, int64_t nsteps);
 
 /* ---- multi-GPU slab decomposition along x ----
